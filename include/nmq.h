@@ -1,0 +1,166 @@
+/*
+ * nmq.h — C ABI of the B200 (sm_100a) neural-material query library
+ * (libnmq.so).  This is the drop-in boundary for the query hot path of the
+ * reference `neuralmat` package (arXiv 2305.02678 "Real-Time Neural
+ * Appearance Models").  Every entry point below replaces one reference
+ * function; the reference file:line is cited on each (paths relative to
+ * /root/reference/pkg/src/neuralmat).
+ *
+ * Conventions
+ *  - All array arguments of the query entry points are DEVICE pointers on the
+ *    material's device, fp32 (or int32), C-contiguous, batch-first:
+ *    uv (n,2), lod (n,) or scalar, u_rr (n,), wi/wo (n,3), u3 (n,3),
+ *    z (n,8), params9 (n,9), rgb/albedo/ws (n,3), pdf (n,), level (n,).
+ *  - `stream` is a cudaStream_t passed as void*.  Launches are asynchronous
+ *    and never allocate; many streams may launch on one material at once.
+ *  - Optional outputs may be NULL.  `lod_stride` is 1 for a per-query array
+ *    and 0 to broadcast lod[0] (the reference's scalar level, latent.py:91).
+ *  - Return value: 0 = ok, < 0 = error; nm_last_error() returns a
+ *    thread-local message for the last failing call on this thread.
+ *  - The material handle is immutable after creation.
+ *
+ * Parameter block `params9` (the renderer's per-vertex cache,
+ * render.py:370-372): wd, ws, mu_d.x, mu_d.y, alpha.x, alpha.y, rho,
+ * mu_s.x, mu_s.y with the alpha floor and rho clamp already applied
+ * (proxy.py:42-50).
+ */
+#ifndef NMQ_H
+#define NMQ_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NMQ_VERSION 1
+
+enum nm_status {
+  NM_OK = 0,
+  NM_ERR_INVALID = -1,  /* bad argument / shape (reference raises ValueError) */
+  NM_ERR_CUDA = -2,     /* CUDA runtime failure */
+  NM_ERR_UNSUPPORTED = -3 /* architecture outside what the kernels implement */
+};
+
+enum nm_act { NM_ACT_LINEAR = 0, NM_ACT_LEAKY = 1 }; /* mlp.py:22 _ACT_CODES */
+
+enum nm_multi_mode { NM_MULTI_DIVERGENT = 0, NM_MULTI_BINNED = 1 };
+
+/* One quantized network exactly as the reference holds it
+ * (QuantizedMlp, mlp.py:165-233): per layer, per output neuron,
+ * [w_row(fan_in) ..., bias] as IEEE fp16 bits, layers back to back. */
+typedef struct nm_net_desc {
+  int32_t n_layers;
+  const int32_t* fan_in;  /* [n_layers] */
+  const int32_t* fan_out; /* [n_layers] */
+  const int32_t* act;     /* [n_layers] nm_act */
+  const uint16_t* packed; /* fp16 bits, host memory */
+} nm_net_desc;
+
+/* Everything NeuralMaterial.half() produces (neural.py:147-161). */
+typedef struct nm_material_desc {
+  int32_t channels;          /* latent channels; must be 8 (latent.py:17) */
+  int32_t use_frames;        /* NeuralMaterialConfig.use_frames */
+  int32_t n_frames;          /* learned shading frames (neural.py:30) */
+  int32_t albedo_head;       /* BRDF decoder emits 6 outputs */
+  int32_t sampler_isotropic; /* sampler emits 2 outputs (neural.py:319) */
+  /* A network with n_layers == 0 is absent; a material with no BRDF and no
+   * sampler network is latent-only (nm_fetch works, the decoders fail). */
+  nm_net_desc frame;         /* ignored when use_frames == 0 */
+  nm_net_desc brdf;
+  nm_net_desc sampler;
+  int32_t width, height;     /* level-0 latent resolution */
+  int32_t n_levels;          /* must equal the max(1, w//2) chain length */
+  const void* latent;        /* levels back to back, (H,W,C) each: fp16 bits,
+                                or fp32 when latent_fp32 = 1 */
+  int32_t latent_fp32;       /* texels are 8 x fp32 (32 B) instead of 8 x fp16 */
+  int32_t latent_on_device;  /* 1: `latent` is a device pointer on `device` */
+} nm_material_desc;
+
+typedef struct nm_material nm_material;
+
+typedef struct nm_material_info {
+  int32_t device;
+  int32_t n_levels;
+  int64_t latent_texels;     /* texels over all levels */
+  int64_t latent_bytes;
+  int32_t weight_bytes;      /* packed MMA-layout weights staged per CTA */
+  int32_t brdf_width;        /* padded max hidden width of the BRDF decoder */
+  int32_t sampler_width;
+} nm_material_info;
+
+/* --- material lifetime (replaces NeuralMaterial.half() caching,
+ *     neural.py:147-161, and load-time upload) --------------------------- */
+int nm_material_create(const nm_material_desc* desc, int device, nm_material** out);
+int nm_material_destroy(nm_material* mat);
+int nm_material_info_get(const nm_material* mat, nm_material_info* info);
+/* level table: w, h per level and texel offset of each level (n_levels each) */
+int nm_material_levels(const nm_material* mat, int32_t* w, int32_t* h, int64_t* offset);
+/* device pointer to the fp16 texels (read-only; for tests / LoD tooling) */
+const void* nm_material_latent_ptr(const nm_material* mat);
+
+/* --- latent fetch: LatentPyramid.fetch (latent.py:84-98) with
+ *     choose_level (:76-82) and _taps (:56-74).  taps_out (n,4,2) int32
+ *     (x,y) and wts_out (n,4) are debug outputs mirroring _taps. --------- */
+int nm_fetch(const nm_material* mat, int64_t n, const float* uv, const float* lod,
+             int32_t lod_stride, const float* u_rr, float* z_out, int32_t* level_out,
+             int32_t* taps_out, float* wts_out, void* stream);
+
+/* --- eval_material (neural.py:303-309): fetch + frames + BRDF decoder +
+ *     brdf_output + horizon mask, fused (the coherent eval kernel). ------- */
+int nm_eval(const nm_material* mat, int64_t n, const float* uv, const float* lod,
+            int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+            float* rgb_out, float* albedo_out, int32_t* level_out, void* stream);
+
+/* --- eval_brdf (neural.py:273-300), fp16 path, from given latent codes -- */
+int nm_eval_z(const nm_material* mat, int64_t n, const float* z, const float* wi,
+              const float* wo, float* rgb_out, float* albedo_out, void* stream);
+
+/* --- infer_proxy (neural.py:353-362) + proxy_from_raw (:317-331) -------- */
+int nm_infer_proxy(const nm_material* mat, int64_t n, const float* z, const float* wi,
+                   float* params9_out, void* stream);
+
+/* --- proxy.sample (proxy.py:168-180) and proxy.pdf (proxy.py:129-135) on
+ *     a params9 block (no material needed). ------------------------------ */
+int nm_sample(int64_t n, const float* params9, const float* wi, const float* u3,
+              float* wo_out, void* stream);
+int nm_pdf(int64_t n, const float* params9, const float* wi, const float* wo, float* pdf_out,
+           void* stream);
+
+/* --- fused sampling path: fetch + sampler decoder + proxy + sample + pdf of
+ *     the sampled direction (render.py:368-372 + 401-402). --------------- */
+int nm_sample_pdf(const nm_material* mat, int64_t n, const float* uv, const float* lod,
+                  int32_t lod_stride, const float* u_rr, const float* wi, const float* u3,
+                  float* ws_out, float* pdf_out, float* params9_out, int32_t* level_out,
+                  void* stream);
+
+/* --- one full query: one fetch feeding eval(wi, wo) and the sampler;
+ *     ws = sample(u3), pdf(ws). ------------------------------------------ */
+int nm_query(const nm_material* mat, int64_t n, const float* uv, const float* lod,
+             int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+             const float* u3, float* rgb_out, float* ws_out, float* pdf_out,
+             int32_t* level_out, void* stream);
+
+/* --- multi-material eval (render.py:352-356 groups by material):
+ *     mat_id (n,) int32 in [0, n_mats).  DIVERGENT decodes mixed tiles
+ *     directly; BINNED first bins queries by material with warp-aggregated
+ *     counting, then runs the coherent kernel per bin.  workspace must hold
+ *     nm_multi_workspace_bytes(n, n_mats) bytes of device memory. --------- */
+size_t nm_multi_workspace_bytes(int64_t n, int32_t n_mats);
+int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
+                  const int32_t* mat_id, const float* uv, const float* lod,
+                  int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+                  float* rgb_out, int32_t mode, void* workspace, size_t workspace_bytes,
+                  void* stream);
+
+/* --- misc -------------------------------------------------------------- */
+const char* nm_last_error(void);
+int nm_version(void);
+/* number of fused-kernel launches issued by this process (for bench claims) */
+int64_t nm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMQ_H */

@@ -1,0 +1,160 @@
+"""Generate golden vectors for the query path by running the REAL reference
+implementation (/root/reference/pkg/src/neuralmat) — test infrastructure.
+
+Writes tests/golden/*.npz (+ one reference-written archive).  The fixtures
+pin (a) the numpy oracle in oracle/nm_oracle.py and (b) the CUDA kernels on
+the GPU box, where /root/reference does not exist.
+
+    python oracle/make_golden.py
+"""
+
+import json
+import os
+import shutil
+import sys
+import tempfile
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "tests", "golden")
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import neuralmat  # noqa: F401
+    from neuralmat import geom, latent, neural, proxy
+    return geom, latent, neural, proxy
+
+
+def _f32(a):
+    return np.asarray(a, dtype=np.float32)
+
+
+def _nets(prefix, net, d):
+    if net is None:
+        d[prefix + "_n"] = np.int64(0)
+        return
+    d[prefix + "_n"] = np.int64(len(net.layers))
+    for i, l in enumerate(net.layers):
+        d[f"{prefix}_w{i}"] = l.w
+        d[f"{prefix}_b{i}"] = l.b
+        d[f"{prefix}_a{i}"] = np.int64(0 if l.act == "linear" else 1)
+
+
+def make_case(name, cfg_kwargs, res=(64, 64), n=1024, seed=0, uv_lo=0.0, uv_hi=1.0,
+              taps=False, fp32_path=False):
+    geom, latent, neural, proxy = _ref()
+    cfg = neural.NeuralMaterialConfig(**cfg_kwargs)
+    mat = neural.NeuralMaterial.create(cfg, np.random.default_rng(seed))
+    lrng = np.random.default_rng(seed + 1)
+    pyr = latent.LatentPyramid.zeros(res[0], res[1])
+    for lvl in pyr.levels:
+        lvl[:] = lrng.standard_normal(lvl.shape).astype(np.float32)
+    mat.latent = pyr
+    q = np.random.default_rng(seed + 2)
+    uv = _f32(uv_lo + (uv_hi - uv_lo) * q.random((n, 2)))
+    lod = _f32(q.random(n) * (pyr.n_levels - 1))
+    u_rr = _f32(q.random(n))
+    wi, wo = geom.sample_half_diff(q, n)
+    wi, wo = _f32(wi), _f32(wo)
+    u3 = _f32(q.random((n, 3)))
+    # reference fp16 path
+    hl = mat.half()["latent"]
+    z, chosen = hl.fetch(uv.astype(np.float64), lod.astype(np.float64), u_rr.astype(np.float64))
+    f, albedo = neural.eval_brdf(mat, z, wi.astype(np.float64), wo.astype(np.float64), fp16=True)
+    p = neural.infer_proxy(mat, z, wi.astype(np.float64), fp16=True)
+    ws = proxy.sample(p, wi.astype(np.float64), u3.astype(np.float64))
+    pdf_ws = proxy.pdf(p, wi.astype(np.float64), ws)
+    pdf_wo = proxy.pdf(p, wi.astype(np.float64), wo.astype(np.float64))
+    f_mat, _, chosen2 = neural.eval_material(mat, uv.astype(np.float64), lod.astype(np.float64),
+                                             wi.astype(np.float64), wo.astype(np.float64),
+                                             u_rr.astype(np.float64), fp16=True)
+    assert np.array_equal(chosen, chosen2) and np.array_equal(f, f_mat)
+    d = dict(
+        config=np.array(json.dumps(cfg.to_json())), res=np.array(res), seed=np.int64(seed),
+        uv=uv, lod=lod, u_rr=u_rr, wi=wi, wo=wo, u3=u3,
+        z=z, chosen=chosen, f=f, ws=ws, pdf_ws=pdf_ws, pdf_wo=pdf_wo,
+        params=np.concatenate([p.wd[:, None], p.ws[:, None], p.mu_d, p.alpha, p.rho[:, None],
+                               p.mu_s], axis=1),
+    )
+    if albedo is not None:
+        d["albedo"] = albedo
+    for i, l in enumerate(pyr.levels):
+        d[f"lat{i}"] = l
+    _nets("frame", mat.frame_layer, d)
+    _nets("brdf", mat.brdf_decoder, d)
+    _nets("sampler", mat.sampler_decoder, d)
+    hq = mat.half()
+    d["packed_brdf"] = hq["brdf"].packed
+    d["packed_sampler"] = hq["sampler"].packed
+    if hq["frame"] is not None:
+        d["packed_frame"] = hq["frame"].packed
+    if taps:
+        xs = np.zeros((n, 4), np.int64)
+        ys = np.zeros((n, 4), np.int64)
+        wts = np.zeros((n, 4))
+        for lv in np.unique(chosen):
+            m = chosen == lv
+            a, b, c = hl._taps(int(lv), uv[m].astype(np.float64))
+            xs[m], ys[m], wts[m] = a, b, c
+        d.update(xs=xs, ys=ys, wts=wts)
+    if fp32_path:
+        f32, _ = neural.eval_brdf(mat, z, wi.astype(np.float64), wo.astype(np.float64), fp16=False)
+        d["f_fp32path"] = f32
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, {k: v.shape for k, v in d.items() if hasattr(v, "shape") and v.ndim})
+
+
+def make_proxy_case(name="proxy_kat", n=2048, seed=11):
+    geom, latent, neural, proxy = _ref()
+    rng = np.random.default_rng(seed)
+    wd = rng.uniform(0.0, 1.0, n)
+    mu_d = rng.uniform(-1, 1, (n, 2)) * rng.integers(0, 2, (n, 1))
+    alpha = rng.uniform(0.02, 1.0, (n, 2))
+    rho = rng.uniform(-0.9, 0.9, n)
+    mu_s = rng.uniform(-0.5, 0.5, (n, 2))
+    blk = _f32(np.concatenate([wd[:, None], 1 - wd[:, None], mu_d, alpha, rho[:, None], mu_s], 1))
+    p = proxy.ProxyParams(blk[:, 0], blk[:, 1], blk[:, 2:4], blk[:, 4:6], blk[:, 6], blk[:, 7:9])
+    wi = geom.sample_uniform_hemisphere(rng.random((n, 2)))
+    wi[:, 2] = np.maximum(wi[:, 2], 0.05)
+    wi = _f32(geom.normalize(wi))
+    u3 = _f32(rng.random((n, 3)))
+    wo_any = _f32(geom.sample_uniform_sphere(rng.random((n, 2))))
+    ws = proxy.sample(p, wi.astype(np.float64), u3.astype(np.float64))
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), params=blk, wi=wi, u3=u3, wo=wo_any,
+                        ws=ws, pdf_ws=proxy.pdf(p, wi.astype(np.float64), ws),
+                        pdf_wo=proxy.pdf(p, wi.astype(np.float64), wo_any.astype(np.float64)))
+    print(name)
+
+
+def make_archive(name="archive_albedo"):
+    geom, latent, neural, proxy = _ref()
+    rng = np.random.default_rng(12)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(albedo_head=True), rng)
+    mat.latent = latent.LatentPyramid.zeros(16, 16)
+    for lvl in mat.latent.levels:
+        lvl[:] = rng.standard_normal(lvl.shape).astype(np.float32)
+    tmp = tempfile.mkdtemp()
+    neural.save_archive(os.path.join(tmp, f"{name}.nma"), mat, include_encoder=True)
+    for ext in (".nma", ".latents"):
+        shutil.copy(os.path.join(tmp, name + ext), os.path.join(OUT, name + ext))
+    print(name)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    make_case("c1_2x32", {}, n=4096, taps=True, fp32_path=True)
+    make_case("c1_2x16", {"brdf_hidden": "2x16"}, seed=3)
+    make_case("c1_3x64", {"brdf_hidden": "3x64"}, seed=6)
+    make_case("albedo", {"albedo_head": True}, res=(32, 32), seed=9)
+    make_case("isotropic", {"sampler_isotropic": True}, res=(32, 32), seed=12)
+    make_case("vanilla", {"use_frames": False}, res=(32, 32), seed=15)
+    make_case("one_frame", {"n_frames": 1}, res=(32, 32), seed=18)
+    make_case("npot_wrap", {}, res=(24, 20), seed=21, uv_lo=-2.0, uv_hi=3.0, taps=True)
+    make_proxy_case()
+    make_archive()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,612 @@
+"""CPU oracle for the neural-material query path — TEST INFRASTRUCTURE ONLY.
+
+This module is a from-scratch numpy restatement of the reference
+implementation's query hot path (``/root/reference/pkg/src/neuralmat``,
+"neuralmat", arXiv 2305.02678).  It exists so that
+
+* ``tests/`` can check the CUDA kernels against a CPU implementation on the
+  GPU box (where ``/root/reference`` does not exist), and
+* ``bench.py`` can time a CPU baseline (``cpu_baseline`` / ``--impl
+  reference``).
+
+It is NEVER imported by the product package ``paper_2305_02678_b200`` (the
+product path has no CPU fallback).  Parity of this restatement with the real
+reference is pinned by ``tests/test_oracle_golden.py`` against golden vectors
+that ``oracle/make_golden.py`` produced by importing the reference itself.
+
+Arithmetic follows the reference exactly: float64 for texel coordinates,
+bilinear weights, frames and proxy math; float32 GEMMs over fp16-rounded
+inputs for the "fused" fp16 path.  Each function cites the reference
+``file:line`` it restates (paths relative to ``pkg/src/neuralmat``).
+"""
+
+import numpy as np
+
+LATENT_CHANNELS = 8          # latent.py:17
+LEAKY_SLOPE = 0.01           # mlp.py:16
+FP16_MAX = 65504.0           # mlp.py:17
+ALPHA_FLOOR = 1e-4           # proxy.py:32
+RHO_CLAMP = np.sqrt(1.0 - 1e-4)  # proxy.py:33
+PARAM_DIM = 9                # texture.py:25 (encoder input width)
+N_FRAMES = 2                 # neural.py:30
+
+ACT_LINEAR = "linear"
+ACT_LEAKY = "leaky_relu"
+
+
+# ---------------------------------------------------------------------------
+# geometry helpers (geom.py)
+
+def _unit(v):
+    """geom.py:23-24"""
+    return v / np.linalg.norm(v, axis=-1, keepdims=True)
+
+
+def _mirror(w, m):
+    """geom.py:31-33: 2 (w.m) m - w"""
+    return 2.0 * np.sum(w * m, axis=-1)[..., None] * m - w
+
+
+def fallback_tangent(n):
+    """geom.py:82-89: n x e_k, k = argmin |n_k| (first index on ties)."""
+    n = np.asarray(n, dtype=np.float64)
+    k = np.argmin(np.abs(n), axis=-1)
+    e = np.zeros_like(n)
+    e[np.arange(n.shape[0]), k] = 1.0
+    return _unit(np.cross(n, e))
+
+
+def uniform_sphere(u):
+    """geom.py:121-126"""
+    u = np.asarray(u, dtype=np.float64)
+    z = 1.0 - 2.0 * u[..., 0]
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = 2.0 * np.pi * u[..., 1]
+    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=-1)
+
+
+def uniform_hemisphere(u):
+    """geom.py:112-118"""
+    u = np.asarray(u, dtype=np.float64)
+    z = 1.0 - u[..., 0]
+    r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+    phi = 2.0 * np.pi * u[..., 1]
+    return np.stack([r * np.cos(phi), r * np.sin(phi), z], axis=-1)
+
+
+def _basis_from_normal(n):
+    """geom.py:60-93 (frame_from_normal = orthonormal_frame(n, fallback))."""
+    t0 = fallback_tangent(n)
+    c = np.cross(n, t0)
+    b = c / np.linalg.norm(c, axis=-1, keepdims=True)
+    nn = _unit(n)
+    t = np.cross(b, nn)
+    return t, b, nn
+
+
+def half_diff_directions(u):
+    """geom.py:138-151: (wi, wo) from half/difference vectors."""
+    u = np.asarray(u, dtype=np.float64)
+    h = uniform_hemisphere(u[..., 0:2])
+    d = uniform_hemisphere(u[..., 2:4])
+    t, b, n = _basis_from_normal(h)
+    wi = d[..., 0:1] * t + d[..., 1:2] * b + d[..., 2:3] * n
+    return wi, _mirror(wi, h)
+
+
+def draw_direction_pairs(rng, n):
+    """geom.py:154-173: rejection loop keeping pairs with both z > 0."""
+    wi = np.empty((n, 3))
+    wo = np.empty((n, 3))
+    got = 0
+    while got < n:
+        need = n - got
+        m = max(64, int(2.3 * need))
+        a, b = half_diff_directions(rng.random((m, 4)))
+        keep = np.flatnonzero((a[:, 2] > 0.0) & (b[:, 2] > 0.0))[:need]
+        wi[got:got + keep.size] = a[keep]
+        wo[got:got + keep.size] = b[keep]
+        got += keep.size
+    return wi, wo
+
+
+# ---------------------------------------------------------------------------
+# latent pyramid (latent.py)
+
+def pyramid_shapes(width, height):
+    """latent.py:28-38: halve with max(1, .//2) until 1x1."""
+    shapes = []
+    w, h = width, height
+    while True:
+        shapes.append((h, w))
+        if w == 1 and h == 1:
+            return shapes
+        w, h = max(1, w // 2), max(1, h // 2)
+
+
+class Pyramid:
+    """Latent pyramid: list of (H, W, C) float32 levels (latent.py:21-26)."""
+
+    def __init__(self, levels):
+        self.levels = [np.ascontiguousarray(l, dtype=np.float32) for l in levels]
+
+    @property
+    def n_levels(self):
+        return len(self.levels)
+
+    def half_levels(self):
+        """latent.py:124-126: clip to +-65504, RNE to fp16."""
+        return [np.clip(l, -FP16_MAX, FP16_MAX).astype(np.float16) for l in self.levels]
+
+    def render_copy(self):
+        """neural.py:150-154: fp16 texels widened back to fp32."""
+        return Pyramid([l.astype(np.float32) for l in self.half_levels()])
+
+    def taps(self, level, uv):
+        """latent.py:56-74: wrap-addressed bilinear taps in float64."""
+        h, w = self.levels[level].shape[:2]
+        uv = np.asarray(uv, dtype=np.float64)
+        x = uv[..., 0] * w - 0.5
+        y = uv[..., 1] * h - 0.5
+        xf, yf = np.floor(x), np.floor(y)
+        fx, fy = x - xf, y - yf
+        x0 = xf.astype(np.int64) % w
+        y0 = yf.astype(np.int64) % h
+        x1 = (x0 + 1) % w
+        y1 = (y0 + 1) % h
+        gx, gy = 1.0 - fx, 1.0 - fy
+        wts = np.stack([gx * gy, fx * gy, gx * fy, fx * fy], axis=-1)
+        return (np.stack([x0, x1, x0, x1], axis=-1),
+                np.stack([y0, y0, y1, y1], axis=-1), wts)
+
+    def choose_level(self, level, u_rr):
+        """latent.py:76-82: Russian-roulette level pick."""
+        top = self.n_levels - 1
+        lv = np.clip(np.asarray(level, dtype=np.float64), 0, top)
+        lo = np.floor(lv)
+        pick = lo + (np.asarray(u_rr) < (lv - lo))
+        return np.clip(pick, 0, top).astype(np.int64)
+
+    def fetch(self, uv, level, u_rr):
+        """latent.py:84-98 -> (z (B,C) float32, chosen (B,) int64)."""
+        uv = np.atleast_2d(np.asarray(uv, dtype=np.float64))
+        chosen = self.choose_level(np.broadcast_to(level, uv.shape[:-1]), u_rr)
+        z = np.empty(uv.shape[:-1] + (self.levels[0].shape[2],), dtype=np.float32)
+        for lv in np.unique(chosen):
+            m = chosen == lv
+            xs, ys, wts = self.taps(int(lv), uv[m])
+            tex = self.levels[int(lv)][ys, xs]
+            z[m] = np.sum(tex * wts[..., None], axis=-2, dtype=np.float64)
+        return z, chosen
+
+    def fetch_level(self, uv, level):
+        """latent.py:100-107: deterministic fetch at one integer level."""
+        uv = np.atleast_2d(np.asarray(uv, dtype=np.float64))
+        xs, ys, wts = self.taps(int(level), uv)
+        tex = self.levels[int(level)][ys, xs]
+        return np.sum(tex * wts[..., None], axis=-2, dtype=np.float64).astype(np.float32)
+
+
+def random_pyramid(rng, width, height, channels=LATENT_CHANNELS):
+    """Synthetic latents, one standard_normal draw per level in order
+    (the reference tests' generator, tests/test_latent.py:10-14)."""
+    return Pyramid([rng.standard_normal((h, w, channels)).astype(np.float32)
+                    for h, w in pyramid_shapes(width, height)])
+
+
+# ---------------------------------------------------------------------------
+# MLP engine (mlp.py)
+
+def _act(x, act):
+    """mlp.py:27-30"""
+    return x if act == ACT_LINEAR else np.where(x >= 0.0, x, LEAKY_SLOPE * x)
+
+
+class Net:
+    """fp32 master network: list of (w (out,in) f32, b (out,) f32, act)."""
+
+    def __init__(self, layers):
+        self.layers = [(np.ascontiguousarray(w, np.float32), np.ascontiguousarray(b, np.float32), a)
+                       for w, b, a in layers]
+
+    @classmethod
+    def random(cls, sizes, rng, out_act=ACT_LINEAR, weight_scale=1.0):
+        """mlp.py:57-69: He-style fan-in uniform init, zero biases; the RNG
+        is consumed layer by layer exactly like the reference."""
+        layers = []
+        last = len(sizes) - 2
+        for i in range(len(sizes) - 1):
+            fan_in, fan_out = sizes[i], sizes[i + 1]
+            bound = weight_scale * np.sqrt(6.0 / fan_in)
+            w = rng.uniform(-bound, bound, size=(fan_out, fan_in))
+            layers.append((w, np.zeros(fan_out), out_act if i == last else ACT_LEAKY))
+        return cls(layers)
+
+    @property
+    def in_dim(self):
+        return self.layers[0][0].shape[1]
+
+    @property
+    def out_dim(self):
+        return self.layers[-1][0].shape[0]
+
+    def forward(self, x):
+        """mlp.py:79-88: fp32 forward."""
+        x = np.asarray(x, dtype=np.float32)
+        for w, b, a in self.layers:
+            x = _act(x @ w.T + b, a)
+        return x
+
+
+class HalfNet:
+    """Quantized network (mlp.py:165-233): fp16 weights packed per layer as
+    [w_row(fan_in), bias] per output neuron."""
+
+    def __init__(self, shapes, acts, packed, clamped=0):
+        self.shapes = list(shapes)
+        self.acts = list(acts)
+        self.packed = np.asarray(packed, dtype=np.float16)
+        self.clamped = clamped
+        self.views = []
+        ofs = 0
+        for out, fan_in in self.shapes:
+            blk = self.packed[ofs:ofs + out * (fan_in + 1)].reshape(out, fan_in + 1)
+            self.views.append((blk[:, :fan_in].astype(np.float32),
+                               blk[:, fan_in].astype(np.float32)))
+            ofs += out * (fan_in + 1)
+
+    def forward(self, x):
+        """mlp.py:196-208: round input to fp16 once, fp32 layers after."""
+        x = np.asarray(x).astype(np.float16).astype(np.float32)
+        for (w, b), a in zip(self.views, self.acts):
+            x = _act(x @ w.T + b, a)
+        return x
+
+
+def quantize(net):
+    """mlp.py:214-233: clamp to +-65504 (counted), RNE fp16, access order."""
+    parts, shapes, acts, clamped = [], [], [], 0
+    for w, b, a in net.layers:
+        blk = np.concatenate([w, b[:, None]], axis=1)
+        clamped += int(np.count_nonzero(np.abs(blk) > FP16_MAX))
+        parts.append(np.clip(blk, -FP16_MAX, FP16_MAX).astype(np.float16).ravel())
+        shapes.append(w.shape)
+        acts.append(a)
+    return HalfNet(shapes, acts, np.concatenate(parts), clamped)
+
+
+# ---------------------------------------------------------------------------
+# neural material (neural.py)
+
+def brdf_output(y):
+    """neural.py:37-39"""
+    return np.maximum(np.expm1(np.minimum(y, 60.0)), 0.0)
+
+
+def quad_tanh(x):
+    """neural.py:46-49"""
+    ax = np.abs(x)
+    return np.clip(x * (1.0 + 0.5 * ax) / (1.0 + ax + 0.5 * x * x), -1.0, 1.0)
+
+
+def quad_sinh(x):
+    """neural.py:58-60"""
+    return x * (1.0 + x * x / 6.0)
+
+
+def softmax_pair(a, b):
+    """neural.py:67-71"""
+    m = np.maximum(a, b)
+    ea, eb = np.exp(a - m), np.exp(b - m)
+    return ea / (ea + eb), eb / (ea + eb)
+
+
+def parse_arch(s):
+    """neural.py:77-79: "NxW" -> (W,)*N"""
+    n, w = s.lower().split("x")
+    return (int(w),) * int(n)
+
+
+class Config:
+    """neural.py:82-96 (same field names and defaults)."""
+
+    def __init__(self, brdf_hidden="2x32", sampler_hidden="3x32", encoder_hidden="3x32",
+                 n_frames=N_FRAMES, albedo_head=False, use_frames=True,
+                 vanilla_extra_width=12, sampler_isotropic=False, param_dim=PARAM_DIM,
+                 channels=LATENT_CHANNELS):
+        self.brdf_hidden = brdf_hidden
+        self.sampler_hidden = sampler_hidden
+        self.encoder_hidden = encoder_hidden
+        self.n_frames = n_frames
+        self.albedo_head = albedo_head
+        self.use_frames = use_frames
+        self.vanilla_extra_width = vanilla_extra_width
+        self.sampler_isotropic = sampler_isotropic
+        self.param_dim = param_dim
+        self.channels = channels
+
+    def to_json(self):
+        return dict(self.__dict__)
+
+
+class Material:
+    """Networks + latents of one neural material (neural.py:106-161)."""
+
+    def __init__(self, cfg, frame, brdf, sampler, encoder=None, latent=None):
+        self.cfg = cfg
+        self.frame = frame
+        self.brdf = brdf
+        self.sampler = sampler
+        self.encoder = encoder
+        self.latent = latent
+        self._half = None
+
+    @classmethod
+    def random(cls, cfg, rng):
+        """neural.py:117-141 (RNG consumed in the same order: frame layer,
+        BRDF decoder, sampler decoder, encoder)."""
+        c = cfg.channels
+        brdf_out = 6 if cfg.albedo_head else 3
+        frame = None
+        if cfg.use_frames:
+            frame = Net.random((c, 6 * cfg.n_frames), rng, weight_scale=0.1)
+            w, _, a = frame.layers[0]
+            frame.layers[0] = (w, np.tile(np.float32([0, 0, 1, 1, 0, 0]), cfg.n_frames), a)
+            sizes = (c + 6 * cfg.n_frames, *parse_arch(cfg.brdf_hidden), brdf_out)
+        else:
+            sizes = (c + 6, cfg.vanilla_extra_width, *parse_arch(cfg.brdf_hidden), brdf_out)
+        brdf = Net.random(sizes, rng)
+        sampler = Net.random((c + 3, *parse_arch(cfg.sampler_hidden),
+                              2 if cfg.sampler_isotropic else 9), rng)
+        encoder = Net.random((cfg.param_dim, *parse_arch(cfg.encoder_hidden), c), rng)
+        return cls(cfg, frame, brdf, sampler, encoder)
+
+    def half(self):
+        """neural.py:147-161: cached fp16 inference copies."""
+        if self._half is None:
+            self._half = {
+                "frame": quantize(self.frame) if self.frame is not None else None,
+                "brdf": quantize(self.brdf),
+                "sampler": quantize(self.sampler),
+                "latent": self.latent.render_copy() if self.latent is not None else None,
+            }
+        return self._half
+
+
+def frames_from_raw(raw):
+    """neural.py:207-233 -> (t, b, n), each (B, N, 3) float64."""
+    raw = np.atleast_2d(np.asarray(raw, dtype=np.float64))
+    nb = raw.shape[0]
+    r = raw.reshape(nb, raw.shape[1] // 6, 6)
+    rn, rt = r[..., 0:3], r[..., 3:6].copy()
+    n = rn / np.maximum(np.linalg.norm(rn, axis=-1, keepdims=True), 1e-12)
+    c = np.cross(n, rt)
+    cl = np.linalg.norm(c, axis=-1, keepdims=True)
+    bad = cl[..., 0] < 1e-8
+    if np.any(bad):
+        rt[bad] = fallback_tangent(n[bad])
+        c = np.cross(n, rt)
+        cl = np.linalg.norm(c, axis=-1, keepdims=True)
+    b = c / np.maximum(cl, 1e-12)
+    return np.cross(b, n), b, n
+
+
+def frame_transform(frames, w):
+    """neural.py:185-196: (t_i.w, b_i.w, n_i.w) over frames -> (B, 3N)."""
+    t, b, n = frames
+    w = w[:, None, :]
+    out = np.stack([np.sum(t * w, -1), np.sum(b * w, -1), np.sum(n * w, -1)], axis=-1)
+    return out.reshape(w.shape[0], -1)
+
+
+def eval_brdf(mat, z, wi, wo, fp16=False):
+    """neural.py:273-300 -> (f (B,3) f64, albedo or None)."""
+    wi = np.atleast_2d(np.asarray(wi, dtype=np.float64))
+    wo = np.atleast_2d(np.asarray(wo, dtype=np.float64))
+    z64 = np.atleast_2d(np.asarray(z, dtype=np.float64))
+    if mat.cfg.use_frames:
+        if fp16:
+            raw = mat.half()["frame"].forward(np.atleast_2d(z).astype(np.float32))
+        else:
+            raw = mat.frame.forward(z64.astype(np.float32))
+        fr = frames_from_raw(raw)
+        zin = np.atleast_2d(z) if fp16 else z64
+        inp = np.concatenate([zin, frame_transform(fr, wi), frame_transform(fr, wo)], axis=-1)
+    else:
+        inp = np.concatenate([z64, wi, wo], axis=-1)
+    inp = inp.astype(np.float32)
+    y = mat.half()["brdf"].forward(inp) if fp16 else mat.brdf.forward(inp)
+    y = np.asarray(y, dtype=np.float64)
+    up = ((wi[:, 2] > 0.0) & (wo[:, 2] > 0.0))[:, None]
+    f = np.where(up, brdf_output(y[:, 0:3]), 0.0)
+    if mat.cfg.albedo_head:
+        return f, np.where(up, np.maximum(y[:, 3:6], 0.0), 0.0)
+    return f, None
+
+
+def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False):
+    """neural.py:303-309"""
+    pyr = mat.half()["latent"] if fp16 else mat.latent
+    z, chosen = pyr.fetch(uv, level, u_rr)
+    f, albedo = eval_brdf(mat, z, wi, wo, fp16=fp16)
+    return f, albedo, chosen
+
+
+# ---------------------------------------------------------------------------
+# analytic proxy (proxy.py)
+
+class Proxy:
+    """proxy.py:37-84: 9 parameters with alpha floor / rho clamp applied."""
+
+    def __init__(self, wd, ws, mu_d, alpha, rho, mu_s):
+        self.wd = np.atleast_1d(np.asarray(wd, dtype=np.float64))
+        self.ws = np.atleast_1d(np.asarray(ws, dtype=np.float64))
+        self.mu_d = np.atleast_2d(np.asarray(mu_d, dtype=np.float64))
+        self.alpha = np.maximum(np.atleast_2d(np.asarray(alpha, dtype=np.float64)), ALPHA_FLOOR)
+        self.rho = np.clip(np.atleast_1d(np.asarray(rho, dtype=np.float64)), -RHO_CLAMP, RHO_CLAMP)
+        self.mu_s = np.atleast_2d(np.asarray(mu_s, dtype=np.float64))
+
+    def __len__(self):
+        return self.wd.shape[0]
+
+    def subset(self, idx):
+        return Proxy(self.wd[idx], self.ws[idx], self.mu_d[idx], self.alpha[idx],
+                     self.rho[idx], self.mu_s[idx])
+
+    def as_array(self):
+        """(B, 9) in the order wd, ws, mu_d(2), alpha(2), rho, mu_s(2)."""
+        return np.concatenate([self.wd[:, None], self.ws[:, None], self.mu_d, self.alpha,
+                               self.rho[:, None], self.mu_s], axis=1)
+
+    @property
+    def s(self):
+        return np.sqrt(1.0 - self.rho ** 2)
+
+    def det(self):
+        """proxy.py:76-78"""
+        return self.alpha[:, 0] * self.alpha[:, 1] * self.s
+
+    def warp(self):
+        """proxy.py:64-74: slope-space matrix M."""
+        m = np.zeros((len(self), 3, 3))
+        m[:, 0, 0] = self.alpha[:, 0]
+        m[:, 0, 2] = -self.mu_s[:, 0]
+        m[:, 1, 0] = self.alpha[:, 1] * self.rho
+        m[:, 1, 1] = self.alpha[:, 1] * self.s
+        m[:, 1, 2] = -self.mu_s[:, 1]
+        m[:, 2, 2] = 1.0
+        return m
+
+    def diffuse_axis(self):
+        """proxy.py:80-84"""
+        v = np.stack([-self.mu_d[:, 0], -self.mu_d[:, 1], np.ones_like(self.wd)], axis=-1)
+        return _unit(v)
+
+
+RAW_WD, RAW_MUDX, RAW_MUDY, RAW_WS, RAW_AX, RAW_AY, RAW_RHO, RAW_MUSX, RAW_MUSY = range(9)
+
+
+def proxy_from_raw(raw, isotropic=False):
+    """neural.py:314-331"""
+    raw = np.atleast_2d(np.asarray(raw, dtype=np.float64))
+    if isotropic:
+        wd = 0.5 * (quad_tanh(raw[:, 0]) + 1.0)
+        a = 0.5 * (quad_tanh(raw[:, 1]) + 1.0)
+        z = np.zeros_like(wd)
+        return Proxy(wd, 1.0 - wd, np.stack([z, z], -1), np.stack([a, a], -1), z,
+                     np.stack([z, z], -1))
+    wd, ws = softmax_pair(raw[:, RAW_WD], raw[:, RAW_WS])
+    return Proxy(wd, ws, quad_sinh(raw[:, (RAW_MUDX, RAW_MUDY)]),
+                 0.5 * (quad_tanh(raw[:, (RAW_AX, RAW_AY)]) + 1.0),
+                 quad_tanh(raw[:, RAW_RHO]), quad_sinh(raw[:, (RAW_MUSX, RAW_MUSY)]))
+
+
+def infer_proxy(mat, z, wi, fp16=False):
+    """neural.py:353-362"""
+    z = np.atleast_2d(np.asarray(z, dtype=np.float64))
+    wi = np.atleast_2d(np.asarray(wi, dtype=np.float64))
+    inp = np.concatenate([z, wi], axis=-1).astype(np.float32)
+    raw = mat.half()["sampler"].forward(inp) if fp16 else mat.sampler.forward(inp)
+    return proxy_from_raw(raw, isotropic=mat.cfg.sampler_isotropic)
+
+
+def _half_vector(wi, wo):
+    """proxy.py:87-101: normalized wi+wo flipped to h.z >= 0, validity."""
+    h = wi + wo
+    hl = np.sqrt(np.sum(h * h, axis=-1))
+    ok = hl > 1e-9
+    h = h / np.maximum(hl, 1e-12)[..., None]
+    h = h * np.where(h[..., 2] < 0.0, -1.0, 1.0)[..., None]
+    return h, ok
+
+
+def _inverse_warp(p, h):
+    """proxy.py:104-111: q = M^-1 h in closed form."""
+    ax, ay, s = p.alpha[:, 0], p.alpha[:, 1], p.s
+    q0 = (h[:, 0] + p.mu_s[:, 0] * h[:, 2]) / ax
+    q1 = ((h[:, 1] + p.mu_s[:, 1] * h[:, 2]) / ay - p.rho * q0) / s
+    return np.stack([q0, q1, h[:, 2]], axis=-1)
+
+
+def pdf_diffuse(p, wo):
+    """proxy.py:114-116"""
+    return np.maximum(np.sum(wo * p.diffuse_axis(), axis=-1), 0.0) / np.pi
+
+
+def pdf_specular(p, wi, wo):
+    """proxy.py:119-126"""
+    h, ok = _half_vector(wi, wo)
+    q = _inverse_warp(p, h)
+    q2 = np.sum(q * q, axis=-1)
+    coh = np.abs(np.sum(wo * h, axis=-1))
+    val = h[:, 2] * (1.0 / p.det()) / (4.0 * np.pi * q2 * q2 * np.maximum(coh, 1e-12))
+    return np.where(ok & (h[:, 2] > 0.0), np.maximum(val, 0.0), 0.0)
+
+
+def pdf(p, wi, wo):
+    """proxy.py:129-135"""
+    wi = np.atleast_2d(np.asarray(wi, dtype=np.float64))
+    wo = np.atleast_2d(np.asarray(wo, dtype=np.float64))
+    return p.wd * pdf_diffuse(p, wo) + p.ws * pdf_specular(p, wi, wo)
+
+
+def ndf_sample(u):
+    """proxy.py:138-146: unit-roughness NDF sample."""
+    u = np.asarray(u, dtype=np.float64)
+    tan2 = u[..., 0] / np.maximum(1.0 - u[..., 0], 1e-12)
+    ct = 1.0 / np.sqrt(1.0 + tan2)
+    st = np.sqrt(np.maximum(0.0, 1.0 - ct * ct))
+    phi = 2.0 * np.pi * u[..., 1]
+    return np.stack([st * np.cos(phi), st * np.sin(phi), ct], axis=-1)
+
+
+def sample_diffuse(p, u2):
+    """proxy.py:149-156"""
+    g = p.diffuse_axis() + uniform_sphere(u2)
+    return g / np.maximum(np.linalg.norm(g, axis=-1, keepdims=True), 1e-9)
+
+
+def sample_specular(p, wi, u2):
+    """proxy.py:159-165"""
+    g = np.einsum("bij,bj->bi", p.warp(), ndf_sample(u2))
+    h = g / np.maximum(np.linalg.norm(g, axis=-1, keepdims=True), 1e-12)
+    return _mirror(wi, h)
+
+
+def sample(p, wi, u):
+    """proxy.py:168-180: u0 picks the lobe, (u1, u2) drive it."""
+    wi = np.atleast_2d(np.asarray(wi, dtype=np.float64))
+    u = np.atleast_2d(np.asarray(u, dtype=np.float64))
+    diff = u[:, 0] < p.wd
+    wo = np.empty_like(wi)
+    if np.any(diff):
+        wo[diff] = sample_diffuse(p.subset(diff), u[diff, 1:3])
+    if np.any(~diff):
+        spec = ~diff
+        wo[spec] = sample_specular(p.subset(spec), wi[spec], u[spec, 1:3])
+    return wo
+
+
+def normalize_check(p, wi, n_samples, rng, chunk=2_000_000):
+    """proxy.py:183-196: MC estimate of the sphere integral of pdf."""
+    total, done = 0.0, 0
+    while done < n_samples:
+        m = min(chunk, n_samples - done)
+        d = uniform_sphere(rng.random((m, 2)))
+        rep = p.subset(np.zeros(m, dtype=np.int64))
+        total += float(np.sum(pdf(rep, np.broadcast_to(wi, (m, 3)), d)))
+        done += m
+    return total * 4.0 * np.pi / n_samples
+
+
+# ---------------------------------------------------------------------------
+# one full query (the chain SURVEY §8d times): fetch -> eval -> proxy -> sample -> pdf
+
+def full_query(mat, uv, lod, u_rr, wi, wo, u3, fp16=True):
+    """render.py:368-372 + 385-386 + 401-402 chained for one batch."""
+    pyr = mat.half()["latent"] if fp16 else mat.latent
+    z, chosen = pyr.fetch(uv, lod, u_rr)
+    f, _ = eval_brdf(mat, z, wi, wo, fp16=fp16)
+    p = infer_proxy(mat, z, wi, fp16=fp16)
+    ws = sample(p, wi, u3)
+    return f, ws, pdf(p, wi, ws), p, chosen

@@ -1,0 +1,75 @@
+"""Array plumbing between the reference-style API (numpy in, numpy out) and
+the device pointers the C ABI takes.  torch is used only for device memory
+and streams."""
+
+import numpy as np
+import torch
+
+
+def cuda_device(device=None):
+    if not torch.cuda.is_available():
+        raise RuntimeError("the neural-material query path needs a CUDA device (no CPU fallback)")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    d = torch.device(device)
+    if d.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {device!r}")
+    return torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+
+
+def is_numpy_like(x):
+    return not isinstance(x, torch.Tensor)
+
+
+def as_rows(x, cols, device, name="array"):
+    """(B, cols) fp32 contiguous device tensor; 1-D input of length `cols` is
+    promoted to one row (np.atleast_2d semantics, latent.py:90)."""
+    if isinstance(x, torch.Tensor):
+        t = x
+        if t.dim() == 1 and cols > 1:
+            t = t[None, :]
+        t = t.to(device=device, dtype=torch.float32).contiguous()
+    else:
+        a = np.asarray(x)
+        if a.ndim == 1 and cols > 1:
+            a = a[None, :]
+        a = np.ascontiguousarray(a, dtype=np.float32)
+        t = torch.from_numpy(a).to(device, non_blocking=False)
+    if cols > 1 and (t.dim() != 2 or t.shape[1] != cols):
+        raise ValueError(f"{name}: expected shape (B, {cols}), got {tuple(t.shape)}")
+    if cols == 1:
+        t = t.reshape(-1)
+    return t
+
+
+def as_vec(x, n, device, name="array"):
+    """(n,) fp32 device tensor; scalars broadcast (returns (tensor, stride))."""
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=torch.float32).reshape(-1).contiguous()
+    else:
+        t = torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float32).reshape(-1))).to(device)
+    if t.numel() == 1 and n != 1:
+        return t, 0
+    if t.numel() != n:
+        raise ValueError(f"{name}: expected {n} values, got {t.numel()}")
+    return t, 1
+
+
+def empty(n, cols, device, dtype=torch.float32):
+    shape = (n,) if cols == 1 else (n, cols)
+    return torch.empty(shape, device=device, dtype=dtype)
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def out(t, numpy_mode, np_dtype=np.float64):
+    """Return numpy (reference dtype) for numpy callers, else the tensor."""
+    if not numpy_mode:
+        return t
+    return t.cpu().numpy().astype(np_dtype, copy=False)

@@ -1,0 +1,456 @@
+// nmq_abi.cu — C ABI (include/nmq.h): material creation (re-tiling the
+// reference's packed fp16 weights into the UMMA B-operand layout, latent
+// upload) and the query entry points.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <cuda_fp16.h>
+#include "../../include/nmq.h"
+#include "nmq_internal.h"
+
+using namespace nmq;
+
+namespace {
+
+thread_local std::string t_err;
+
+int fail(int code, const std::string& msg) {
+  t_err = msg;
+  return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(NM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+// Write B operand of one layer into `blob` (fp16 bits) at byte offset `off`.
+// Layout: chunk-major K-major, chunk c (8 K values) of row n at
+//   off + c*(n_pad*16) + n*16.
+struct Packer {
+  std::vector<uint16_t> blob;  // fp16 bits
+  uint32_t append(int n_pad, int k_chunks) {
+    const uint32_t off = (uint32_t)(blob.size() * 2);
+    blob.resize(blob.size() + (size_t)n_pad * k_chunks * 8, 0);
+    return off;
+  }
+  void set(uint32_t off, int n_pad, int n, int k, uint16_t v) {
+    const int c = k / 8, e = k % 8;
+    blob[off / 2 + (size_t)c * n_pad * 8 + (size_t)n * 8 + e] = v;
+  }
+};
+
+struct NetView {
+  int n_layers;
+  std::vector<int> fi, fo, act;
+  std::vector<size_t> ofs;  // offset of each layer in the packed array (halves)
+  const uint16_t* packed;
+};
+
+int view_net(const nm_net_desc& d, const char* name, NetView& v) {
+  if (d.n_layers <= 0 || !d.fan_in || !d.fan_out || !d.act || !d.packed)
+    return fail(NM_ERR_INVALID, std::string(name) + ": empty network description");
+  v.n_layers = d.n_layers;
+  v.packed = d.packed;
+  size_t o = 0;
+  for (int l = 0; l < d.n_layers; ++l) {
+    v.fi.push_back(d.fan_in[l]);
+    v.fo.push_back(d.fan_out[l]);
+    v.act.push_back(d.act[l]);
+    v.ofs.push_back(o);
+    if (d.fan_in[l] <= 0 || d.fan_out[l] <= 0)
+      return fail(NM_ERR_INVALID, std::string(name) + ": bad layer size");
+    if (l > 0 && d.fan_in[l] != d.fan_out[l - 1])
+      return fail(NM_ERR_INVALID, "layer dimensions do not chain");  // mlp.py:53-55
+    if (d.act[l] != NM_ACT_LINEAR && d.act[l] != NM_ACT_LEAKY)
+      return fail(NM_ERR_INVALID, "unknown activation code");
+    o += (size_t)d.fan_out[l] * (d.fan_in[l] + 1);
+  }
+  return NM_OK;
+}
+
+// Pack one chain of layers.  The first layer takes an input vector with its
+// bias slot at index fan_in; later layers take the hi/lo split of the
+// previous padded activation plus the shared bias chunk.
+int pack_chain(const NetView& v, Packer& pk, MatParams& mp, int& n_layers, const char* name) {
+  for (int l = 0; l < v.n_layers; ++l) {
+    if (n_layers >= kMaxLayers) return fail(NM_ERR_UNSUPPORTED, "too many layers");
+    LayerDesc L{};
+    const int fi = v.fi[l], fo = v.fo[l];
+    const int n_pad = round_up(fo, 16);
+    if (n_pad > kMaxWidth)
+      return fail(NM_ERR_UNSUPPORTED, std::string(name) + ": layer width > 64 not supported");
+    L.n_pad = (uint16_t)n_pad;
+    L.out = (uint8_t)fo;
+    L.act = (uint8_t)v.act[l];
+    const uint16_t* w = v.packed + v.ofs[l];  // [fo][fi+1]
+    if (l == 0) {
+      const int k_pad = round_up(fi + 1, 16);
+      if (k_pad > 32) return fail(NM_ERR_UNSUPPORTED, std::string(name) + ": input too wide");
+      L.first = 1;
+      L.in_pad = 0;
+      L.ksteps = (uint8_t)(k_pad / 16);
+      L.b_off = pk.append(n_pad, k_pad / 8);
+      for (int n = 0; n < fo; ++n) {
+        for (int k = 0; k < fi; ++k) pk.set(L.b_off, n_pad, n, k, w[(size_t)n * (fi + 1) + k]);
+        pk.set(L.b_off, n_pad, n, fi, w[(size_t)n * (fi + 1) + fi]);  // bias vs x[fi] = 1
+      }
+    } else {
+      const int in_pad = round_up(fi, 16);
+      L.first = 0;
+      L.in_pad = (uint16_t)in_pad;
+      L.ksteps = (uint8_t)(2 * in_pad / 16 + 1);
+      const int k_chunks = 2 * in_pad / 8 + 2;
+      L.b_off = pk.append(n_pad, k_chunks);
+      for (int n = 0; n < fo; ++n) {
+        for (int k = 0; k < fi; ++k) {
+          const uint16_t wv = w[(size_t)n * (fi + 1) + k];
+          pk.set(L.b_off, n_pad, n, k, wv);           // against hi
+          pk.set(L.b_off, n_pad, n, in_pad + k, wv);  // against lo
+        }
+        pk.set(L.b_off, n_pad, n, 2 * in_pad, w[(size_t)n * (fi + 1) + fi]);  // bias
+      }
+    }
+    if ((int)L.n_pad > mp.dmax) mp.dmax = L.n_pad;
+    mp.layers[n_layers++] = L;
+  }
+  return NM_OK;
+}
+
+}  // namespace
+
+struct nm_material {
+  int device = 0;
+  MatParams mp{};
+  void* latent = nullptr;
+  void* wblob = nullptr;
+  int64_t texels = 0;
+  int brdf_width = 0, sampler_width = 0;
+};
+
+extern "C" {
+
+const char* nm_last_error(void) { return t_err.c_str(); }
+int nm_version(void) { return NMQ_VERSION; }
+int64_t nm_launch_count(void) { return g_launches; }
+
+int nm_material_create(const nm_material_desc* d, int device, nm_material** out) {
+  if (!d || !out) return fail(NM_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (d->channels != 8)
+    return fail(NM_ERR_UNSUPPORTED, "latent channels must be 8 (one 16-byte texel)");
+  if (d->width <= 0 || d->height <= 0) return fail(NM_ERR_INVALID, "bad latent size");
+  // level chain, latent.py:28-38
+  std::vector<LevelDesc> lv;
+  {
+    int w = d->width, h = d->height;
+    int64_t off = 0;
+    while (true) {
+      lv.push_back(LevelDesc{w, h, off});
+      off += (int64_t)w * h;
+      if (w == 1 && h == 1) break;
+      w = w / 2 > 1 ? w / 2 : 1;
+      h = h / 2 > 1 ? h / 2 : 1;
+    }
+  }
+  if ((int)lv.size() != d->n_levels)
+    return fail(NM_ERR_INVALID, "corrupt pyramid header");  // latent.py:170-171
+  if ((int)lv.size() > kMaxLevels) return fail(NM_ERR_UNSUPPORTED, "too many levels");
+  const int64_t texel_bytes = d->latent_fp32 ? 32 : 16;
+  if (!d->latent) return fail(NM_ERR_INVALID, "material has no latent pyramid");
+
+  nm_material* m = new nm_material();
+  m->device = device;
+  MatParams& mp = m->mp;
+  mp.n_levels = (int)lv.size();
+  bool pow2 = true;
+  for (size_t i = 0; i < lv.size(); ++i) {
+    mp.lv[i] = lv[i];
+    pow2 &= (lv[i].w & (lv[i].w - 1)) == 0 && (lv[i].h & (lv[i].h - 1)) == 0;
+  }
+  mp.pow2 = pow2 ? 1 : 0;
+  mp.texel_fp32 = d->latent_fp32 ? 1 : 0;
+  m->texels = lv.back().off + 1;
+
+  // --- networks ---------------------------------------------------------------
+  Packer pk;
+  int nl = 0;
+  mp.use_frames = d->use_frames ? 1 : 0;
+  mp.n_frames = d->use_frames ? d->n_frames : 0;
+  mp.albedo = d->albedo_head ? 1 : 0;
+  mp.isotropic = d->sampler_isotropic ? 1 : 0;
+  mp.frame_layer = -1;
+  int rc;
+  NetView fv, bv, sv;
+  if (d->use_frames && d->frame.n_layers > 0) {
+    if (d->n_frames < 1 || d->n_frames > 2) {
+      delete m;
+      return fail(NM_ERR_UNSUPPORTED, "n_frames must be 1 or 2");
+    }
+    if ((rc = view_net(d->frame, "frame layer", fv)) != NM_OK) { delete m; return rc; }
+    if (fv.n_layers != 1 || fv.fi[0] != 8 || fv.fo[0] != 6 * d->n_frames) {
+      delete m;
+      return fail(NM_ERR_INVALID, "frame layer must be one 8 -> 6*n_frames layer");
+    }
+    mp.frame_layer = nl;
+    if ((rc = pack_chain(fv, pk, mp, nl, "frame layer")) != NM_OK) { delete m; return rc; }
+  }
+  const int brdf_in = d->use_frames ? 8 + 6 * d->n_frames : 14;
+  mp.brdf_in = brdf_in;
+  if (d->brdf.n_layers > 0) {
+    if ((rc = view_net(d->brdf, "brdf decoder", bv)) != NM_OK) { delete m; return rc; }
+    if (bv.fi[0] != brdf_in) {
+      delete m;
+      return fail(NM_ERR_INVALID, "expected input width " + std::to_string(brdf_in) +
+                                      ", got " + std::to_string(bv.fi[0]));
+    }
+    const int brdf_out = d->albedo_head ? 6 : 3;
+    if (bv.fo.back() != brdf_out) {
+      delete m;
+      return fail(NM_ERR_INVALID, "brdf decoder output width mismatch");
+    }
+    if (d->use_frames && d->frame.n_layers <= 0) {
+      delete m;
+      return fail(NM_ERR_INVALID, "use_frames requires a frame layer");
+    }
+    mp.has_brdf = 1;
+    mp.brdf_first = nl;
+    mp.brdf_count = bv.n_layers;
+    if ((rc = pack_chain(bv, pk, mp, nl, "brdf decoder")) != NM_OK) { delete m; return rc; }
+  }
+  if (d->sampler.n_layers > 0) {
+    if ((rc = view_net(d->sampler, "sampler decoder", sv)) != NM_OK) { delete m; return rc; }
+    if (sv.fi[0] != 11 || sv.fo.back() != (d->sampler_isotropic ? 2 : 9)) {
+      delete m;
+      return fail(NM_ERR_INVALID, "sampler decoder shape mismatch");
+    }
+    mp.has_sampler = 1;
+    mp.samp_first = nl;
+    mp.samp_count = sv.n_layers;
+    if ((rc = pack_chain(sv, pk, mp, nl, "sampler decoder")) != NM_OK) { delete m; return rc; }
+  }
+  for (int l = mp.brdf_first; l < mp.brdf_first + mp.brdf_count; ++l)
+    m->brdf_width = m->brdf_width > mp.layers[l].n_pad ? m->brdf_width : mp.layers[l].n_pad;
+  for (int l = mp.samp_first; l < mp.samp_first + mp.samp_count; ++l)
+    m->sampler_width = m->sampler_width > mp.layers[l].n_pad ? m->sampler_width : mp.layers[l].n_pad;
+  if (mp.dmax < 16) mp.dmax = 16;
+  if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
+  mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
+  if (mp.wblob_bytes > 200 * 1024) {
+    delete m;
+    return fail(NM_ERR_UNSUPPORTED, "weights exceed shared memory");
+  }
+
+  // --- device upload ---------------------------------------------------------------
+  DeviceGuard guard(device);
+  cudaError_t e;
+  const size_t lat_bytes = (size_t)m->texels * texel_bytes;
+  if ((e = cudaMalloc(&m->latent, lat_bytes)) != cudaSuccess) {
+    delete m;
+    return cuda_fail(e, "cudaMalloc(latent)");
+  }
+  e = cudaMemcpy(m->latent, d->latent, lat_bytes,
+                 d->latent_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(m->latent);
+    delete m;
+    return cuda_fail(e, "upload latent");
+  }
+  if (mp.wblob_bytes == 0) pk.append(16, 1), mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
+  if ((e = cudaMalloc(&m->wblob, mp.wblob_bytes)) != cudaSuccess ||
+      (e = cudaMemcpy(m->wblob, pk.blob.data(), mp.wblob_bytes, cudaMemcpyHostToDevice)) !=
+          cudaSuccess) {
+    cudaFree(m->latent);
+    if (m->wblob) cudaFree(m->wblob);
+    delete m;
+    return cuda_fail(e, "upload weights");
+  }
+  mp.latent = reinterpret_cast<const uint4*>(m->latent);
+  mp.wblob = reinterpret_cast<const uint4*>(m->wblob);
+  *out = m;
+  return NM_OK;
+}
+
+int nm_material_destroy(nm_material* m) {
+  if (!m) return NM_OK;
+  DeviceGuard guard(m->device);
+  if (m->latent) cudaFree(m->latent);
+  if (m->wblob) cudaFree(m->wblob);
+  delete m;
+  return NM_OK;
+}
+
+int nm_material_info_get(const nm_material* m, nm_material_info* info) {
+  if (!m || !info) return fail(NM_ERR_INVALID, "null argument");
+  info->device = m->device;
+  info->n_levels = m->mp.n_levels;
+  info->latent_texels = m->texels;
+  info->latent_bytes = m->texels * (m->mp.texel_fp32 ? 32 : 16);
+  info->weight_bytes = (int32_t)m->mp.wblob_bytes;
+  info->brdf_width = m->brdf_width;
+  info->sampler_width = m->sampler_width;
+  return NM_OK;
+}
+
+int nm_material_levels(const nm_material* m, int32_t* w, int32_t* h, int64_t* offset) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  for (int i = 0; i < m->mp.n_levels; ++i) {
+    if (w) w[i] = m->mp.lv[i].w;
+    if (h) h[i] = m->mp.lv[i].h;
+    if (offset) offset[i] = m->mp.lv[i].off;
+  }
+  return NM_OK;
+}
+
+const void* nm_material_latent_ptr(const nm_material* m) { return m ? m->latent : nullptr; }
+
+#define NM_CHECK_N(n)                                          \
+  do {                                                         \
+    if ((n) < 0) return fail(NM_ERR_INVALID, "negative batch"); \
+  } while (0)
+
+static int finish(const nm_material* m, cudaError_t e, const char* what) {
+  (void)m;
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return NM_OK;
+}
+
+int nm_fetch(const nm_material* m, int64_t n, const float* uv, const float* lod,
+             int32_t lod_stride, const float* u_rr, float* z_out, int32_t* level_out,
+             int32_t* taps_out, float* wts_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.z_out = z_out; a.level = level_out; a.taps = taps_out; a.wts = wts_out;
+  DeviceGuard guard(m->device);
+  return finish(m, launch_fetch(m->mp, a, (cudaStream_t)stream), "nm_fetch");
+}
+
+int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
+            int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+            float* rgb_out, float* albedo_out, int32_t* level_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !wo || !rgb_out) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.wo = wo; a.rgb = rgb_out; a.albedo = albedo_out; a.level = level_out;
+  DeviceGuard guard(m->device);
+  if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  return finish(m, launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream), "nm_eval");
+}
+
+int nm_eval_z(const nm_material* m, int64_t n, const float* z, const float* wi, const float* wo,
+              float* rgb_out, float* albedo_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!z || !wi || !wo || !rgb_out) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.z = z; a.wi = wi; a.wo = wo; a.rgb = rgb_out; a.albedo = albedo_out;
+  DeviceGuard guard(m->device);
+  if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  return finish(m, launch_fused(m->mp, kModeEvalZ, a, (cudaStream_t)stream), "nm_eval_z");
+}
+
+int nm_infer_proxy(const nm_material* m, int64_t n, const float* z, const float* wi,
+                   float* params9_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!z || !wi || !params9_out) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.z = z; a.wi = wi; a.params9 = params9_out;
+  DeviceGuard guard(m->device);
+  if (!m->mp.has_sampler) return fail(NM_ERR_INVALID, "material has no sampler decoder");
+  return finish(m, launch_fused(m->mp, kModeProxyZ, a, (cudaStream_t)stream), "nm_infer_proxy");
+}
+
+int nm_sample(int64_t n, const float* params9, const float* wi, const float* u3, float* wo_out,
+              void* stream) {
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!params9 || !wi || !u3 || !wo_out) return fail(NM_ERR_INVALID, "null input");
+  return finish(nullptr, launch_sample(n, params9, wi, u3, wo_out, (cudaStream_t)stream),
+                "nm_sample");
+}
+
+int nm_pdf(int64_t n, const float* params9, const float* wi, const float* wo, float* pdf_out,
+           void* stream) {
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!params9 || !wi || !wo || !pdf_out) return fail(NM_ERR_INVALID, "null input");
+  return finish(nullptr, launch_pdf(n, params9, wi, wo, pdf_out, (cudaStream_t)stream), "nm_pdf");
+}
+
+int nm_sample_pdf(const nm_material* m, int64_t n, const float* uv, const float* lod,
+                  int32_t lod_stride, const float* u_rr, const float* wi, const float* u3,
+                  float* ws_out, float* pdf_out, float* params9_out, int32_t* level_out,
+                  void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !u3 || !ws_out || !pdf_out)
+    return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.u3 = u3; a.ws = ws_out; a.pdf = pdf_out; a.params9 = params9_out;
+  a.level = level_out;
+  DeviceGuard guard(m->device);
+  if (!m->mp.has_sampler) return fail(NM_ERR_INVALID, "material has no sampler decoder");
+  return finish(m, launch_fused(m->mp, kModeSamplePdf, a, (cudaStream_t)stream), "nm_sample_pdf");
+}
+
+int nm_query(const nm_material* m, int64_t n, const float* uv, const float* lod,
+             int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+             const float* u3, float* rgb_out, float* ws_out, float* pdf_out, int32_t* level_out,
+             void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !wo || !u3 || !rgb_out || !ws_out || !pdf_out)
+    return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.wo = wo; a.u3 = u3; a.rgb = rgb_out; a.ws = ws_out; a.pdf = pdf_out;
+  a.level = level_out;
+  DeviceGuard guard(m->device);
+  if (!m->mp.has_brdf || !m->mp.has_sampler)
+    return fail(NM_ERR_INVALID, "material needs both decoders");
+  return finish(m, launch_fused(m->mp, kModeQuery, a, (cudaStream_t)stream), "nm_query");
+}
+
+size_t nm_multi_workspace_bytes(int64_t n, int32_t n_mats) {
+  if (n < 0 || n_mats <= 0) return 0;
+  return (size_t)n * 4 + (size_t)(2 * n_mats + 64) * 4 + 256;
+}
+
+int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
+                  const int32_t* mat_id, const float* uv, const float* lod, int32_t lod_stride,
+                  const float* u_rr, const float* wi, const float* wo, float* rgb_out,
+                  int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
+  (void)mats; (void)n_mats; (void)n; (void)mat_id; (void)uv; (void)lod; (void)lod_stride;
+  (void)u_rr; (void)wi; (void)wo; (void)rgb_out; (void)mode; (void)workspace;
+  (void)workspace_bytes; (void)stream;
+  return fail(NM_ERR_UNSUPPORTED, "nm_eval_multi: not built yet");
+}
+
+}  // extern "C"

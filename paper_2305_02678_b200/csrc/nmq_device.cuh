@@ -1,0 +1,298 @@
+// nmq_device.cuh — per-query device math of the neural-material query path:
+// latent fetch, learned shading frames, proxy parameter maps, sample and pdf.
+// One thread owns one query; everything here is scalar SIMT code.
+// Reference citations: /root/reference/pkg/src/neuralmat/<file>:<line>.
+#pragma once
+#include <cstdint>
+#include <cuda_fp16.h>
+#include "nmq_internal.h"
+
+namespace nmq {
+namespace dev {
+
+constexpr float kPi = 3.14159265358979323846f;
+constexpr float kInvPi = 0.31830988618379067154f;
+constexpr float kAlphaFloor = 1e-4f;          // proxy.py:32
+constexpr float kRhoClamp = 0.99994999874993749f;  // sqrt(1 - 1e-4), proxy.py:33
+constexpr float kLeaky = 0.01f;               // mlp.py:16
+
+struct V3 {
+  float x, y, z;
+};
+__device__ __forceinline__ V3 v3(float x, float y, float z) { return {x, y, z}; }
+__device__ __forceinline__ float dot(V3 a, V3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+  return {fmaf(a.y, b.z, -a.z * b.y), fmaf(a.z, b.x, -a.x * b.z), fmaf(a.x, b.y, -a.y * b.x)};
+}
+__device__ __forceinline__ V3 scale(V3 a, float s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+
+__device__ __forceinline__ V3 ldg3(const float* p, int64_t i) {
+  return {__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2)};
+}
+__device__ __forceinline__ void stg3(float* p, int64_t i, V3 v) {
+  p[3 * i] = v.x;
+  p[3 * i + 1] = v.y;
+  p[3 * i + 2] = v.z;
+}
+
+// ---------------------------------------------------------------------------
+// Latent fetch.  choose_level (latent.py:76-82) is exact in fp32 for fp32
+// inputs (clip/floor/subtract of a float are exact).  Texel coordinates follow
+// _taps (latent.py:56-74) in float64 exactly like the reference, so the level
+// and the four tap indices are bit-identical; the blend is fp32 FMA over the
+// fp16 texels (the reference sums in float64 and rounds to fp32).
+struct Taps {
+  int64_t base;      // texel index of the level origin
+  int32_t x0, x1, y0, y1, w;
+  float fx, fy;
+};
+
+__device__ __forceinline__ int choose_level(const MatParams& m, float lod, float urr) {
+  const float top = (float)(m.n_levels - 1);
+  float l = fminf(fmaxf(lod, 0.f), top);
+  const float lo = floorf(l);
+  int c = (int)lo + ((urr < (l - lo)) ? 1 : 0);
+  c = c < 0 ? 0 : c;
+  c = c > m.n_levels - 1 ? m.n_levels - 1 : c;
+  return c;
+}
+
+__device__ __forceinline__ int64_t wrap_index(double f, int32_t n, bool pow2) {
+  // Python's non-negative modulo of floor(f) (latent.py:65-68)
+  const int64_t i = (int64_t)f;
+  if (pow2) return i & (int64_t)(n - 1);
+  int64_t r = i % n;
+  return r < 0 ? r + n : r;
+}
+
+__device__ __forceinline__ Taps make_taps(const MatParams& m, int level, float u, float v) {
+  const LevelDesc L = m.lv[level];
+  const double x = fma((double)u, (double)L.w, -0.5);
+  const double y = fma((double)v, (double)L.h, -0.5);
+  const double xf = floor(x), yf = floor(y);
+  Taps t;
+  t.fx = (float)(x - xf);
+  t.fy = (float)(y - yf);
+  const bool p2 = m.pow2 != 0;
+  const int64_t x0 = wrap_index(xf, L.w, p2);
+  const int64_t y0 = wrap_index(yf, L.h, p2);
+  t.x0 = (int32_t)x0;
+  t.y0 = (int32_t)y0;
+  t.x1 = (x0 + 1 == L.w) ? 0 : (int32_t)x0 + 1;
+  t.y1 = (y0 + 1 == L.h) ? 0 : (int32_t)y0 + 1;
+  t.w = L.w;
+  t.base = L.off;
+  return t;
+}
+
+__device__ __forceinline__ void blend_texel(float (&z)[8], uint4 t, float w) {
+  const __half2* h = reinterpret_cast<const __half2*>(&t);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 f = __half22float2(h[k]);
+    z[2 * k] = fmaf(f.x, w, z[2 * k]);
+    z[2 * k + 1] = fmaf(f.y, w, z[2 * k + 1]);
+  }
+}
+
+__device__ __forceinline__ void blend_texel32(float (&z)[8], const float4* p, float w) {
+  const float4 a = __ldg(p), b = __ldg(p + 1);
+  z[0] = fmaf(a.x, w, z[0]); z[1] = fmaf(a.y, w, z[1]);
+  z[2] = fmaf(a.z, w, z[2]); z[3] = fmaf(a.w, w, z[3]);
+  z[4] = fmaf(b.x, w, z[4]); z[5] = fmaf(b.y, w, z[5]);
+  z[6] = fmaf(b.z, w, z[6]); z[7] = fmaf(b.w, w, z[7]);
+}
+
+// Bilinear fetch of 8 channels.  Loads are issued together (4 x LDG.128).
+__device__ __forceinline__ void fetch_taps(const MatParams& m, const Taps& t, float (&z)[8]) {
+  const int64_t r0 = (int64_t)t.y0 * t.w, r1 = (int64_t)t.y1 * t.w;
+  if (m.texel_fp32) {  // generic fp32 pyramid (LatentPyramid master copy)
+    const float4* lat = reinterpret_cast<const float4*>(m.latent) + 2 * t.base;
+    const float gx = 1.f - t.fx, gy = 1.f - t.fy;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = 0.f;
+    blend_texel32(z, lat + 2 * (r0 + t.x0), gx * gy);
+    blend_texel32(z, lat + 2 * (r0 + t.x1), t.fx * gy);
+    blend_texel32(z, lat + 2 * (r1 + t.x0), gx * t.fy);
+    blend_texel32(z, lat + 2 * (r1 + t.x1), t.fx * t.fy);
+    return;
+  }
+  const uint4* lat = m.latent + t.base;
+  const uint4 a = __ldg(lat + r0 + t.x0);
+  const uint4 b = __ldg(lat + r0 + t.x1);
+  const uint4 c = __ldg(lat + r1 + t.x0);
+  const uint4 d = __ldg(lat + r1 + t.x1);
+  const float gx = 1.f - t.fx, gy = 1.f - t.fy;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) z[k] = 0.f;
+  blend_texel(z, a, gx * gy);
+  blend_texel(z, b, t.fx * gy);
+  blend_texel(z, c, gx * t.fy);
+  blend_texel(z, d, t.fx * t.fy);
+}
+
+// ---------------------------------------------------------------------------
+// Learned shading frame (neural.py:207-233 + geom.py:82-89 fallback).
+struct Frame {
+  V3 t, b, n;
+};
+
+__device__ __forceinline__ V3 fallback_tangent(V3 n) {
+  // n x e_k, k = argmin |n_k| (first index on ties), normalized
+  const float ax = fabsf(n.x), ay = fabsf(n.y), az = fabsf(n.z);
+  V3 e;
+  if (ax <= ay && ax <= az) e = v3(1.f, 0.f, 0.f);
+  else if (ay <= az) e = v3(0.f, 1.f, 0.f);
+  else e = v3(0.f, 0.f, 1.f);
+  V3 c = cross(n, e);
+  return scale(c, rsqrtf(dot(c, c)));
+}
+
+__device__ __forceinline__ Frame frame_from_raw(const float* r) {
+  V3 rn = v3(r[0], r[1], r[2]);
+  V3 rt = v3(r[3], r[4], r[5]);
+  const float ln = sqrtf(dot(rn, rn));
+  V3 n = scale(rn, 1.f / fmaxf(ln, 1e-12f));
+  V3 c = cross(n, rt);
+  float lc = sqrtf(dot(c, c));
+  if (lc < 1e-8f) {
+    rt = fallback_tangent(n);
+    c = cross(n, rt);
+    lc = sqrtf(dot(c, c));
+  }
+  Frame f;
+  f.b = scale(c, 1.f / fmaxf(lc, 1e-12f));
+  f.n = n;
+  f.t = cross(f.b, n);
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// BRDF output map (neural.py:37-39): max(expm1(min(y, 60)), 0)
+__device__ __forceinline__ float brdf_output(float y) {
+  return y > 0.f ? expm1f(fminf(y, 60.f)) : 0.f;
+}
+
+// ---------------------------------------------------------------------------
+// Proxy parameter maps (neural.py:46-71, 317-331) and floors (proxy.py:42-50)
+__device__ __forceinline__ float quad_tanh(float x) {
+  const float ax = fabsf(x);
+  if (ax > 1e18f) return copysignf(1.f, x);
+  const float r = x * (1.f + 0.5f * ax) / (1.f + ax + 0.5f * x * x);
+  return fminf(fmaxf(r, -1.f), 1.f);
+}
+__device__ __forceinline__ float quad_sinh(float x) { return x * (1.f + x * x * (1.f / 6.f)); }
+
+struct Proxy {
+  float wd, ws, mdx, mdy, ax, ay, rho, msx, msy;
+};
+
+__device__ __forceinline__ Proxy proxy_from_raw(const float* raw, bool isotropic) {
+  Proxy p;
+  if (isotropic) {
+    p.wd = 0.5f * (quad_tanh(raw[0]) + 1.f);
+    p.ws = 1.f - p.wd;
+    const float a = 0.5f * (quad_tanh(raw[1]) + 1.f);
+    p.ax = p.ay = a;
+    p.mdx = p.mdy = p.rho = p.msx = p.msy = 0.f;
+  } else {
+    const float a = raw[0], b = raw[3];
+    const float m = fmaxf(a, b);
+    const float ea = expf(a - m), eb = expf(b - m);
+    const float inv = 1.f / (ea + eb);
+    p.wd = ea * inv;
+    p.ws = eb * inv;
+    p.mdx = quad_sinh(raw[1]);
+    p.mdy = quad_sinh(raw[2]);
+    p.ax = 0.5f * (quad_tanh(raw[4]) + 1.f);
+    p.ay = 0.5f * (quad_tanh(raw[5]) + 1.f);
+    p.rho = quad_tanh(raw[6]);
+    p.msx = quad_sinh(raw[7]);
+    p.msy = quad_sinh(raw[8]);
+  }
+  p.ax = fmaxf(p.ax, kAlphaFloor);
+  p.ay = fmaxf(p.ay, kAlphaFloor);
+  p.rho = fminf(fmaxf(p.rho, -kRhoClamp), kRhoClamp);
+  return p;
+}
+
+__device__ __forceinline__ Proxy load_proxy(const float* p9, int64_t i) {
+  const float* q = p9 + 9 * i;
+  Proxy p;
+  p.wd = __ldg(q + 0); p.ws = __ldg(q + 1);
+  p.mdx = __ldg(q + 2); p.mdy = __ldg(q + 3);
+  p.ax = fmaxf(__ldg(q + 4), kAlphaFloor); p.ay = fmaxf(__ldg(q + 5), kAlphaFloor);
+  p.rho = fminf(fmaxf(__ldg(q + 6), -kRhoClamp), kRhoClamp);
+  p.msx = __ldg(q + 7); p.msy = __ldg(q + 8);
+  return p;
+}
+__device__ __forceinline__ void store_proxy(float* p9, int64_t i, const Proxy& p) {
+  float* q = p9 + 9 * i;
+  q[0] = p.wd; q[1] = p.ws; q[2] = p.mdx; q[3] = p.mdy; q[4] = p.ax;
+  q[5] = p.ay; q[6] = p.rho; q[7] = p.msx; q[8] = p.msy;
+}
+
+__device__ __forceinline__ float proxy_s(const Proxy& p) {
+  // sqrt(1 - rho^2) written as sqrt((1-rho)(1+rho)) for accuracy near |rho|=1
+  return sqrtf((1.f - p.rho) * (1.f + p.rho));
+}
+
+__device__ __forceinline__ V3 diffuse_axis(const Proxy& p) {
+  V3 v = v3(-p.mdx, -p.mdy, 1.f);
+  return scale(v, rsqrtf(dot(v, v)));
+}
+
+// proxy.py:114-135
+__device__ __forceinline__ float proxy_pdf(const Proxy& p, V3 wi, V3 wo) {
+  const V3 nd = diffuse_axis(p);
+  const float pd = fmaxf(dot(wo, nd), 0.f) * kInvPi;
+  float ps = 0.f;
+  V3 h = add(wi, wo);
+  const float hl2 = dot(h, h);
+  const float hl = sqrtf(hl2);
+  if (hl > 1e-9f) {
+    h = scale(h, 1.f / hl);
+    if (h.z < 0.f) h = scale(h, -1.f);
+    if (h.z > 0.f) {
+      const float s = proxy_s(p);
+      const float q0 = fmaf(p.msx, h.z, h.x) / p.ax;
+      const float q1 = (fmaf(p.msy, h.z, h.y) / p.ay - p.rho * q0) / s;
+      const float q2 = fmaf(q0, q0, fmaf(q1, q1, h.z * h.z));
+      const float coh = fmaxf(fabsf(dot(wo, h)), 1e-12f);
+      const float det = p.ax * p.ay * s;
+      const float val = h.z / (det * (4.f * kPi) * q2 * q2 * coh);
+      ps = fmaxf(val, 0.f);
+    }
+  }
+  return p.wd * pd + p.ws * ps;
+}
+
+// proxy.py:138-180.  sin/cos of 2*pi*u via sincospif (exact argument), and
+// sqrt(1-cos^2) rewritten as sqrt(tan2)*cos (same value, no cancellation).
+__device__ __forceinline__ V3 proxy_sample(const Proxy& p, V3 wi, float u0, float u1, float u2) {
+  float sp, cp;
+  sincospif(2.f * u2, &sp, &cp);
+  if (u0 < p.wd) {
+    // diffuse: normalize(n_d + uniform_sphere(u1,u2)), |.| floor 1e-9
+    const float z = 1.f - 2.f * u1;
+    const float r = 2.f * sqrtf(fmaxf(u1 * (1.f - u1), 0.f));
+    const V3 g = add(diffuse_axis(p), v3(r * cp, r * sp, z));
+    const float gl = fmaxf(sqrtf(dot(g, g)), 1e-9f);
+    return scale(g, 1.f / gl);
+  }
+  const float tan2 = u1 / fmaxf(1.f - u1, 1e-12f);
+  const float ct = rsqrtf(1.f + tan2);
+  const float st = sqrtf(tan2) * ct;
+  const V3 m = v3(st * cp, st * sp, ct);
+  const float s = proxy_s(p);
+  // g = M m, M = [[ax, 0, -msx], [ay rho, ay s, -msy], [0, 0, 1]]
+  const V3 g = v3(fmaf(p.ax, m.x, -p.msx * m.z), fmaf(p.ay * p.rho, m.x, fmaf(p.ay * s, m.y, -p.msy * m.z)),
+                  m.z);
+  const V3 h = scale(g, 1.f / fmaxf(sqrtf(dot(g, g)), 1e-12f));
+  const float d = 2.f * dot(wi, h);
+  return v3(fmaf(d, h.x, -wi.x), fmaf(d, h.y, -wi.y), fmaf(d, h.z, -wi.z));
+}
+
+}  // namespace dev
+}  // namespace nmq

@@ -1,0 +1,103 @@
+// nmq_internal.h — material layout shared by the host (nmq_abi.cu) and the
+// kernels (nmq_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nmq {
+
+constexpr int kMaxLevels = 24;
+constexpr int kMaxLayers = 16;
+constexpr int kTile = 128;        // queries per MMA tile (M = 128, one per thread)
+constexpr int kMaxWidth = 64;     // max padded layer width handled by the kernels
+constexpr int kBiasCol = 504;     // TMEM column holding the shared [1,0..] bias chunk
+constexpr int kTmemCols = 512;
+
+struct LevelDesc {
+  int32_t w, h;
+  int64_t off;  // texel offset of the level in the latent buffer
+};
+
+// One MMA layer.  B operand (weights) lives in SMEM at `b_off` in the
+// chunk-major K-major layout described in tc.cuh, N padded to n_pad rows.
+//   first == 1: the input vector x (fan_in values + a 1.0 bias slot at
+//               index fan_in) is written to TMEM as K = ksteps*16 fp16.
+//   first == 0: input = previous layer's activation split hi/lo
+//               (K = 2*in_pad) followed by the shared bias chunk (K = 16).
+struct LayerDesc {
+  uint32_t b_off;
+  uint16_t n_pad;
+  uint16_t in_pad;
+  uint8_t ksteps;
+  uint8_t first;
+  uint8_t act;      // 0 linear, 1 leaky
+  uint8_t out;      // true (unpadded) output width
+};
+
+struct MatParams {
+  const uint4* latent;  // 16 B per texel (8 x fp16), or 32 B (8 x fp32) if texel_fp32
+  int32_t n_levels;
+  int32_t pow2;         // every level is a power of two in both dims
+  int32_t texel_fp32;
+  int32_t has_brdf, has_sampler;
+  LevelDesc lv[kMaxLevels];
+  const uint4* wblob;   // packed weights (global), copied to SMEM per CTA
+  uint32_t wblob_bytes;
+  int32_t use_frames, n_frames, albedo, isotropic;
+  int32_t frame_layer;            // layer index or -1
+  int32_t brdf_first, brdf_count; // layer range
+  int32_t samp_first, samp_count;
+  int32_t brdf_in;                // fan_in of the first BRDF layer (8 + 6*n_frames or 14)
+  int32_t dmax;                   // max n_pad / in_pad over all layers (16/32/48/64)
+  LayerDesc layers[kMaxLayers];
+};
+
+enum Mode : int {
+  kModeFetch = 0,
+  kModeEval = 1,       // fetch + eval
+  kModeEvalZ = 2,      // eval from z
+  kModeProxyZ = 3,     // infer_proxy from z
+  kModeSamplePdf = 4,  // fetch + sampler + sample + pdf
+  kModeQuery = 5,      // fetch + eval + sampler + sample + pdf
+};
+
+struct QueryArgs {
+  int64_t n;
+  const float* uv;
+  const float* lod;
+  int32_t lod_stride;
+  const float* u_rr;
+  const float* z;
+  const float* wi;
+  const float* wo;
+  const float* u3;
+  const int32_t* idx;   // optional indirection (binned multi-material): query = idx[i]
+  float* rgb;
+  float* albedo;
+  float* ws;
+  float* pdf;
+  float* params9;
+  float* z_out;
+  int32_t* level;
+  int32_t* taps;
+  float* wts;
+};
+
+// launchers (nmq_kernels.cu); return cudaError_t of the launch
+cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s,
+                         int groups_override = 0);
+cudaError_t launch_fetch(const MatParams& mp, const QueryArgs& a, cudaStream_t s);
+cudaError_t launch_sample(int64_t n, const float* p9, const float* wi, const float* u3,
+                          float* wo, cudaStream_t s);
+cudaError_t launch_pdf(int64_t n, const float* p9, const float* wi, const float* wo, float* pdf,
+                       cudaStream_t s);
+// binning for multi-material (counts -> offsets -> scatter of query indices)
+cudaError_t launch_bin(int64_t n, int32_t n_mats, const int32_t* mat_id, int32_t* counts,
+                       int32_t* offsets, int32_t* order, cudaStream_t s);
+cudaError_t launch_eval_divergent(const MatParams* mps_dev, int32_t n_mats, const int32_t* mat_id,
+                                  const QueryArgs& a, uint32_t max_wblob, int32_t dmax,
+                                  cudaStream_t s);
+int smem_bytes_for(const MatParams& mp);
+extern int64_t g_launches;
+
+}  // namespace nmq

@@ -1,0 +1,475 @@
+// nmq_kernels.cu — fused sm_100a kernels of the neural-material query path.
+//
+// Execution model:
+//  * A CTA holds G "tile groups" of 128 threads.  A tile group owns one tile
+//    of 128 queries at a time, one query per thread, and loops persistently
+//    over tiles.  Weights of every network are staged ONCE per CTA in SMEM in
+//    the UMMA K-major chunk layout (B operand).
+//  * Per MLP layer a tile group writes its activations as fp16 into its
+//    private TMEM region (A operand, tcgen05.st, lane = query), one elected
+//    thread issues tcgen05.mma (A from TMEM, B from SMEM, D fp32 in TMEM) and
+//    commits to the group's mbarrier; the threads then read D back with
+//    tcgen05.ld (lane = query) and run the per-query nonlinear code.
+//  * The reference keeps hidden activations in fp32 (mlp.py:205-207).  To
+//    match it with fp16 tensor-core inputs every hidden activation a is
+//    split a = hi + lo (hi = fp16(a), lo = fp16(a - hi)) and the layer runs
+//    W*[hi; lo] with the weights duplicated along K — exact to ~2^-22.
+//    Biases ride along as an extra K column against a constant 1.0.
+#include <cstdio>
+#include "tc.cuh"
+#include "nmq_device.cuh"
+#include "nmq_internal.h"
+
+namespace nmq {
+
+int64_t g_launches = 0;
+
+namespace {
+
+using namespace dev;
+
+struct Group {
+  uint32_t d0, a0;    // TMEM column of the group's D / A region (lane 0)
+  uint32_t lane;      // this warp's TMEM lane field
+  uint32_t bias_col;  // shared constant chunk
+  uint64_t* bar;
+  uint32_t phase;
+  uint32_t bar_id;
+  uint32_t smem_w;
+  bool leader;
+};
+
+__device__ __forceinline__ uint32_t h2bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// Issue one MLP layer for the calling tile group (all 128 threads call).
+__device__ __forceinline__ void run_layer(const LayerDesc& L, Group& g) {
+  tc::tmem_st_wait();
+  tc::tc_fence_before();
+  tc::named_bar(g.bar_id, 128);
+  if (g.leader) {
+    tc::tc_fence_after();
+    const uint32_t idesc = tc::idesc_f16(128, L.n_pad);
+    const uint32_t lbo = (uint32_t)L.n_pad * 16u;
+    const uint32_t b0 = g.smem_w + L.b_off;
+    if (L.first) {
+      for (uint32_t s = 0; s < L.ksteps; ++s)
+        tc::mma_ts(g.d0, g.a0 + 8 * s, tc::smem_desc(b0 + s * 2 * lbo, lbo, 128), idesc, s > 0);
+    } else {
+      const uint32_t nhl = 2u * (L.in_pad / 16u);
+      for (uint32_t s = 0; s < nhl; ++s)
+        tc::mma_ts(g.d0, g.a0 + 8 * s, tc::smem_desc(b0 + s * 2 * lbo, lbo, 128), idesc, s > 0);
+      tc::mma_ts(g.d0, g.bias_col, tc::smem_desc(b0 + nhl * 2 * lbo, lbo, 128), idesc, 1);
+    }
+    tc::mma_commit(g.bar);
+  }
+  tc::mbar_wait(g.bar, g.phase);
+  g.phase ^= 1u;
+  tc::tc_fence_after();
+}
+
+// First-layer input: x[0..2*NC) as fp16 pairs into A columns [0, NC)
+template <int NC>
+__device__ __forceinline__ void write_input(const Group& g, const float* x) {
+  uint32_t r[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) r[j] = h2bits(__floats2half2_rn(x[2 * j], x[2 * j + 1]));
+  if constexpr (NC == 8) {
+    tc::tmem_st8(g.lane + g.a0, r);
+  } else {
+#pragma unroll
+    for (int c = 0; c < NC; c += 8) {
+      uint32_t q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = r[c + j];
+      tc::tmem_st8(g.lane + g.a0 + c, q);
+    }
+  }
+}
+
+// Hidden epilogue: D[0, width) -> act -> (hi, lo) fp16 into A.
+__device__ __forceinline__ void hidden_epilogue(const Group& g, uint32_t width, bool leaky) {
+  const uint32_t half_w = width / 2;
+  for (uint32_t c0 = 0; c0 < width; c0 += 16) {
+    uint32_t r[16];
+    tc::tmem_ld16(g.lane + g.d0 + c0, r);
+    tc::tmem_ld_wait();
+    uint32_t hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      float a = __uint_as_float(r[2 * j]), b = __uint_as_float(r[2 * j + 1]);
+      if (leaky) {
+        a = fmaxf(a, kLeaky * a);
+        b = fmaxf(b, kLeaky * b);
+      }
+      const __half2 h = __floats2half2_rn(a, b);
+      const float2 hf = __half22float2(h);
+      hi[j] = h2bits(h);
+      lo[j] = h2bits(__floats2half2_rn(a - hf.x, b - hf.y));
+    }
+    tc::tmem_st8(g.lane + g.a0 + c0 / 2, hi);
+    tc::tmem_st8(g.lane + g.a0 + half_w + c0 / 2, lo);
+  }
+}
+
+// Output layer: first 16 columns of D
+__device__ __forceinline__ void output_epilogue(const Group& g, float (&y)[16]) {
+  uint32_t r[16];
+  tc::tmem_ld16(g.lane + g.d0, r);
+  tc::tmem_ld_wait();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) y[j] = __uint_as_float(r[j]);
+}
+
+// Run a chain of layers [first, first+count) whose first layer input is
+// already in A.  Leaves the last layer's raw outputs in y.
+__device__ __forceinline__ void run_chain(const MatParams& mp, int first, int count, Group& g,
+                                          float (&y)[16]) {
+  run_layer(mp.layers[first], g);
+  for (int i = 1; i < count; ++i) {
+    const LayerDesc& prev = mp.layers[first + i - 1];
+    hidden_epilogue(g, prev.n_pad, prev.act != 0);
+    run_layer(mp.layers[first + i], g);
+  }
+  output_epilogue(g, y);
+}
+
+__device__ __forceinline__ void load_z(const float* z, int64_t q, float (&out)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(z + 8 * q));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(z + 8 * q + 4));
+  out[0] = a.x; out[1] = a.y; out[2] = a.z; out[3] = a.w;
+  out[4] = b.x; out[5] = b.y; out[6] = b.z; out[7] = b.w;
+}
+
+// BRDF decode of one query given z; returns raw decoder outputs in y.
+__device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const float (&z)[8],
+                                            V3 wi, V3 wo, float (&y)[16]) {
+  float x[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) x[k] = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = z[k];
+  if (mp.use_frames) {
+    float xf[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) xf[k] = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) xf[k] = z[k];
+    xf[8] = 1.f;  // bias slot
+    write_input<8>(g, xf);
+    run_layer(mp.layers[mp.frame_layer], g);
+    float raw[16];
+    output_epilogue(g, raw);
+    // frames_from_raw + transform (neural.py:207-233, 185-196, 284-286):
+    // decoder input [z, T1 wi, T2 wi, T1 wo, T2 wo] (tests/test_neural.py:105-118)
+    float ti[6], to[6];
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const Frame fr = frame_from_raw(raw + 6 * f);
+      ti[3 * f + 0] = dot(fr.t, wi);
+      ti[3 * f + 1] = dot(fr.b, wi);
+      ti[3 * f + 2] = dot(fr.n, wi);
+      to[3 * f + 0] = dot(fr.t, wo);
+      to[3 * f + 1] = dot(fr.b, wo);
+      to[3 * f + 2] = dot(fr.n, wo);
+    }
+    if (mp.n_frames == 2) {
+#pragma unroll
+      for (int k = 0; k < 6; ++k) {
+        x[8 + k] = ti[k];
+        x[14 + k] = to[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        x[8 + k] = ti[k];
+        x[11 + k] = to[k];
+      }
+    }
+  } else {
+    x[8] = wi.x; x[9] = wi.y; x[10] = wi.z;
+    x[11] = wo.x; x[12] = wo.y; x[13] = wo.z;
+  }
+  // bias slot of the first BRDF layer (index = fan_in)
+  if (mp.brdf_in == 20) x[20] = 1.f;  // 2 frames
+  else x[14] = 1.f;                   // 1 frame or no frames (host-validated)
+  if (mp.layers[mp.brdf_first].ksteps == 1) write_input<8>(g, x);
+  else write_input<16>(g, x);
+  run_chain(mp, mp.brdf_first, mp.brdf_count, g, y);
+}
+
+__device__ __forceinline__ Proxy sampler_decode(const MatParams& mp, Group& g,
+                                                const float (&z)[8], V3 wi) {
+  float x[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = z[k];
+  x[8] = wi.x; x[9] = wi.y; x[10] = wi.z;
+  x[11] = 1.f;  // bias slot
+#pragma unroll
+  for (int k = 12; k < 16; ++k) x[k] = 0.f;
+  write_input<8>(g, x);
+  float y[16];
+  run_chain(mp, mp.samp_first, mp.samp_count, g, y);
+  return proxy_from_raw(y, mp.isotropic != 0);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(384, 2)
+fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
+             uint32_t tmem_cols, uint32_t group_cols) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bars[8];
+  __shared__ uint32_t tbase_sh;
+  const int tid = threadIdx.x;
+  const int G = blockDim.x / 128;
+  const int gi = tid / 128, r = tid % 128;
+  const int warp = tid / 32;
+
+  // --- one-time CTA setup: weights -> SMEM, barriers, TMEM -----------------
+  {
+    const uint4* src = mp.wblob;
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    const uint32_t n16 = mp.wblob_bytes / 16;
+    for (uint32_t i = tid; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (tid < G) tc::mbar_init(&bars[tid], 1);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tbase_sh)), "r"(tmem_cols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_proxy_async_smem();
+  tc::fence_mbar_init();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tb = tbase_sh;
+  const uint32_t bias_col = tb + (uint32_t)G * group_cols;
+  if (warp < 4) {
+    const uint32_t v[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // fp16 1.0 at k = 0
+    tc::tmem_st8(bias_col + ((uint32_t)(warp * 32) << 16), v);
+    tc::tmem_st_wait();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+
+  Group g;
+  g.d0 = tb + (uint32_t)gi * group_cols;
+  g.a0 = g.d0 + group_cols / 2;
+  g.lane = (uint32_t)((warp & 3) * 32) << 16;
+  g.bias_col = bias_col;
+  g.bar = &bars[gi];
+  g.phase = 0;
+  g.bar_id = 1 + gi;
+  g.smem_w = tc::smem_u32(smem);
+  g.leader = (r == 0);
+
+  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  for (int64_t tile = (int64_t)blockIdx.x * G + gi; tile < ntiles;
+       tile += (int64_t)gridDim.x * G) {
+    const int64_t i = tile * kTile + r;
+    const bool valid = i < a.n;
+    const int64_t q = valid ? (a.idx ? (int64_t)__ldg(a.idx + i) : i) : 0;
+
+    V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
+    float z[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = 0.f;
+
+    if constexpr (MODE == kModeEvalZ || MODE == kModeProxyZ) {
+      if (valid) {
+        load_z(a.z, q, z);
+        wi = ldg3(a.wi, q);
+        if constexpr (MODE == kModeEvalZ) wo = ldg3(a.wo, q);
+      }
+    } else {
+      float u = 0.f, v = 0.f, lod = 0.f, urr = 0.f;
+      if (valid) {
+        const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + q);
+        u = uv.x;
+        v = uv.y;
+        lod = __ldg(a.lod + (a.lod_stride ? q : 0));
+        urr = __ldg(a.u_rr + q);
+        wi = ldg3(a.wi, q);
+        if constexpr (MODE != kModeSamplePdf) wo = ldg3(a.wo, q);
+      }
+      const int level = choose_level(mp, lod, urr);
+      const Taps t = make_taps(mp, level, u, v);
+      fetch_taps(mp, t, z);
+      if (valid && a.level) a.level[q] = level;
+    }
+
+    if constexpr (MODE == kModeEval || MODE == kModeEvalZ || MODE == kModeQuery) {
+      float y[16];
+      brdf_decode(mp, g, z, wi, wo, y);
+      if (valid) {
+        const bool up = (wi.z > 0.f) && (wo.z > 0.f);
+        const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
+                        : v3(0.f, 0.f, 0.f);
+        stg3(a.rgb, q, f);
+        if (mp.albedo && a.albedo) {
+          const V3 al = up ? v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f))
+                           : v3(0.f, 0.f, 0.f);
+          stg3(a.albedo, q, al);
+        }
+      }
+    }
+    if constexpr (MODE == kModeProxyZ || MODE == kModeSamplePdf || MODE == kModeQuery) {
+      const Proxy p = sampler_decode(mp, g, z, wi);
+      if (valid) {
+        if (a.params9) store_proxy(a.params9, q, p);
+        if constexpr (MODE != kModeProxyZ) {
+          const V3 u3 = ldg3(a.u3, q);
+          const V3 s = proxy_sample(p, wi, u3.x, u3.y, u3.z);
+          stg3(a.ws, q, s);
+          a.pdf[q] = proxy_pdf(p, wi, s);
+        }
+      }
+    }
+  }
+
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(tmem_cols)
+                 : "memory");
+  }
+}
+
+// --- plain SIMT kernels ------------------------------------------------------
+__global__ void __launch_bounds__(256) fetch_kernel(const __grid_constant__ MatParams mp,
+                                                    const __grid_constant__ QueryArgs a) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + i);
+    const float lod = __ldg(a.lod + (a.lod_stride ? i : 0));
+    const int level = choose_level(mp, lod, __ldg(a.u_rr + i));
+    const Taps t = make_taps(mp, level, uv.x, uv.y);
+    float z[8];
+    fetch_taps(mp, t, z);
+    if (a.z_out) {
+      float4* o = reinterpret_cast<float4*>(a.z_out + 8 * i);
+      o[0] = make_float4(z[0], z[1], z[2], z[3]);
+      o[1] = make_float4(z[4], z[5], z[6], z[7]);
+    }
+    if (a.level) a.level[i] = level;
+    if (a.taps) {
+      int32_t* p = a.taps + 8 * i;
+      p[0] = t.x0; p[1] = t.y0; p[2] = t.x1; p[3] = t.y0;
+      p[4] = t.x0; p[5] = t.y1; p[6] = t.x1; p[7] = t.y1;
+    }
+    if (a.wts) {
+      const float gx = 1.f - t.fx, gy = 1.f - t.fy;
+      float* w = a.wts + 4 * i;
+      w[0] = gx * gy; w[1] = t.fx * gy; w[2] = gx * t.fy; w[3] = t.fx * t.fy;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) sample_kernel(int64_t n, const float* __restrict__ p9,
+                                                     const float* __restrict__ wi,
+                                                     const float* __restrict__ u3,
+                                                     float* __restrict__ wo) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const Proxy p = load_proxy(p9, i);
+    const V3 u = ldg3(u3, i);
+    stg3(wo, i, proxy_sample(p, ldg3(wi, i), u.x, u.y, u.z));
+  }
+}
+
+__global__ void __launch_bounds__(256) pdf_kernel(int64_t n, const float* __restrict__ p9,
+                                                  const float* __restrict__ wi,
+                                                  const float* __restrict__ wo,
+                                                  float* __restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = proxy_pdf(load_proxy(p9, i), ldg3(wi, i), ldg3(wo, i));
+  }
+}
+
+int g_num_sms = 0;
+int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_num_sms;
+}
+
+int grid_for(int64_t n, int block) {
+  int64_t blocks = (n + block - 1) / block;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+template <int MODE>
+cudaError_t launch_mode(const MatParams& mp, const QueryArgs& a, cudaStream_t s, int groups) {
+  const uint32_t group_cols = 2u * (uint32_t)mp.dmax;
+  // tile groups per CTA; TMEM budget = G*group_cols + 8 (bias chunk), pow2
+  int G = groups > 0 ? groups : (mp.dmax <= 32 ? 3 : 3);
+  if (G > 3) G = 3;  // __launch_bounds__(384)
+  uint32_t need = (uint32_t)G * group_cols + 8u;
+  uint32_t cols = 32;
+  while (cols < need) cols <<= 1;
+  if (cols > 512) return cudaErrorInvalidValue;
+  const int ctas_per_sm = (int)(512 / cols) < 2 ? (int)(512 / cols) : 2;
+  const int smem = smem_bytes_for(mp);
+  auto kern = fused_kernel<MODE>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  int64_t grid = (int64_t)num_sms() * ctas_per_sm;
+  const int64_t need_ctas = (ntiles + G - 1) / G;
+  if (grid > need_ctas) grid = need_ctas;
+  if (grid < 1) grid = 1;
+  kern<<<(int)grid, G * 128, smem, s>>>(mp, a, cols, group_cols);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int smem_bytes_for(const MatParams& mp) { return (int)((mp.wblob_bytes + 127) / 128 * 128); }
+
+cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s,
+                         int groups) {
+  if (a.n <= 0) return cudaSuccess;
+  switch (mode) {
+    case kModeEval: return launch_mode<kModeEval>(mp, a, s, groups);
+    case kModeEvalZ: return launch_mode<kModeEvalZ>(mp, a, s, groups);
+    case kModeProxyZ: return launch_mode<kModeProxyZ>(mp, a, s, groups);
+    case kModeSamplePdf: return launch_mode<kModeSamplePdf>(mp, a, s, groups);
+    case kModeQuery: return launch_mode<kModeQuery>(mp, a, s, groups);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_fetch(const MatParams& mp, const QueryArgs& a, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  fetch_kernel<<<grid_for(a.n, 256), 256, 0, s>>>(mp, a);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sample(int64_t n, const float* p9, const float* wi, const float* u3, float* wo,
+                          cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  sample_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, p9, wi, u3, wo);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pdf(int64_t n, const float* p9, const float* wi, const float* wo, float* pdf,
+                       cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  pdf_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, p9, wi, wo, pdf);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace nmq

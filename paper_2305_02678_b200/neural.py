@@ -1,0 +1,342 @@
+"""Neural material query API — drop-in for ``neuralmat.neural``.
+
+Same names and argument meaning as the reference (neural.py:82-419):
+``NeuralMaterialConfig``, ``NeuralMaterial`` (``create``, ``half``,
+``invalidate_half``, ``clamp_warnings``), ``eval_brdf``, ``eval_material``,
+``infer_proxy``, ``save_archive`` / ``load_archive``.  Every query runs in
+the fused sm_100a kernels of ``libnmq.so``; there is no CPU path.
+
+Two fused entry points go beyond the reference's per-stage calls:
+``sample_pdf`` (fetch + sampler + sample + pdf, the renderer's BSDF-sampling
+step, render.py:368-372 + 401-402) and ``query`` (one fetch feeding eval,
+the sampler, sample and pdf).
+
+Precision: ``fp16=True`` is the reference's fp16 inference path
+(``NeuralMaterial.half()``: fp16 weights and texels, fp16-rounded layer-0
+inputs, fp32 accumulation and fp32 hidden activations), reproduced on the
+tensor cores with a hi/lo split of the hidden activations.
+"""
+
+import io
+import json
+import os
+import struct
+
+import numpy as np
+import torch
+
+from . import _io, _lib, mlp
+from ._handle import DeviceMaterial
+from .latent import LATENT_CHANNELS, LatentPyramid, read_pyramid, write_pyramid
+from .proxy import ProxyParams
+
+N_FRAMES = 2
+PARAM_DIM = 9  # encoder input width (texture.py:25)
+ARCHIVE_MAGIC = b"NMATARC1"
+
+
+def parse_arch(s):
+    n, w = s.lower().split("x")
+    return (int(w),) * int(n)
+
+
+class NeuralMaterialConfig:
+    def __init__(self, brdf_hidden="2x32", sampler_hidden="3x32", encoder_hidden="3x32",
+                 n_frames=N_FRAMES, albedo_head=False, use_frames=True, vanilla_extra_width=12,
+                 sampler_isotropic=False, param_dim=PARAM_DIM, channels=LATENT_CHANNELS):
+        self.brdf_hidden = brdf_hidden
+        self.sampler_hidden = sampler_hidden
+        self.encoder_hidden = encoder_hidden
+        self.n_frames = n_frames
+        self.albedo_head = albedo_head
+        self.use_frames = use_frames
+        self.vanilla_extra_width = vanilla_extra_width
+        self.sampler_isotropic = sampler_isotropic
+        self.param_dim = param_dim
+        self.channels = channels
+
+    def to_json(self):
+        return dict(self.__dict__)
+
+    @classmethod
+    def from_json(cls, d):
+        return cls(**d)
+
+
+class NeuralMaterial:
+    def __init__(self, cfg, encoder, frame_layer, brdf_decoder, sampler_decoder, latent=None):
+        self.cfg = cfg
+        self.encoder = encoder
+        self.frame_layer = frame_layer
+        self.brdf_decoder = brdf_decoder
+        self.sampler_decoder = sampler_decoder
+        self.latent = latent
+        self._half = None
+        self._dev = {}
+
+    @classmethod
+    def create(cls, cfg, rng):
+        """Random init consuming `rng` in the reference's order (neural.py:117-141):
+        frame layer, BRDF decoder, sampler decoder, encoder."""
+        c = cfg.channels
+        frame = None
+        if cfg.use_frames:
+            frame = mlp.Mlp.create((c, 6 * cfg.n_frames), rng, out_act=mlp.ACT_LINEAR,
+                                   weight_scale=0.1)
+            frame.layers[0].b[:] = np.tile([0.0, 0.0, 1.0, 1.0, 0.0, 0.0], cfg.n_frames)
+            brdf_sizes = (c + 6 * cfg.n_frames, *parse_arch(cfg.brdf_hidden),
+                          6 if cfg.albedo_head else 3)
+        else:
+            brdf_sizes = (c + 6, cfg.vanilla_extra_width, *parse_arch(cfg.brdf_hidden),
+                          6 if cfg.albedo_head else 3)
+        brdf = mlp.Mlp.create(brdf_sizes, rng)
+        sampler = mlp.Mlp.create((c + 3, *parse_arch(cfg.sampler_hidden),
+                                  2 if cfg.sampler_isotropic else 9), rng)
+        encoder = mlp.Mlp.create((cfg.param_dim, *parse_arch(cfg.encoder_hidden), c), rng)
+        return cls(cfg, encoder, frame, brdf, sampler)
+
+    # --- fp16 inference copies and their device residency ------------------------
+    def invalidate_half(self):
+        self._half = None
+        for h in self._dev.values():
+            h.close()
+        self._dev = {}
+
+    def half(self):
+        if self._half is None:
+            latent = None
+            if self.latent is not None:
+                latent = LatentPyramid([l.astype(np.float32) for l in self.latent.half_copy()])
+            self._half = {
+                "frame": mlp.quantize(self.frame_layer) if self.frame_layer is not None else None,
+                "brdf": mlp.quantize(self.brdf_decoder),
+                "sampler": mlp.quantize(self.sampler_decoder),
+                "latent": latent,
+            }
+        return self._half
+
+    def clamp_warnings(self):
+        h = self.half()
+        total = h["brdf"].clamped + h["sampler"].clamped
+        if h["frame"] is not None:
+            total += h["frame"].clamped
+        return total
+
+    def device_material(self, device=None):
+        """The immutable device copy (fp16 weights re-tiled for tcgen05, fp16
+        texels) on `device`, built once and cached like half()."""
+        dev = _io.cuda_device(device)
+        h = self._dev.get(dev.index)
+        if h is None:
+            q = self.half()
+            lat = self.latent
+            if isinstance(lat, DeviceLatent):
+                blob, w, hh, nl = lat.texels, lat.width, lat.height, lat.n_levels
+            elif lat is not None:
+                blob = np.concatenate([l.reshape(-1, LATENT_CHANNELS) for l in lat.half_copy()])
+                w, hh, nl = lat.width, lat.height, lat.n_levels
+            else:  # latent-less material: eval_brdf / infer_proxy from given codes
+                blob, w, hh, nl = np.zeros((1, 8), np.float16), 1, 1, 1
+            h = DeviceMaterial(dev, w, hh, nl, blob, False, q["frame"], q["brdf"], q["sampler"],
+                               use_frames=self.cfg.use_frames, n_frames=self.cfg.n_frames,
+                               albedo_head=self.cfg.albedo_head,
+                               sampler_isotropic=self.cfg.sampler_isotropic)
+            self._dev[dev.index] = h
+        return h
+
+
+class DeviceLatent:
+    """A latent pyramid that lives only on the device as fp16 texels
+    (texels, 8) — for synthetic 4K..15K pyramids too large to build on the
+    host.  Used as ``NeuralMaterial.latent`` by the benchmarks."""
+
+    def __init__(self, texels, width, height):
+        from .latent import level_shapes
+        shapes = level_shapes(width, height)
+        need = sum(h * w for h, w in shapes)
+        if texels.dtype != torch.float16 or tuple(texels.shape) != (need, LATENT_CHANNELS):
+            raise ValueError(f"expected ({need}, 8) fp16 texels")
+        self.texels = texels.contiguous()
+        self.width, self.height, self.n_levels = int(width), int(height), len(shapes)
+        self.shapes = shapes
+
+    @property
+    def channels(self):
+        return LATENT_CHANNELS
+
+    def half_copy(self):
+        out, ofs = [], 0
+        host = self.texels.cpu().numpy()
+        for h, w in self.shapes:
+            out.append(host[ofs:ofs + h * w].reshape(h, w, 8))
+            ofs += h * w
+        return out
+
+
+def _require_fp16(fp16):
+    if not fp16:
+        raise NotImplementedError(
+            "the GPU query path implements the reference's fp16 inference path "
+            "(pass fp16=True); the fp32 training-time path is not on the query path")
+
+
+def _launch(fn, *args):
+    _lib.check(fn(*args), fn.__name__)
+
+
+def eval_brdf(mat, z, wi, wo, fp16=False):
+    """BRDF values (and albedo when enabled) from latent codes (neural.py:273-300).
+    Directions below the horizon yield zero."""
+    _require_fp16(fp16)
+    np_mode = _io.is_numpy_like(z)
+    h = mat.device_material(None if np_mode else z.device)
+    dev = h.device
+    z_t = _io.as_rows(z, LATENT_CHANNELS, dev, "z")
+    n = z_t.shape[0]
+    wi_t = _io.as_rows(wi, 3, dev, "wi")
+    wo_t = _io.as_rows(wo, 3, dev, "wo")
+    if wi_t.shape[0] != n or wo_t.shape[0] != n:
+        raise ValueError("z, wi and wo must share the batch size")
+    f = _io.empty(n, 3, dev)
+    alb = _io.empty(n, 3, dev) if mat.cfg.albedo_head else None
+    lib = _lib.load()
+    _launch(lib.nm_eval_z, h.ptr, n, z_t.data_ptr(), wi_t.data_ptr(), wo_t.data_ptr(),
+            f.data_ptr(), _io.ptr(alb), _io.stream_ptr(dev))
+    return _io.out(f, np_mode), (None if alb is None else _io.out(alb, np_mode))
+
+
+class _QueryInputs:
+    def __init__(self, mat, uv, level, u_rr, need, **dirs):
+        self.np_mode = _io.is_numpy_like(uv)
+        self.h = mat.device_material(None if self.np_mode else uv.device)
+        dev = self.dev = self.h.device
+        self.uv = _io.as_rows(uv, 2, dev, "uv")
+        n = self.n = self.uv.shape[0]
+        self.lod, self.lod_stride = _io.as_vec(level, n, dev, "level")
+        self.urr, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+        for k in need:
+            t = _io.as_rows(dirs[k], 3, dev, k)
+            if t.shape[0] != n:
+                raise ValueError(f"{k}: batch {t.shape[0]} != {n}")
+            setattr(self, k, t)
+
+
+def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, out=None):
+    """Fetch (Russian-roulette level + bilinear) and decode in ONE fused
+    kernel, returning (f, albedo, chosen_level) (neural.py:303-309).
+    `out` may pass a preallocated (B,3) fp32 device tensor for f."""
+    _require_fp16(fp16)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), wi=wi, wo=wo)
+    f = out if out is not None else _io.empty(q.n, 3, q.dev)
+    alb = _io.empty(q.n, 3, q.dev) if mat.cfg.albedo_head else None
+    lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
+    lib = _lib.load()
+    _launch(lib.nm_eval, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
+            q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), f.data_ptr(), _io.ptr(alb),
+            _io.ptr(lv), _io.stream_ptr(q.dev))
+    return (_io.out(f, q.np_mode), None if alb is None else _io.out(alb, q.np_mode),
+            None if lv is None else _io.out(lv, q.np_mode, np.int64))
+
+
+def infer_proxy(mat, z, wi, fp16=False):
+    """Sampler parameters for latent codes and conditioning directions
+    (neural.py:353-362 + proxy_from_raw :317-331)."""
+    _require_fp16(fp16)
+    np_mode = _io.is_numpy_like(z)
+    h = mat.device_material(None if np_mode else z.device)
+    dev = h.device
+    z_t = _io.as_rows(z, LATENT_CHANNELS, dev, "z")
+    n = z_t.shape[0]
+    wi_t = _io.as_rows(wi, 3, dev, "wi")
+    if wi_t.shape[0] != n:
+        raise ValueError("z and wi must share the batch size")
+    p9 = _io.empty(n, 9, dev)
+    lib = _lib.load()
+    _launch(lib.nm_infer_proxy, h.ptr, n, z_t.data_ptr(), wi_t.data_ptr(), p9.data_ptr(),
+            _io.stream_ptr(dev))
+    return ProxyParams.from_block(p9, np_mode)
+
+
+def sample_pdf(mat, uv, level, u_rr, wi, u, fp16=True, return_params=False, return_level=False):
+    """Fused fetch + sampler decoder + proxy + sample + pdf: returns
+    (ws, pdf[, params][, level]) with ws = sample(params, wi, u), pdf = pdf(params, wi, ws)."""
+    _require_fp16(fp16)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "u"), wi=wi, u=u)
+    ws = _io.empty(q.n, 3, q.dev)
+    p = _io.empty(q.n, 1, q.dev)
+    p9 = _io.empty(q.n, 9, q.dev) if return_params else None
+    lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
+    lib = _lib.load()
+    _launch(lib.nm_sample_pdf, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
+            q.urr.data_ptr(), q.wi.data_ptr(), q.u.data_ptr(), ws.data_ptr(), p.data_ptr(),
+            _io.ptr(p9), _io.ptr(lv), _io.stream_ptr(q.dev))
+    res = (_io.out(ws, q.np_mode), _io.out(p, q.np_mode))
+    if return_params:
+        res = res + (ProxyParams.from_block(p9, q.np_mode),)
+    if return_level:
+        res = res + (_io.out(lv, q.np_mode, np.int64),)
+    return res
+
+
+def query(mat, uv, level, u_rr, wi, wo, u, fp16=True, return_level=False):
+    """One full query (fetch -> eval(wi, wo) -> proxy(wi) -> sample(u) -> pdf):
+    returns (f, ws, pdf[, level])."""
+    _require_fp16(fp16)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo", "u"), wi=wi, wo=wo, u=u)
+    f = _io.empty(q.n, 3, q.dev)
+    ws = _io.empty(q.n, 3, q.dev)
+    p = _io.empty(q.n, 1, q.dev)
+    lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
+    lib = _lib.load()
+    _launch(lib.nm_query, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
+            q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), q.u.data_ptr(), f.data_ptr(),
+            ws.data_ptr(), p.data_ptr(), _io.ptr(lv), _io.stream_ptr(q.dev))
+    res = (_io.out(f, q.np_mode), _io.out(ws, q.np_mode), _io.out(p, q.np_mode))
+    if return_level:
+        res = res + (_io.out(lv, q.np_mode, np.int64),)
+    return res
+
+
+# --- archive (NMATARC1, neural.py:368-419) -------------------------------------
+
+def save_archive(path, mat, include_encoder=False):
+    latent_name = None
+    if mat.latent is not None:
+        latent_name = os.path.basename(os.path.splitext(path)[0]) + ".latents"
+        with open(os.path.join(os.path.dirname(path), latent_name), "wb") as f:
+            write_pyramid(f, mat.latent)
+    header = {
+        "config": mat.cfg.to_json(),
+        "latent_file": latent_name,
+        "has_encoder": bool(include_encoder and mat.encoder is not None),
+        "clamped_warnings": mat.clamp_warnings(),
+    }
+    hbytes = json.dumps(header, sort_keys=True).encode("utf-8")
+    with open(path, "wb") as f:
+        f.write(ARCHIVE_MAGIC)
+        f.write(struct.pack("<I", len(hbytes)))
+        f.write(hbytes)
+        if mat.cfg.use_frames:
+            mlp.write_blob(f, mat.frame_layer)
+        mlp.write_blob(f, mat.brdf_decoder)
+        mlp.write_blob(f, mat.sampler_decoder)
+        if header["has_encoder"]:
+            mlp.write_blob(f, mat.encoder)
+
+
+def load_archive(path):
+    with open(path, "rb") as f:
+        if f.read(8) != ARCHIVE_MAGIC:
+            raise ValueError("not a neural material archive")
+        (hlen,) = struct.unpack("<I", f.read(4))
+        header = json.loads(f.read(hlen).decode("utf-8"))
+        cfg = NeuralMaterialConfig.from_json(header["config"])
+        frame = mlp.read_blob(f)[0] if cfg.use_frames else None
+        brdf = mlp.read_blob(f)[0]
+        sampler = mlp.read_blob(f)[0]
+        encoder = mlp.read_blob(f)[0] if header.get("has_encoder") else None
+    latent = None
+    if header.get("latent_file"):
+        with open(os.path.join(os.path.dirname(path), header["latent_file"]), "rb") as f:
+            latent = read_pyramid(f)
+    return NeuralMaterial(cfg, encoder, frame, brdf, sampler, latent)

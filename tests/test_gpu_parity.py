@@ -1,0 +1,172 @@
+"""GPU parity of the fused sm_100a kernels against the golden vectors the
+reference produced, and against the numpy oracle on fresh seeded inputs.
+
+Tolerances (stated in DESIGN.md §5, from the north star / SURVEY §8c4):
+  * chosen level and the 4 tap indices: bit-exact;
+  * z: |dz| <= 1e-6 * (sum_k |w_k t_k|) + 1e-7  (fp32 blend vs float64);
+  * RGB, albedo, proxy params: rel = |a-b|/(|b|+1e-2) max <= 1e-2, mean <= 1e-3;
+  * sampled direction: |dw| <= 1e-3 outside a 1e-3 guard band around the
+    lobe pick u0 = wd (lobe flips counted, must be rare);
+  * pdf: decoupled check (GPU params and reference params at the same
+    direction) rel max <= 1e-2, mean <= 1e-3.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, golden_config, golden_levels, golden_nets, load_golden, rel_err
+
+pytestmark = pytest.mark.gpu
+
+CASES = golden_cases()
+
+
+def our_material(g):
+    from paper_2305_02678_b200 import mlp, neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+
+    cfg = neural.NeuralMaterialConfig(**golden_config(g))
+
+    def net(prefix):
+        layers = golden_nets(g, prefix)
+        return mlp.Mlp([mlp.Layer(w, b, a) for w, b, a in layers]) if layers else None
+
+    mat = neural.NeuralMaterial(cfg, None, net("frame"), net("brdf"), net("sampler"))
+    mat.latent = LatentPyramid(golden_levels(g))
+    return mat
+
+
+def check_rel(a, b, max_tol=1e-2, mean_tol=1e-3, what=""):
+    r = rel_err(a, b)
+    assert np.all(np.isfinite(a)), f"{what}: non-finite"
+    i = int(np.argmax(r))
+    assert r.max() <= max_tol, (f"{what}: max rel {r.max():.3e} at {i}: got {np.ravel(a)[i]!r} "
+                                f"want {np.ravel(b)[i]!r}, mean {r.mean():.2e}")
+    assert r.mean() <= mean_tol, f"{what}: mean rel {r.mean():.3e}"
+    return r
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_fetch_bit_exact_levels_and_taps(name):
+    g = load_golden(name)
+    mat = our_material(g)
+    pyr = mat.half()["latent"]
+    z, chosen, xs, ys, wts = pyr.fetch(g["uv"], g["lod"], g["u_rr"], return_taps=True)
+    assert chosen.dtype == np.int64 and np.array_equal(chosen, g["chosen"])
+    if "xs" in g:
+        assert np.array_equal(xs, g["xs"]) and np.array_equal(ys, g["ys"])
+        np.testing.assert_allclose(wts, g["wts"], rtol=0, atol=1e-7)
+    # z tolerance relative to the magnitude of the blended terms
+    lv = golden_levels(g)
+    scale = np.ones(len(z))
+    if "xs" in g:
+        tex = np.stack([np.abs(lv[c].astype(np.float16).astype(np.float32)[ys[i], xs[i]]).max()
+                        for i, c in enumerate(chosen)])
+        scale = tex
+    dz = np.abs(z.astype(np.float64) - g["z"]).max(axis=1)
+    assert np.all(dz <= 1e-6 * scale + 1e-7), dz.max()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_eval_material_fused(name):
+    from paper_2305_02678_b200 import neural
+
+    g = load_golden(name)
+    mat = our_material(g)
+    f, albedo, chosen = neural.eval_material(mat, g["uv"], g["lod"], g["wi"], g["wo"], g["u_rr"],
+                                             fp16=True)
+    assert np.array_equal(chosen, g["chosen"])
+    check_rel(f, g["f"], what=f"{name} rgb")
+    if "albedo" in g:
+        check_rel(albedo, g["albedo"], what=f"{name} albedo")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_eval_brdf_from_codes(name):
+    from paper_2305_02678_b200 import neural
+
+    g = load_golden(name)
+    mat = our_material(g)
+    f, _ = neural.eval_brdf(mat, g["z"].astype(np.float32), g["wi"], g["wo"], fp16=True)
+    check_rel(f, g["f"], what=f"{name} eval_brdf")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_infer_proxy_and_pdf(name):
+    from paper_2305_02678_b200 import neural, proxy
+
+    g = load_golden(name)
+    mat = our_material(g)
+    p = neural.infer_proxy(mat, g["z"].astype(np.float32), g["wi"], fp16=True)
+    check_rel(p.as_array(), g["params"], what=f"{name} params")
+    # decoupled pdf: our params at the reference's direction
+    pw = proxy.pdf(p, g["wi"], g["wo"])
+    check_rel(pw, g["pdf_wo"], what=f"{name} pdf(wo)")
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_sample_pdf_fused(name):
+    from paper_2305_02678_b200 import neural
+
+    g = load_golden(name)
+    mat = our_material(g)
+    ws, pdf, p, chosen = neural.sample_pdf(mat, g["uv"], g["lod"], g["u_rr"], g["wi"], g["u3"],
+                                           return_params=True, return_level=True)
+    assert np.array_equal(chosen, g["chosen"])
+    check_rel(p.as_array(), g["params"], what=f"{name} params")
+    guard = np.abs(g["u3"][:, 0].astype(np.float64) - g["params"][:, 0]) >= 1e-3
+    flips = np.count_nonzero(~guard)
+    assert flips <= max(3, 0.01 * len(guard))
+    dw = np.abs(ws - g["ws"]).max(axis=1)
+    assert np.all(dw[guard] <= 1e-3), dw[guard].max()
+    # decoupled pdf: our params at the reference's sampled direction.  The
+    # specular pdf carries 1/|wo.h| and h = normalize(wi + wo): near grazing
+    # reflection (|wo.h| -> 0) rounding the direction to fp32 alone moves the
+    # pdf by ~eps/|wo.h|^2, so the strict bound applies where |wo.h| >= 1e-2
+    # (> 99% of samples; the excluded share is asserted).
+    from paper_2305_02678_b200 import proxy
+    h = g["wi"] + g["ws"]
+    h = h / np.linalg.norm(h, axis=1, keepdims=True)
+    well = np.abs(np.sum(g["ws"] * h, axis=1)) >= 1e-2
+    assert well.mean() > 0.99
+    check_rel(proxy.pdf(p, g["wi"], g["ws"])[well], g["pdf_ws"][well], what=f"{name} pdf(ws_ref)")
+    # the fused kernel's pdf is exactly pdf(params, wi, ws) of its own sample
+    own = proxy.pdf(p, g["wi"], ws)
+    np.testing.assert_allclose(pdf, own, rtol=1e-5, atol=1e-7)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_full_query_fused(name):
+    from paper_2305_02678_b200 import neural
+
+    g = load_golden(name)
+    mat = our_material(g)
+    f, ws, pdf, chosen = neural.query(mat, g["uv"], g["lod"], g["u_rr"], g["wi"], g["wo"], g["u3"],
+                                      return_level=True)
+    assert np.array_equal(chosen, g["chosen"])
+    check_rel(f, g["f"], what=f"{name} rgb")
+    guard = np.abs(g["u3"][:, 0].astype(np.float64) - g["params"][:, 0]) >= 1e-3
+    dw = np.abs(ws - g["ws"]).max(axis=1)
+    assert np.all(dw[guard] <= 1e-3)
+
+
+def test_proxy_sample_pdf_kat():
+    from paper_2305_02678_b200 import proxy
+
+    g = load_golden("proxy_kat")
+    b = g["params"]
+    p = proxy.ProxyParams(b[:, 0], b[:, 1], b[:, 2:4], b[:, 4:6], b[:, 6], b[:, 7:9])
+    ws = proxy.sample(p, g["wi"], g["u3"])
+    guard = np.abs(g["u3"][:, 0] - b[:, 0]) >= 1e-6
+    dw = np.abs(ws - g["ws"]).max(axis=1)
+    assert np.all(dw[guard] <= 1e-4), dw[guard].max()
+    check_rel(proxy.pdf(p, g["wi"], g["wo"]), g["pdf_wo"], max_tol=1e-3, mean_tol=1e-5,
+              what="pdf(wo)")
+    h = g["wi"] + g["ws"]
+    h = h / np.linalg.norm(h, axis=1, keepdims=True)
+    coh = np.abs(np.sum(g["ws"] * h, axis=1))
+    pw = proxy.pdf(p, g["wi"], g["ws"])
+    # fp32 vs float64: 1/|wo.h| conditioning near grazing reflection
+    check_rel(pw[guard & (coh >= 1e-2)], g["pdf_ws"][guard & (coh >= 1e-2)], max_tol=1e-3,
+              mean_tol=1e-5, what="pdf(ws)")
+    assert (coh >= 1e-2).mean() > 0.99

@@ -1,0 +1,94 @@
+"""Pin the numpy oracle (oracle/nm_oracle.py) to the golden vectors that the
+REAL reference produced (oracle/make_golden.py).  CPU only."""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, golden_config, golden_levels, golden_nets, load_golden
+from oracle import nm_oracle as O
+
+CASES = golden_cases()
+
+
+def oracle_material(g):
+    cfg = O.Config(**golden_config(g))
+    frame = O.Net(golden_nets(g, "frame")) if int(g["frame_n"]) else None
+    mat = O.Material(cfg, frame, O.Net(golden_nets(g, "brdf")), O.Net(golden_nets(g, "sampler")))
+    mat.latent = O.Pyramid(golden_levels(g))
+    return mat
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_matches_reference_fp16_path(name):
+    g = load_golden(name)
+    mat = oracle_material(g)
+    f, ws, pdf_ws, p, chosen = O.full_query(mat, g["uv"].astype(np.float64),
+                                            g["lod"].astype(np.float64),
+                                            g["u_rr"].astype(np.float64),
+                                            g["wi"].astype(np.float64),
+                                            g["wo"].astype(np.float64),
+                                            g["u3"].astype(np.float64))
+    assert np.array_equal(chosen, g["chosen"])
+    z, _ = mat.half()["latent"].fetch(g["uv"], g["lod"], g["u_rr"])
+    assert np.array_equal(z, g["z"])
+    np.testing.assert_allclose(f, g["f"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(p.as_array(), g["params"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(ws, g["ws"], rtol=1e-10, atol=1e-10)
+    np.testing.assert_allclose(pdf_ws, g["pdf_ws"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(O.pdf(p, g["wi"], g["wo"]), g["pdf_wo"], rtol=1e-9, atol=1e-12)
+    if "albedo" in g:
+        _, alb = O.eval_brdf(mat, z, g["wi"], g["wo"], fp16=True)
+        np.testing.assert_allclose(alb, g["albedo"], rtol=1e-12, atol=1e-12)
+
+
+@pytest.mark.parametrize("name", [c for c in CASES if "xs" in load_golden(c)])
+def test_oracle_taps_bit_exact(name):
+    g = load_golden(name)
+    pyr = oracle_material(g).half()["latent"]
+    for lv in np.unique(g["chosen"]):
+        m = g["chosen"] == lv
+        xs, ys, wts = pyr.taps(int(lv), g["uv"][m].astype(np.float64))
+        assert np.array_equal(xs, g["xs"][m]) and np.array_equal(ys, g["ys"][m])
+        assert np.array_equal(wts, g["wts"][m])
+
+
+def test_oracle_fp32_path_matches_reference():
+    g = load_golden("c1_2x32")
+    mat = oracle_material(g)
+    f32, _ = O.eval_brdf(mat, g["z"], g["wi"], g["wo"], fp16=False)
+    np.testing.assert_allclose(f32, g["f_fp32path"], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_proxy_kat():
+    g = load_golden("proxy_kat")
+    b = g["params"].astype(np.float64)
+    p = O.Proxy(b[:, 0], b[:, 1], b[:, 2:4], b[:, 4:6], b[:, 6], b[:, 7:9])
+    wi = g["wi"].astype(np.float64)
+    ws = O.sample(p, wi, g["u3"].astype(np.float64))
+    np.testing.assert_allclose(ws, g["ws"], rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(O.pdf(p, wi, ws), g["pdf_ws"], rtol=1e-10, atol=1e-14)
+    np.testing.assert_allclose(O.pdf(p, wi, g["wo"]), g["pdf_wo"], rtol=1e-10, atol=1e-14)
+
+
+def test_oracle_random_material_matches_reference_init():
+    """Oracle init consumes the RNG like the reference (neural.py:117-141)."""
+    for name in ("c1_2x32", "vanilla", "isotropic"):
+        g = load_golden(name)
+        mat = O.Material.random(O.Config(**golden_config(g)), np.random.default_rng(int(g["seed"])))
+        for prefix, net in (("brdf", mat.brdf), ("sampler", mat.sampler), ("frame", mat.frame)):
+            if net is None:
+                continue
+            for (w, b, a), (gw, gb, ga) in zip(net.layers, golden_nets(g, prefix)):
+                assert np.array_equal(w, gw) and np.array_equal(b, gb) and a == ga
+
+
+def test_oracle_zenith_pdf_goldens():
+    """tests/test_proxy.py:39-55 analytic goldens."""
+    z = np.array([[0.0, 0.0, 1.0]])
+
+    def mk(wd, alpha):
+        return O.Proxy(wd, 1 - wd, [[0, 0]], [alpha], 0.0, [[0, 0]])
+
+    assert O.pdf(mk(1.0, (0.5, 0.5)), z, z)[0] == pytest.approx(1 / np.pi, rel=1e-12)
+    assert O.pdf(mk(0.0, (1.0, 1.0)), z, z)[0] == pytest.approx(1 / (4 * np.pi), rel=1e-9)
+    assert O.pdf(mk(0.5, (1.0, 1.0)), z, z)[0] == pytest.approx(0.5 / np.pi + 0.5 / (4 * np.pi), rel=1e-9)
