@@ -1,0 +1,452 @@
+"""Benchmark of the neural-material query path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c3|full]
+
+Default workload (BASELINE.json configs[1], "C2"): one random-init 2x32
+material with a 4096^2 latent pyramid (13 levels, fp16), 1920x1080 =
+2,073,600 coherent fused eval queries (fetch + frames + BRDF decoder) per
+step per GPU.  Multi-GPU runs are weak-scaled pixel tiles (each rank owns a
+1080p tile of a larger frame, replicated material, no collective on the
+data path); `value` = all ranks' queries / max-over-ranks time.
+
+One JSON line on rank 0.  `value` = device-timed throughput with inputs in
+HBM (CUDA events, inputs rotating over 3 sets > L2); `e2e` = the public API
+(`neural.eval_material` on pinned host numpy buffers, H2D + kernel + D2H
+inside the timed region); `roofline` = the fused kernel's algorithmic bytes
+(fp32 I/O + 16 B per unique texel touched) / launch time vs measured HBM
+peak; `cpu_baseline` = the numpy oracle (restatement of the reference,
+oracle/nm_oracle.py) on the host cores for a bounded sample.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")  # the CPU baseline forks one worker per core
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+C2_N = 1920 * 1080
+C3_N = 1920 * 1080 * 16
+RES = 4096
+METRIC = "neural BRDF queries/sec (eval, sample+pdf) at 1/2/4/8 B200; % of roofline"
+FLOPS_EVAL = 2 * (8 * 12 + 20 * 32 + 32 * 32 + 32 * 3)          # 3712
+FLOPS_SAMPLE = 2 * (11 * 32 + 32 * 32 + 32 * 32 + 32 * 9)         # 5376
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+def dist_init(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if n_gpus != world:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML, sampled from the host between launches)
+
+class Clocks:
+    REASONS = {
+        0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+        0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle",
+        0x2: "applications_clocks_setting",
+    }
+
+    def __init__(self, index):
+        self.ok = False
+        self.samples = []
+        self.reasons = 0
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max = None
+
+    def sample(self):
+        if not self.ok:
+            return
+        try:
+            self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+            self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            pass
+
+    def report(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": [], "samples": 0}
+        names = [v for k, v in self.REASONS.items() if self.reasons & k and v != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes: fp32 I/O + 16 B per unique texel touched
+
+def unique_texels(mat_handle, q):
+    from paper_2305_02678_b200 import _lib
+    lib = _lib.load()
+    n = q["uv"].shape[0]
+    taps = torch.empty((n, 8), device="cuda", dtype=torch.int32)
+    lv = torch.empty((n,), device="cuda", dtype=torch.int32)
+    lod_stride = 1
+    _lib.check(lib.nm_fetch(mat_handle.ptr, n, q["uv"].data_ptr(), q["lod"].data_ptr(), lod_stride,
+                            q["u_rr"].data_ptr(), None, lv.data_ptr(), taps.data_ptr(), None,
+                            torch.cuda.current_stream().cuda_stream))
+    w, h, off = mat_handle.level_table()
+    w_t = torch.from_numpy(w.astype(np.int64)).cuda()
+    off_t = torch.from_numpy(off).cuda()
+    t = taps.view(n, 4, 2).long()
+    lvl = lv.long()
+    gid = off_t[lvl][:, None] + t[..., 1] * w_t[lvl][:, None] + t[..., 0]
+    return int(torch.unique(gid.reshape(-1)).numel())
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle restatement of the reference on host cores
+
+_CPU = {}
+
+
+def _cpu_eval_chunk(bounds):
+    from oracle import nm_oracle as O
+    s, e = bounds
+    d = _CPU
+    z, _ = d["pyr"].fetch(d["uv"][s:e], d["lod"][s:e], d["u_rr"][s:e])
+    if d["kind"] == "eval":
+        O.eval_brdf(d["mat"], z, d["wi"][s:e], d["wo"][s:e], fp16=True)
+    else:
+        p = O.infer_proxy(d["mat"], z, d["wi"][s:e], fp16=True)
+        ws = O.sample(p, d["wi"][s:e], d["u3"][s:e])
+        O.pdf(p, d["wi"][s:e], ws)
+    return e - s
+
+
+def cpu_setup(mat, q, n_sample, kind):
+    """Build the oracle material (same weights, same fp16 texels) and a
+    host copy of the first n_sample queries."""
+    from oracle import nm_oracle as O
+
+    def net(m):
+        return None if m is None else O.Net([(l.w, l.b, l.act) for l in m.layers])
+
+    cfg = O.Config(**mat.cfg.to_json())
+    om = O.Material(cfg, net(mat.frame_layer), net(mat.brdf_decoder), net(mat.sampler_decoder))
+    levels = [l.astype(np.float32) for l in mat.latent.half_copy()]
+    om._half = {"frame": O.quantize(om.frame) if om.frame is not None else None,
+                "brdf": O.quantize(om.brdf), "sampler": O.quantize(om.sampler),
+                "latent": O.Pyramid(levels)}
+    _CPU.clear()
+    _CPU.update(mat=om, pyr=om._half["latent"], kind=kind)
+    for k in ("uv", "lod", "u_rr", "wi", "wo", "u3"):
+        if k in q:
+            _CPU[k] = q[k][:n_sample].double().cpu().numpy()
+
+
+_POOL = {}
+
+
+def cpu_pool(workers):
+    """Forked worker pool created once (after cpu_setup), outside timing."""
+    import multiprocessing as mp
+    if workers > 1 and _POOL.get("n") != workers:
+        if "pool" in _POOL:
+            _POOL["pool"].terminate()
+        _POOL["pool"] = mp.get_context("fork").Pool(workers)
+        _POOL["n"] = workers
+    return _POOL.get("pool")
+
+
+def cpu_run(n_sample, workers):
+    chunk = (n_sample + workers - 1) // workers
+    bounds = [(s, min(n_sample, s + chunk)) for s in range(0, n_sample, chunk)]
+    pool = cpu_pool(workers)
+    t0 = time.perf_counter()
+    if pool is None:
+        done = sum(_cpu_eval_chunk(b) for b in bounds)
+    else:
+        done = sum(pool.map(_cpu_eval_chunk, bounds))
+    return done / (time.perf_counter() - t0)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------------------
+
+def build_workload(args, rank, device):
+    from paper_2305_02678_b200 import synth
+    mat = synth.material("2x32", RES, RES, seed=0, device=device)
+    n = C2_N if args.workload in ("c2", "full") else C3_N
+    n_levels = mat.latent.n_levels
+    sets = [synth.queries(n, n_levels, seed=1 + 100 * rank + s, device=device)
+            for s in range(args.sets)]
+    return mat, n, sets
+
+
+def launch(lib, h, workload, q, outs, stream):
+    n = q["uv"].shape[0]
+    if workload == "c2":
+        return lib.nm_eval(h.ptr, n, q["uv"].data_ptr(), q["lod"].data_ptr(), 1, q["u_rr"].data_ptr(),
+                           q["wi"].data_ptr(), q["wo"].data_ptr(), outs["rgb"].data_ptr(), None, None,
+                           stream)
+    if workload == "c3":
+        return lib.nm_sample_pdf(h.ptr, n, q["uv"].data_ptr(), q["lod"].data_ptr(), 1,
+                                 q["u_rr"].data_ptr(), q["wi"].data_ptr(), q["u3"].data_ptr(),
+                                 outs["ws"].data_ptr(), outs["pdf"].data_ptr(), None, None, stream)
+    return lib.nm_query(h.ptr, n, q["uv"].data_ptr(), q["lod"].data_ptr(), 1, q["u_rr"].data_ptr(),
+                        q["wi"].data_ptr(), q["wo"].data_ptr(), q["u3"].data_ptr(),
+                        outs["rgb"].data_ptr(), outs["ws"].data_ptr(), outs["pdf"].data_ptr(), None,
+                        stream)
+
+
+def io_bytes(workload):
+    # inputs: uv 8, lod 4, u_rr 4, wi 12 (+ wo 12) (+ u3 12); outputs rgb 12 / ws 12 + pdf 4
+    return {"c2": 40 + 12, "c3": 40 + 16, "full": 52 + 28}[workload]
+
+
+def run_ours(args):
+    rank, world, local = dist_init(args.gpus)
+    device = torch.device("cuda", local)
+    from paper_2305_02678_b200 import _lib, neural
+    lib = _lib.load()
+    mat, n, sets = build_workload(args, rank, device)
+    h = mat.device_material(device)
+    outs = {"rgb": torch.empty((n, 3), device=device), "ws": torch.empty((n, 3), device=device),
+            "pdf": torch.empty((n,), device=device)}
+    stream = torch.cuda.current_stream(device)
+    sp = stream.cuda_stream
+
+    # algorithmic bytes per query (exact for these inputs)
+    uniq = [unique_texels(h, q) for q in sets]
+    texel_bytes_per_q = 16.0 * float(np.mean(uniq)) / n
+    bytes_per_q = io_bytes(args.workload) + texel_bytes_per_q
+    flops_per_q = {"c2": FLOPS_EVAL, "c3": FLOPS_SAMPLE, "full": FLOPS_EVAL + FLOPS_SAMPLE}[args.workload]
+
+    for i in range(args.warmup):
+        _lib.check(launch(lib, h, args.workload, sets[i % len(sets)], outs, sp))
+    torch.cuda.synchronize()
+    clocks = Clocks(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = lib.nm_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(args.steps):
+        _lib.check(launch(lib, h, args.workload, sets[i % len(sets)], outs, sp))
+        if i % 8 == 0:
+            clocks.sample()
+    ev1.record(stream)
+    clocks.sample()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = int(lib.nm_launch_count() - l0)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms, world)
+    ms_step = ms_max / args.steps
+    value = n * world * args.steps / (ms_max / 1e3)
+
+    hbm, tflops, peak_kind = peaks()
+    kernel_s = ms / args.steps / 1e3
+    achieved_gbs = bytes_per_q * n / kernel_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+
+    # ---- e2e through the public API: pinned host numpy in/out -----------------
+    e2e = None
+    if args.workload == "c2" and args.e2e_steps > 0:
+        host = []
+        for q in sets[:2]:
+            hq = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in q.items()}
+            for k in hq:
+                hq[k].copy_(q[k])
+            host.append({k: v.numpy() for k, v in hq.items()})
+        out_host = torch.empty((n, 3), dtype=torch.float32, pin_memory=True).numpy()
+        for i in range(2):
+            hq = host[i % 2]
+            neural.eval_material(mat, hq["uv"], hq["lod"], hq["wi"], hq["wo"], hq["u_rr"], fp16=True,
+                                 return_level=False, out=out_host)
+        torch.cuda.synchronize()
+        barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.e2e_steps):
+            hq = host[i % 2]
+            neural.eval_material(mat, hq["uv"], hq["lod"], hq["wi"], hq["wo"], hq["u_rr"], fp16=True,
+                                 return_level=False, out=out_host)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+        e2e = {"value": n * world * args.e2e_steps / (e_ms / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 12),
+               "steps": args.e2e_steps, "api": "paper_2305_02678_b200.neural.eval_material"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        kind = "eval" if args.workload == "c2" else "sample_pdf"
+        cpu_setup(mat, {k: v for k, v in sets[0].items()}, args.cpu_sample, kind)
+        workers = os.cpu_count() or 1
+        v = cpu_run(args.cpu_sample, workers)
+        cpu = {"value": v, "unit": "queries/s", "cores": workers, "kind": "port",
+               "sample": f"{args.cpu_sample} queries of the same {args.workload.upper()} batch "
+                         f"(oracle/nm_oracle.py fp16 path, {workers} forked workers, "
+                         f"OPENBLAS_NUM_THREADS=1, {cpu_model()})"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp16 x fp16 -> fp32 tensor-core (hi/lo split), fp32 SIMT",
+            "data": "synthetic: random-init material (reference init order), N(0,1) fp16 latents, "
+                    "seeded uniform queries + half/difference direction pairs",
+            "config": {"workload": {"c2": "C2 coherent fused eval, 1 material, 4096^2 latent pyramid, "
+                                          "1920x1080 queries per GPU",
+                                    "c3": "C3 fused sample+pdf, 4096^2, 1920x1080x16 queries per GPU",
+                                    "full": "full query (eval+sample+pdf), 4096^2, 1920x1080 per GPU"}[
+                                        args.workload],
+                       "queries_per_step_per_gpu": n, "latent": f"{RES}x{RES} 8ch fp16, 13 levels",
+                       "brdf": "2x32", "sampler": "3x32", "parallelism": f"pixel-tile x{world}",
+                       "l2": f"inputs rotate over {len(sets)} sets "
+                             f"({len(sets) * n * io_bytes(args.workload) / 1e6:.0f} MB) > 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm, "traffic": traffic,
+                         "peak_source": peak_kind,
+                         "algorithmic_bytes_per_query": bytes_per_q,
+                         "texel_bytes_per_query": texel_bytes_per_q,
+                         "tensor_tflops_achieved": flops_per_q * n / kernel_s / 1e12,
+                         "tensor_frac": flops_per_q * n / kernel_s / 1e12 / tflops,
+                         "kernel": "fused_kernel<%s>" % {"c2": "kModeEval", "c3": "kModeSamplePdf",
+                                                         "full": "kModeQuery"}[args.workload]},
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks.report(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    """The reference's CPU implementation of the path (the oracle port, since
+    the reference is pure Python and cannot travel) on all host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2305_02678_b200 import synth
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else None
+    n_sample = args.ref_sample
+    if dev is not None:
+        mat = synth.material("2x32", RES, RES, seed=0, device=dev)
+        q = synth.queries(n_sample, mat.latent.n_levels, seed=1, device=dev)
+    else:  # no GPU: same recipe generated on the host
+        mat = synth.material_host("2x32", RES, RES, seed=0)
+        q = synth.queries_host(n_sample, mat.latent.n_levels, seed=1)
+    kind = "eval" if args.workload == "c2" else "sample_pdf"
+    cpu_setup(mat, q, n_sample, kind)
+    workers = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_run(n_sample, workers)
+    rates = [cpu_run(n_sample, workers) for _ in range(args.steps)]
+    total_s = sum(n_sample / r for r in rates)
+    value = n_sample * args.steps / total_s
+    sample = (f"{n_sample} queries per step of the {args.workload.upper()} workload "
+              f"(oracle/nm_oracle.py, the reference's fp16 path restated in numpy; "
+              f"{workers} forked workers, {cpu_model()})")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_s / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64/f32 numpy", "data": "synthetic (same recipe as ours)",
+        "config": {"workload": args.workload.upper(), "latent": f"{RES}x{RES}", "brdf": "2x32"},
+        "cpu_baseline": {"value": value, "unit": "queries/s", "cores": workers, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "queries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["c2", "c3", "full"], default="c2")
+    ap.add_argument("--sets", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-sample", type=int, default=C2_N)
+    ap.add_argument("--ref-sample", type=int, default=262144)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    try:
+        if args.impl == "reference":
+            run_reference(args)
+        else:
+            run_ours(args)
+    finally:
+        if "pool" in _POOL:
+            _POOL["pool"].close()
+            _POOL["pool"].join()
+        sys.stdout.flush()
+
+
+if __name__ == "__main__":
+    main()

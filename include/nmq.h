@@ -159,6 +159,9 @@ const char* nm_last_error(void);
 int nm_version(void);
 /* number of fused-kernel launches issued by this process (for bench claims) */
 int64_t nm_launch_count(void);
+/* test hook: 0 = use the architecture-specialized pipelined kernels when the
+ * material matches one (default), 1 = always the runtime-generic kernel */
+int nm_set_kernel_path(int path);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ SIGNATURES = {
     "nm_last_error": (ctypes.c_char_p, []),
     "nm_version": (c_i32, []),
     "nm_launch_count": (c_i64, []),
+    "nm_set_kernel_path": (c_i32, [c_i32]),
 }
 
 _lib = None

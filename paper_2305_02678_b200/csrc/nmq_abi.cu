@@ -122,13 +122,38 @@ int pack_chain(const NetView& v, Packer& pk, MatParams& mp, int& n_layers, const
           pk.set(L.b_off, n_pad, n, k, wv);           // against hi
           pk.set(L.b_off, n_pad, n, in_pad + k, wv);  // against lo
         }
-        pk.set(L.b_off, n_pad, n, 2 * in_pad, w[(size_t)n * (fi + 1) + fi]);  // bias
+        // bias twice: the A-side bias chunk holds (beta_hi, beta_lo) so the
+        // MMA adds beta * b exactly (beta = 1 generic, c^depth fast path)
+        const uint16_t bv = w[(size_t)n * (fi + 1) + fi];
+        pk.set(L.b_off, n_pad, n, 2 * in_pad, bv);
+        pk.set(L.b_off, n_pad, n, 2 * in_pad + 1, bv);
       }
     }
     if ((int)L.n_pad > mp.dmax) mp.dmax = L.n_pad;
     mp.layers[n_layers++] = L;
   }
   return NM_OK;
+}
+
+// Does the material match one of the specialized pipelined kernels
+// (nmq_fast.cu)?  All of them: 2 learned frames, 3x32 sampler (9 outputs or
+// isotropic 2), leaky hidden layers, linear outputs, equal hidden widths.
+int detect_fast_arch(const MatParams& mp, const NetView& bv, const NetView& sv,
+                     const nm_material_desc* d) {
+  if (!mp.has_brdf || !mp.has_sampler || !d->use_frames || d->n_frames != 2) return -1;
+  auto uniform = [](const NetView& v, int w) {
+    for (int l = 0; l < v.n_layers; ++l) {
+      const bool last = l == v.n_layers - 1;
+      if (v.act[l] != (last ? NM_ACT_LINEAR : NM_ACT_LEAKY)) return false;
+      if (!last && v.fo[l] != w) return false;
+    }
+    return true;
+  };
+  if (sv.n_layers != 4 || !uniform(sv, 32)) return -1;
+  if (bv.n_layers == 3 && uniform(bv, 32)) return 0;
+  if (bv.n_layers == 3 && uniform(bv, 16)) return 1;
+  if (bv.n_layers == 4 && uniform(bv, 64)) return 2;
+  return -1;
 }
 
 }  // namespace
@@ -147,6 +172,11 @@ extern "C" {
 const char* nm_last_error(void) { return t_err.c_str(); }
 int nm_version(void) { return NMQ_VERSION; }
 int64_t nm_launch_count(void) { return g_launches; }
+int nm_set_kernel_path(int path) {
+  if (path != 0 && path != 1) return fail(NM_ERR_INVALID, "kernel path must be 0 or 1");
+  g_kernel_path = path;
+  return NM_OK;
+}
 
 int nm_material_create(const nm_material_desc* d, int device, nm_material** out) {
   if (!d || !out) return fail(NM_ERR_INVALID, "null argument");
@@ -250,6 +280,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
   if (mp.dmax < 16) mp.dmax = 16;
   if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
   mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
+  mp.fast_arch = detect_fast_arch(mp, bv, sv, d);
   if (mp.wblob_bytes > 200 * 1024) {
     delete m;
     return fail(NM_ERR_UNSUPPORTED, "weights exceed shared memory");

@@ -1,6 +1,9 @@
 // nmq_device.cuh — per-query device math of the neural-material query path:
 // latent fetch, learned shading frames, proxy parameter maps, sample and pdf.
-// One thread owns one query; everything here is scalar SIMT code.
+// One thread owns one query; everything here is scalar SIMT code written
+// with MUFU approximations (rsqrt / rcp / ex2 / sin / cos): their ~1e-7
+// relative error sits far below the fp16 rounding every value passes through
+// before the next network layer, and below the stated tolerances.
 // Reference citations: /root/reference/pkg/src/neuralmat/<file>:<line>.
 #pragma once
 #include <cstdint>
@@ -12,9 +15,10 @@ namespace dev {
 
 constexpr float kPi = 3.14159265358979323846f;
 constexpr float kInvPi = 0.31830988618379067154f;
-constexpr float kAlphaFloor = 1e-4f;          // proxy.py:32
+constexpr float kLog2e = 1.44269504088896340736f;
+constexpr float kAlphaFloor = 1e-4f;               // proxy.py:32
 constexpr float kRhoClamp = 0.99994999874993749f;  // sqrt(1 - 1e-4), proxy.py:33
-constexpr float kLeaky = 0.01f;               // mlp.py:16
+constexpr float kLeaky = 0.01f;                    // mlp.py:16
 
 struct V3 {
   float x, y, z;
@@ -27,6 +31,17 @@ __device__ __forceinline__ V3 cross(V3 a, V3 b) {
 __device__ __forceinline__ V3 scale(V3 a, float s) { return {a.x * s, a.y * s, a.z * s}; }
 __device__ __forceinline__ V3 add(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
 
+// approximate helpers (MUFU)
+__device__ __forceinline__ float rcp(float x) { return __fdividef(1.f, x); }
+__device__ __forceinline__ float fsqrt(float x) {  // sqrt via rsqrt, exact 0 at 0
+  return x > 0.f ? x * rsqrtf(x) : 0.f;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float r;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
 __device__ __forceinline__ V3 ldg3(const float* p, int64_t i) {
   return {__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2)};
 }
@@ -38,12 +53,15 @@ __device__ __forceinline__ void stg3(float* p, int64_t i, V3 v) {
 
 // ---------------------------------------------------------------------------
 // Latent fetch.  choose_level (latent.py:76-82) is exact in fp32 for fp32
-// inputs (clip/floor/subtract of a float are exact).  Texel coordinates follow
-// _taps (latent.py:56-74) in float64 exactly like the reference, so the level
-// and the four tap indices are bit-identical; the blend is fp32 FMA over the
-// fp16 texels (the reference sums in float64 and rounds to fp32).
+// inputs (clip/floor/subtract of a float are exact).  Texel coordinates
+// follow _taps (latent.py:56-74): for power-of-two level sizes u*w is exact
+// in fp32 and the floor/half-texel decision below is exact; otherwise the
+// coordinate is computed in float64 like the reference.  Either way the
+// level and the four tap indices are bit-identical to the reference.  The
+// blend is fp32 FMA over the stored texels (the reference sums in float64
+// and rounds to fp32).
 struct Taps {
-  int64_t base;      // texel index of the level origin
+  int64_t base;  // texel index of the level origin
   int32_t x0, x1, y0, y1, w;
   float fx, fy;
 };
@@ -58,32 +76,49 @@ __device__ __forceinline__ int choose_level(const MatParams& m, float lod, float
   return c;
 }
 
-__device__ __forceinline__ int64_t wrap_index(double f, int32_t n, bool pow2) {
+__device__ __forceinline__ int64_t wrap_index(double f, int32_t n) {
   // Python's non-negative modulo of floor(f) (latent.py:65-68)
   const int64_t i = (int64_t)f;
-  if (pow2) return i & (int64_t)(n - 1);
   int64_t r = i % n;
   return r < 0 ? r + n : r;
 }
 
+// exact floor(u*w - 0.5) and its fraction for power-of-two w (u*w is exact)
+__device__ __forceinline__ void axis_pow2(float u, int32_t w, int32_t& i0, float& f) {
+  const float t = u * (float)w;  // exact: scaling by a power of two
+  const float ti = floorf(t);
+  const float fr = t - ti;       // exact
+  const bool lo = fr < 0.5f;
+  i0 = ((int32_t)(int64_t)ti - (lo ? 1 : 0)) & (w - 1);
+  f = lo ? fr + 0.5f : fr - 0.5f;
+}
+
 __device__ __forceinline__ Taps make_taps(const MatParams& m, int level, float u, float v) {
   const LevelDesc L = m.lv[level];
-  const double x = fma((double)u, (double)L.w, -0.5);
-  const double y = fma((double)v, (double)L.h, -0.5);
-  const double xf = floor(x), yf = floor(y);
   Taps t;
-  t.fx = (float)(x - xf);
-  t.fy = (float)(y - yf);
-  const bool p2 = m.pow2 != 0;
-  const int64_t x0 = wrap_index(xf, L.w, p2);
-  const int64_t y0 = wrap_index(yf, L.h, p2);
-  t.x0 = (int32_t)x0;
-  t.y0 = (int32_t)y0;
-  t.x1 = (x0 + 1 == L.w) ? 0 : (int32_t)x0 + 1;
-  t.y1 = (y0 + 1 == L.h) ? 0 : (int32_t)y0 + 1;
+  if (m.pow2) {
+    axis_pow2(u, L.w, t.x0, t.fx);
+    axis_pow2(v, L.h, t.y0, t.fy);
+  } else {
+    const double x = fma((double)u, (double)L.w, -0.5);
+    const double y = fma((double)v, (double)L.h, -0.5);
+    const double xf = floor(x), yf = floor(y);
+    t.fx = (float)(x - xf);
+    t.fy = (float)(y - yf);
+    t.x0 = (int32_t)wrap_index(xf, L.w);
+    t.y0 = (int32_t)wrap_index(yf, L.h);
+  }
+  t.x1 = (t.x0 + 1 == L.w) ? 0 : t.x0 + 1;
+  t.y1 = (t.y0 + 1 == L.h) ? 0 : t.y0 + 1;
   t.w = L.w;
   t.base = L.off;
   return t;
+}
+
+__device__ __forceinline__ int64_t tap_index(const Taps& t, int k) {
+  const int32_t x = (k & 1) ? t.x1 : t.x0;
+  const int32_t y = (k & 2) ? t.y1 : t.y0;
+  return t.base + (int64_t)y * t.w + x;
 }
 
 __device__ __forceinline__ void blend_texel(float (&z)[8], uint4 t, float w) {
@@ -96,6 +131,16 @@ __device__ __forceinline__ void blend_texel(float (&z)[8], uint4 t, float w) {
   }
 }
 
+__device__ __forceinline__ void blend4(float (&z)[8], const uint4 (&tex)[4], float fx, float fy) {
+  const float gx = 1.f - fx, gy = 1.f - fy;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) z[k] = 0.f;
+  blend_texel(z, tex[0], gx * gy);
+  blend_texel(z, tex[1], fx * gy);
+  blend_texel(z, tex[2], gx * fy);
+  blend_texel(z, tex[3], fx * fy);
+}
+
 __device__ __forceinline__ void blend_texel32(float (&z)[8], const float4* p, float w) {
   const float4 a = __ldg(p), b = __ldg(p + 1);
   z[0] = fmaf(a.x, w, z[0]); z[1] = fmaf(a.y, w, z[1]);
@@ -104,32 +149,23 @@ __device__ __forceinline__ void blend_texel32(float (&z)[8], const float4* p, fl
   z[6] = fmaf(b.z, w, z[6]); z[7] = fmaf(b.w, w, z[7]);
 }
 
-// Bilinear fetch of 8 channels.  Loads are issued together (4 x LDG.128).
+// Bilinear fetch of 8 channels straight from global memory (4 x LDG.128).
 __device__ __forceinline__ void fetch_taps(const MatParams& m, const Taps& t, float (&z)[8]) {
-  const int64_t r0 = (int64_t)t.y0 * t.w, r1 = (int64_t)t.y1 * t.w;
   if (m.texel_fp32) {  // generic fp32 pyramid (LatentPyramid master copy)
-    const float4* lat = reinterpret_cast<const float4*>(m.latent) + 2 * t.base;
+    const float4* lat = reinterpret_cast<const float4*>(m.latent);
     const float gx = 1.f - t.fx, gy = 1.f - t.fy;
 #pragma unroll
     for (int k = 0; k < 8; ++k) z[k] = 0.f;
-    blend_texel32(z, lat + 2 * (r0 + t.x0), gx * gy);
-    blend_texel32(z, lat + 2 * (r0 + t.x1), t.fx * gy);
-    blend_texel32(z, lat + 2 * (r1 + t.x0), gx * t.fy);
-    blend_texel32(z, lat + 2 * (r1 + t.x1), t.fx * t.fy);
+    blend_texel32(z, lat + 2 * tap_index(t, 0), gx * gy);
+    blend_texel32(z, lat + 2 * tap_index(t, 1), t.fx * gy);
+    blend_texel32(z, lat + 2 * tap_index(t, 2), gx * t.fy);
+    blend_texel32(z, lat + 2 * tap_index(t, 3), t.fx * t.fy);
     return;
   }
-  const uint4* lat = m.latent + t.base;
-  const uint4 a = __ldg(lat + r0 + t.x0);
-  const uint4 b = __ldg(lat + r0 + t.x1);
-  const uint4 c = __ldg(lat + r1 + t.x0);
-  const uint4 d = __ldg(lat + r1 + t.x1);
-  const float gx = 1.f - t.fx, gy = 1.f - t.fy;
+  uint4 tex[4];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) z[k] = 0.f;
-  blend_texel(z, a, gx * gy);
-  blend_texel(z, b, t.fx * gy);
-  blend_texel(z, c, gx * t.fy);
-  blend_texel(z, d, t.fx * t.fy);
+  for (int k = 0; k < 4; ++k) tex[k] = __ldg(m.latent + tap_index(t, k));
+  blend4(z, tex, t.fx, t.fy);
 }
 
 // ---------------------------------------------------------------------------
@@ -150,19 +186,19 @@ __device__ __forceinline__ V3 fallback_tangent(V3 n) {
 }
 
 __device__ __forceinline__ Frame frame_from_raw(const float* r) {
-  V3 rn = v3(r[0], r[1], r[2]);
+  const V3 rn = v3(r[0], r[1], r[2]);
   V3 rt = v3(r[3], r[4], r[5]);
-  const float ln = sqrtf(dot(rn, rn));
-  V3 n = scale(rn, 1.f / fmaxf(ln, 1e-12f));
+  // n = rn / max(|rn|, 1e-12)
+  const V3 n = scale(rn, rsqrtf(fmaxf(dot(rn, rn), 1e-24f)));
   V3 c = cross(n, rt);
-  float lc = sqrtf(dot(c, c));
-  if (lc < 1e-8f) {
+  float c2 = dot(c, c);
+  if (c2 < 1e-16f) {  // |c| < 1e-8: degenerate tangent
     rt = fallback_tangent(n);
     c = cross(n, rt);
-    lc = sqrtf(dot(c, c));
+    c2 = dot(c, c);
   }
   Frame f;
-  f.b = scale(c, 1.f / fmaxf(lc, 1e-12f));
+  f.b = scale(c, rsqrtf(fmaxf(c2, 1e-24f)));
   f.n = n;
   f.t = cross(f.b, n);
   return f;
@@ -171,7 +207,7 @@ __device__ __forceinline__ Frame frame_from_raw(const float* r) {
 // ---------------------------------------------------------------------------
 // BRDF output map (neural.py:37-39): max(expm1(min(y, 60)), 0)
 __device__ __forceinline__ float brdf_output(float y) {
-  return y > 0.f ? expm1f(fminf(y, 60.f)) : 0.f;
+  return y > 0.f ? ex2(fminf(y, 60.f) * kLog2e) - 1.f : 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -179,37 +215,38 @@ __device__ __forceinline__ float brdf_output(float y) {
 __device__ __forceinline__ float quad_tanh(float x) {
   const float ax = fabsf(x);
   if (ax > 1e18f) return copysignf(1.f, x);
-  const float r = x * (1.f + 0.5f * ax) / (1.f + ax + 0.5f * x * x);
+  const float r = __fdividef(x * fmaf(0.5f, ax, 1.f), fmaf(0.5f * x, x, 1.f + ax));
   return fminf(fmaxf(r, -1.f), 1.f);
 }
-__device__ __forceinline__ float quad_sinh(float x) { return x * (1.f + x * x * (1.f / 6.f)); }
+__device__ __forceinline__ float quad_sinh(float x) { return x * fmaf(x * x, 1.f / 6.f, 1.f); }
 
 struct Proxy {
   float wd, ws, mdx, mdy, ax, ay, rho, msx, msy;
 };
 
-__device__ __forceinline__ Proxy proxy_from_raw(const float* raw, bool isotropic) {
+// raw outputs may arrive scaled by `s` (the MLP engine's leaky rescaling)
+__device__ __forceinline__ Proxy proxy_from_raw(const float* raw, bool isotropic, float s = 1.f) {
   Proxy p;
   if (isotropic) {
-    p.wd = 0.5f * (quad_tanh(raw[0]) + 1.f);
+    p.wd = 0.5f * (quad_tanh(raw[0] * s) + 1.f);
     p.ws = 1.f - p.wd;
-    const float a = 0.5f * (quad_tanh(raw[1]) + 1.f);
+    const float a = 0.5f * (quad_tanh(raw[1] * s) + 1.f);
     p.ax = p.ay = a;
     p.mdx = p.mdy = p.rho = p.msx = p.msy = 0.f;
   } else {
-    const float a = raw[0], b = raw[3];
+    const float a = raw[0] * s, b = raw[3] * s;
     const float m = fmaxf(a, b);
-    const float ea = expf(a - m), eb = expf(b - m);
-    const float inv = 1.f / (ea + eb);
+    const float ea = ex2((a - m) * kLog2e), eb = ex2((b - m) * kLog2e);
+    const float inv = rcp(ea + eb);
     p.wd = ea * inv;
     p.ws = eb * inv;
-    p.mdx = quad_sinh(raw[1]);
-    p.mdy = quad_sinh(raw[2]);
-    p.ax = 0.5f * (quad_tanh(raw[4]) + 1.f);
-    p.ay = 0.5f * (quad_tanh(raw[5]) + 1.f);
-    p.rho = quad_tanh(raw[6]);
-    p.msx = quad_sinh(raw[7]);
-    p.msy = quad_sinh(raw[8]);
+    p.mdx = quad_sinh(raw[1] * s);
+    p.mdy = quad_sinh(raw[2] * s);
+    p.ax = 0.5f * (quad_tanh(raw[4] * s) + 1.f);
+    p.ay = 0.5f * (quad_tanh(raw[5] * s) + 1.f);
+    p.rho = quad_tanh(raw[6] * s);
+    p.msx = quad_sinh(raw[7] * s);
+    p.msy = quad_sinh(raw[8] * s);
   }
   p.ax = fmaxf(p.ax, kAlphaFloor);
   p.ay = fmaxf(p.ay, kAlphaFloor);
@@ -235,11 +272,11 @@ __device__ __forceinline__ void store_proxy(float* p9, int64_t i, const Proxy& p
 
 __device__ __forceinline__ float proxy_s(const Proxy& p) {
   // sqrt(1 - rho^2) written as sqrt((1-rho)(1+rho)) for accuracy near |rho|=1
-  return sqrtf((1.f - p.rho) * (1.f + p.rho));
+  return fsqrt((1.f - p.rho) * (1.f + p.rho));
 }
 
 __device__ __forceinline__ V3 diffuse_axis(const Proxy& p) {
-  V3 v = v3(-p.mdx, -p.mdy, 1.f);
+  const V3 v = v3(-p.mdx, -p.mdy, 1.f);
   return scale(v, rsqrtf(dot(v, v)));
 }
 
@@ -250,46 +287,43 @@ __device__ __forceinline__ float proxy_pdf(const Proxy& p, V3 wi, V3 wo) {
   float ps = 0.f;
   V3 h = add(wi, wo);
   const float hl2 = dot(h, h);
-  const float hl = sqrtf(hl2);
-  if (hl > 1e-9f) {
-    h = scale(h, 1.f / hl);
+  if (hl2 > 1e-18f) {  // |wi + wo| > 1e-9
+    h = scale(h, rsqrtf(hl2));
     if (h.z < 0.f) h = scale(h, -1.f);
     if (h.z > 0.f) {
       const float s = proxy_s(p);
-      const float q0 = fmaf(p.msx, h.z, h.x) / p.ax;
-      const float q1 = (fmaf(p.msy, h.z, h.y) / p.ay - p.rho * q0) / s;
+      const float q0 = fmaf(p.msx, h.z, h.x) * rcp(p.ax);
+      const float q1 = fmaf(fmaf(p.msy, h.z, h.y), rcp(p.ay), -p.rho * q0) * rcp(s);
       const float q2 = fmaf(q0, q0, fmaf(q1, q1, h.z * h.z));
       const float coh = fmaxf(fabsf(dot(wo, h)), 1e-12f);
       const float det = p.ax * p.ay * s;
-      const float val = h.z / (det * (4.f * kPi) * q2 * q2 * coh);
-      ps = fmaxf(val, 0.f);
+      ps = fmaxf(__fdividef(h.z, det * (4.f * kPi) * q2 * q2 * coh), 0.f);
     }
   }
-  return p.wd * pd + p.ws * ps;
+  return fmaf(p.wd, pd, p.ws * ps);
 }
 
-// proxy.py:138-180.  sin/cos of 2*pi*u via sincospif (exact argument), and
-// sqrt(1-cos^2) rewritten as sqrt(tan2)*cos (same value, no cancellation).
+// proxy.py:138-180.  sqrt(1-cos^2) rewritten as sqrt(tan2)*cos and
+// sqrt(1-z^2) as 2 sqrt(u(1-u)) (same values, no cancellation).
 __device__ __forceinline__ V3 proxy_sample(const Proxy& p, V3 wi, float u0, float u1, float u2) {
   float sp, cp;
-  sincospif(2.f * u2, &sp, &cp);
+  __sincosf(2.f * kPi * u2, &sp, &cp);
   if (u0 < p.wd) {
     // diffuse: normalize(n_d + uniform_sphere(u1,u2)), |.| floor 1e-9
-    const float z = 1.f - 2.f * u1;
-    const float r = 2.f * sqrtf(fmaxf(u1 * (1.f - u1), 0.f));
+    const float z = fmaf(-2.f, u1, 1.f);
+    const float r = 2.f * fsqrt(u1 * (1.f - u1));
     const V3 g = add(diffuse_axis(p), v3(r * cp, r * sp, z));
-    const float gl = fmaxf(sqrtf(dot(g, g)), 1e-9f);
-    return scale(g, 1.f / gl);
+    return scale(g, rsqrtf(fmaxf(dot(g, g), 1e-18f)));
   }
-  const float tan2 = u1 / fmaxf(1.f - u1, 1e-12f);
+  const float tan2 = u1 * rcp(fmaxf(1.f - u1, 1e-12f));
   const float ct = rsqrtf(1.f + tan2);
-  const float st = sqrtf(tan2) * ct;
+  const float st = fsqrt(tan2) * ct;
   const V3 m = v3(st * cp, st * sp, ct);
   const float s = proxy_s(p);
   // g = M m, M = [[ax, 0, -msx], [ay rho, ay s, -msy], [0, 0, 1]]
-  const V3 g = v3(fmaf(p.ax, m.x, -p.msx * m.z), fmaf(p.ay * p.rho, m.x, fmaf(p.ay * s, m.y, -p.msy * m.z)),
-                  m.z);
-  const V3 h = scale(g, 1.f / fmaxf(sqrtf(dot(g, g)), 1e-12f));
+  const V3 g = v3(fmaf(p.ax, m.x, -p.msx * m.z),
+                  fmaf(p.ay * p.rho, m.x, fmaf(p.ay * s, m.y, -p.msy * m.z)), m.z);
+  const V3 h = scale(g, rsqrtf(fmaxf(dot(g, g), 1e-24f)));
   const float d = 2.f * dot(wi, h);
   return v3(fmaf(d, h.x, -wi.x), fmaf(d, h.y, -wi.y), fmaf(d, h.z, -wi.z));
 }

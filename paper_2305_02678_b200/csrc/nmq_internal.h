@@ -49,6 +49,7 @@ struct MatParams {
   int32_t samp_first, samp_count;
   int32_t brdf_in;                // fan_in of the first BRDF layer (8 + 6*n_frames or 14)
   int32_t dmax;                   // max n_pad / in_pad over all layers (16/32/48/64)
+  int32_t fast_arch;              // specialized pipelined kernel id (nmq_fast.cu), -1 = generic
   LayerDesc layers[kMaxLayers];
 };
 
@@ -83,6 +84,8 @@ struct QueryArgs {
   float* wts;
 };
 
+// pipelined specialized kernels (nmq_fast.cu); cudaErrorNotSupported = use generic
+cudaError_t launch_fast(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s);
 // launchers (nmq_kernels.cu); return cudaError_t of the launch
 cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s,
                          int groups_override = 0);
@@ -99,5 +102,6 @@ cudaError_t launch_eval_divergent(const MatParams* mps_dev, int32_t n_mats, cons
                                   cudaStream_t s);
 int smem_bytes_for(const MatParams& mp);
 extern int64_t g_launches;
+extern int g_kernel_path;  // 0 = specialized when available, 1 = generic only
 
 }  // namespace nmq

@@ -227,14 +227,20 @@ def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, o
     `out` may pass a preallocated (B,3) fp32 device tensor for f."""
     _require_fp16(fp16)
     q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), wi=wi, wo=wo)
-    f = out if out is not None else _io.empty(q.n, 3, q.dev)
+    on_dev = isinstance(out, torch.Tensor) and out.is_cuda
+    f = out if on_dev else _io.empty(q.n, 3, q.dev)
     alb = _io.empty(q.n, 3, q.dev) if mat.cfg.albedo_head else None
     lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
     lib = _lib.load()
     _launch(lib.nm_eval, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
             q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), f.data_ptr(), _io.ptr(alb),
             _io.ptr(lv), _io.stream_ptr(q.dev))
-    return (_io.out(f, q.np_mode), None if alb is None else _io.out(alb, q.np_mode),
+    if out is not None and not on_dev:  # host buffer (numpy or pinned CPU tensor)
+        (torch.from_numpy(out) if isinstance(out, np.ndarray) else out).copy_(f)
+        f_res = out
+    else:
+        f_res = _io.out(f, q.np_mode)
+    return (f_res, None if alb is None else _io.out(alb, q.np_mode),
             None if lv is None else _io.out(lv, q.np_mode, np.int64))
 
 
