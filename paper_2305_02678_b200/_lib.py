@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnmq.so")
+LIB_PATH = os.environ.get("NMQ_LIB") or os.path.join(_HERE, "libnmq.so")
 
 NM_OK = 0
 NM_ERR_INVALID = -1

@@ -156,6 +156,37 @@ int detect_fast_arch(const MatParams& mp, const NetView& bv, const NetView& sv,
   return -1;
 }
 
+float h2f(uint16_t bits) {
+  __half_raw r;
+  r.x = bits;
+  return __half2float(__half(r));
+}
+
+// fp32 copies of the frame layer and the BRDF output layer for the FFMA2
+// paths of the specialized kernels (see MatParams::fw / ow).
+void fill_simt_layers(MatParams& mp, const NetView& fv, const NetView& bv) {
+  {
+    const uint16_t* w = fv.packed + fv.ofs[0];  // [12][8 + 1]
+    for (int p = 0; p < 6; ++p) {
+      for (int k = 0; k < 8; ++k)
+        mp.fw[p][k] = make_float2(h2f(w[(2 * p) * 9 + k]), h2f(w[(2 * p + 1) * 9 + k]));
+      mp.fb[p] = make_float2(h2f(w[(2 * p) * 9 + 8]), h2f(w[(2 * p + 1) * 9 + 8]));
+    }
+  }
+  const int l = bv.n_layers - 1;
+  const int fi = bv.fi[l], fo = bv.fo[l];
+  const uint16_t* w = bv.packed + bv.ofs[l];  // [fo][fi + 1]
+  for (int j = 0; j < 6; ++j) {
+    for (int q = 0; q < 32; ++q) {
+      const int k0 = 2 * q, k1 = 2 * q + 1;
+      const float a = (j < fo && k0 < fi) ? h2f(w[j * (fi + 1) + k0]) : 0.f;
+      const float b = (j < fo && k1 < fi) ? h2f(w[j * (fi + 1) + k1]) : 0.f;
+      mp.ow[j][q] = make_float2(a, b);
+    }
+    mp.ob[j] = j < fo ? h2f(w[j * (fi + 1) + fi]) : 0.f;
+  }
+}
+
 }  // namespace
 
 struct nm_material {
@@ -281,6 +312,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
   if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
   mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
   mp.fast_arch = detect_fast_arch(mp, bv, sv, d);
+  if (mp.fast_arch >= 0) fill_simt_layers(mp, fv, bv);
   if (mp.wblob_bytes > 200 * 1024) {
     delete m;
     return fail(NM_ERR_UNSUPPORTED, "weights exceed shared memory");

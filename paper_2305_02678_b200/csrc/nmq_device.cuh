@@ -141,6 +141,49 @@ __device__ __forceinline__ void blend4(float (&z)[8], const uint4 (&tex)[4], flo
   blend_texel(z, tex[3], fx * fy);
 }
 
+// ---- packed fp32x2 (FFMA2 / FMUL2, sm_100) -----------------------------------
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2s(float2 a, float s, float2 c) {
+  return __ffma2_rn(a, make_float2(s, s), c);
+}
+__device__ __forceinline__ float2 mul2s(float2 a, float s) { return __fmul2_rn(a, make_float2(s, s)); }
+__device__ __forceinline__ float2 neg2(float2 a) { return make_float2(-a.x, -a.y); }
+
+// Bilinear blend with z as four channel pairs: 16 FFMA2 instead of 32 FFMA.
+__device__ __forceinline__ void blend4x2(float2 (&z)[4], const uint4 (&tex)[4], float fx, float fy) {
+  const float gx = 1.f - fx, gy = 1.f - fy;
+  const float w[4] = {gx * gy, fx * gy, gx * fy, fx * fy};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const __half2* h = reinterpret_cast<const __half2*>(&tex[k]);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float2 f = __half22float2(h[c]);
+      z[c] = k == 0 ? mul2s(f, w[0]) : fma2s(f, w[k], z[c]);
+    }
+  }
+}
+
+// Two 3-vectors held component-wise as pairs (lane .x = first, .y = second).
+struct V3x2 {
+  float2 x, y, z;
+};
+__device__ __forceinline__ float2 dot2(const V3x2& a, const V3x2& b) {
+  return fma2(a.x, b.x, fma2(a.y, b.y, mul2(a.z, b.z)));
+}
+__device__ __forceinline__ float2 dot2s(const V3x2& a, V3 w) {  // (a1.w, a2.w)
+  return fma2s(a.x, w.x, fma2s(a.y, w.y, mul2s(a.z, w.z)));
+}
+__device__ __forceinline__ V3x2 cross2(const V3x2& a, const V3x2& b) {
+  return {fma2(a.y, b.z, mul2(neg2(a.z), b.y)), fma2(a.z, b.x, mul2(neg2(a.x), b.z)),
+          fma2(a.x, b.y, mul2(neg2(a.y), b.x))};
+}
+__device__ __forceinline__ V3x2 scale2(const V3x2& a, float2 s) {
+  return {mul2(a.x, s), mul2(a.y, s), mul2(a.z, s)};
+}
+
 __device__ __forceinline__ void blend_texel32(float (&z)[8], const float4* p, float w) {
   const float4 a = __ldg(p), b = __ldg(p + 1);
   z[0] = fmaf(a.x, w, z[0]); z[1] = fmaf(a.y, w, z[1]);
@@ -202,6 +245,38 @@ __device__ __forceinline__ Frame frame_from_raw(const float* r) {
   f.n = n;
   f.t = cross(f.b, n);
   return f;
+}
+
+// Both learned frames at once (neural.py:207-233) with packed fp32x2 math,
+// and the direction transforms T.wi, T.wo (neural.py:185-196):
+// ti = [t1.wi, b1.wi, n1.wi, t2.wi, b2.wi, n2.wi], same for to.  Per-lane
+// results equal frame_from_raw() + dot() exactly (same ops, same rounding).
+__device__ __forceinline__ void frames2_transform(const float* r, V3 wi, V3 wo, float (&ti)[6],
+                                                  float (&to)[6]) {
+  const V3x2 rn = {f2(r[0], r[6]), f2(r[1], r[7]), f2(r[2], r[8])};
+  V3x2 rt = {f2(r[3], r[9]), f2(r[4], r[10]), f2(r[5], r[11])};
+  const float2 l2 = dot2(rn, rn);
+  const V3x2 n = scale2(rn, f2(rsqrtf(fmaxf(l2.x, 1e-24f)), rsqrtf(fmaxf(l2.y, 1e-24f))));
+  V3x2 c = cross2(n, rt);
+  float2 c2 = dot2(c, c);
+  if (c2.x < 1e-16f || c2.y < 1e-16f) {  // |c| < 1e-8: degenerate tangent(s)
+    if (c2.x < 1e-16f) {
+      const V3 f = fallback_tangent(v3(n.x.x, n.y.x, n.z.x));
+      rt.x.x = f.x; rt.y.x = f.y; rt.z.x = f.z;
+    }
+    if (c2.y < 1e-16f) {
+      const V3 f = fallback_tangent(v3(n.x.y, n.y.y, n.z.y));
+      rt.x.y = f.x; rt.y.y = f.y; rt.z.y = f.z;
+    }
+    c = cross2(n, rt);
+    c2 = dot2(c, c);
+  }
+  const V3x2 b = scale2(c, f2(rsqrtf(fmaxf(c2.x, 1e-24f)), rsqrtf(fmaxf(c2.y, 1e-24f))));
+  const V3x2 t = cross2(b, n);
+  const float2 twi = dot2s(t, wi), bwi = dot2s(b, wi), nwi = dot2s(n, wi);
+  const float2 two = dot2s(t, wo), bwo = dot2s(b, wo), nwo = dot2s(n, wo);
+  ti[0] = twi.x; ti[1] = bwi.x; ti[2] = nwi.x; ti[3] = twi.y; ti[4] = bwi.y; ti[5] = nwi.y;
+  to[0] = two.x; to[1] = bwo.x; to[2] = nwo.x; to[3] = two.y; to[4] = bwo.y; to[5] = nwo.y;
 }
 
 // ---------------------------------------------------------------------------

@@ -51,6 +51,14 @@ struct MatParams {
   int32_t dmax;                   // max n_pad / in_pad over all layers (16/32/48/64)
   int32_t fast_arch;              // specialized pipelined kernel id (nmq_fast.cu), -1 = generic
   LayerDesc layers[kMaxLayers];
+  // fp32 copies (exact) of the two smallest layers, evaluated with packed
+  // FFMA2 on the CUDA cores in the specialized kernels:
+  //   frame layer 8 -> 12: fw[p][k] = (W[2p][k], W[2p+1][k]), fb[p] = (b[2p], b[2p+1])
+  //   BRDF output layer W -> 3|6: ow[j][q] = (W[j][2q], W[j][2q+1]), ob[j]
+  float2 fw[6][8];
+  float2 fb[6];
+  float2 ow[6][32];
+  float ob[6];
 };
 
 enum Mode : int {

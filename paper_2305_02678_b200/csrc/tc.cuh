@@ -31,6 +31,9 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+#ifndef NMQ_SUSPEND_NS
+#define NMQ_SUSPEND_NS 0x100000
+#endif
 // try_wait with a suspend-time hint: the warp sleeps in hardware until the
 // phase completes instead of burning issue slots in a spin loop.
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
@@ -40,7 +43,7 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
       "selp.u32 %0, 1, 0, p;\n\t}"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000u)
+      : "r"(smem_u32(bar)), "r"(parity), "r"((uint32_t)NMQ_SUSPEND_NS)
       : "memory");
   return ok != 0;
 }
