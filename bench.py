@@ -224,6 +224,50 @@ def cpu_model():
 
 
 # ---------------------------------------------------------------------------
+# host-side stand-ins for the no-GPU reference arm (same recipe, numpy RNG)
+
+class HostLatent:
+    """Host-side stand-in of DeviceLatent (no-GPU reference arm)."""
+
+    def __init__(self, levels, width, height):
+        self.levels16 = levels
+        self.width, self.height, self.n_levels = width, height, len(levels)
+
+    def half_copy(self):
+        return self.levels16
+
+
+def material_host(brdf_hidden="2x32", width=4096, height=4096, seed=0, **cfg):
+    mat = _nm().NeuralMaterial.create(_nm().NeuralMaterialConfig(brdf_hidden=brdf_hidden, **cfg),
+                                np.random.default_rng(seed))
+    rng = np.random.default_rng(seed + 1000)
+    levels = [rng.standard_normal((h, w, 8), dtype=np.float32).astype(np.float16)
+              for h, w in _ls()(width, height)]
+    mat.latent = HostLatent(levels, width, height)
+    return mat
+
+
+def queries_host(n, n_levels, seed):
+    """Same recipe as queries() on the host (numpy RNG; values differ)."""
+    from oracle import nm_oracle as O  # host generator only used by the CPU reference arm
+    rng = np.random.default_rng(seed)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    f = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32))  # noqa: E731
+    return {"uv": f(rng.random((n, 2))), "lod": f(rng.random(n) * (n_levels - 1)),
+            "u_rr": f(rng.random(n)), "wi": f(wi), "wo": f(wo), "u3": f(rng.random((n, 3)))}
+
+
+def _nm():
+    from paper_2305_02678_b200 import neural
+    return neural
+
+
+def _ls():
+    from paper_2305_02678_b200.latent import level_shapes
+    return level_shapes
+
+
+# ---------------------------------------------------------------------------
 
 def build_workload(args, rank, device):
     from paper_2305_02678_b200 import synth
@@ -396,8 +440,8 @@ def run_reference(args):
         mat = synth.material("2x32", RES, RES, seed=0, device=dev)
         q = synth.queries(n_sample, mat.latent.n_levels, seed=1, device=dev)
     else:  # no GPU: same recipe generated on the host
-        mat = synth.material_host("2x32", RES, RES, seed=0)
-        q = synth.queries_host(n_sample, mat.latent.n_levels, seed=1)
+        mat = material_host("2x32", RES, RES, seed=0)
+        q = queries_host(n_sample, mat.latent.n_levels, seed=1)
     kind = "eval" if args.workload == "c2" else "sample_pdf"
     cpu_setup(mat, q, n_sample, kind)
     workers = os.cpu_count() or 1

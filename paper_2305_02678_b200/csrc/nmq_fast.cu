@@ -346,17 +346,23 @@ __device__ __forceinline__ void out_layer_simt(const FG& g, const MatParams& mp,
       av[c0 / 2 + i] = __ffma2_rn(make_float2(fabsf(p.x), fabsf(p.y)), make_float2(kLk, kLk), p);
     }
   }
-  const int nout = albedo ? 6 : 3;
 #pragma unroll
-  for (int j = 0; j < 6; ++j) {
-    if (j < nout) {
+  for (int j = 0; j < 3; ++j) {
+    float2 acc = mul2(mp.ow[j][0], av[0]);
+#pragma unroll
+    for (int q = 1; q < W / 2; ++q) acc = fma2(mp.ow[j][q], av[q], acc);
+    y[j] = fmaf(acc.x + acc.y, inv_scale, mp.ob[j]);
+  }
+  if (albedo) {  // warp-uniform branch: the albedo head costs nothing otherwise
+#pragma unroll
+    for (int j = 3; j < 6; ++j) {
       float2 acc = mul2(mp.ow[j][0], av[0]);
 #pragma unroll
       for (int q = 1; q < W / 2; ++q) acc = fma2(mp.ow[j][q], av[q], acc);
       y[j] = fmaf(acc.x + acc.y, inv_scale, mp.ob[j]);
-    } else {
-      y[j] = 0.f;
     }
+  } else {
+    y[3] = y[4] = y[5] = 0.f;
   }
 }
 

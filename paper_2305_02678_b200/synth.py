@@ -94,33 +94,3 @@ def queries(n, n_levels, seed, device, need=("uv", "lod", "u_rr", "wi", "wo", "u
     out["u3"] = torch.rand((n, 3), device=device, generator=gen)
     return {k: v.contiguous() for k, v in out.items() if k in need}
 
-
-class HostLatent:
-    """Host-side stand-in of DeviceLatent (no-GPU reference arm)."""
-
-    def __init__(self, levels, width, height):
-        self.levels16 = levels
-        self.width, self.height, self.n_levels = width, height, len(levels)
-
-    def half_copy(self):
-        return self.levels16
-
-
-def material_host(brdf_hidden="2x32", width=4096, height=4096, seed=0, **cfg):
-    mat = NeuralMaterial.create(NeuralMaterialConfig(brdf_hidden=brdf_hidden, **cfg),
-                                np.random.default_rng(seed))
-    rng = np.random.default_rng(seed + 1000)
-    levels = [rng.standard_normal((h, w, 8), dtype=np.float32).astype(np.float16)
-              for h, w in level_shapes(width, height)]
-    mat.latent = HostLatent(levels, width, height)
-    return mat
-
-
-def queries_host(n, n_levels, seed):
-    """Same recipe as queries() on the host (numpy RNG; values differ)."""
-    from oracle import nm_oracle as O  # host generator only used by the CPU reference arm
-    rng = np.random.default_rng(seed)
-    wi, wo = O.draw_direction_pairs(rng, n)
-    f = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32))  # noqa: E731
-    return {"uv": f(rng.random((n, 2))), "lod": f(rng.random(n) * (n_levels - 1)),
-            "u_rr": f(rng.random(n)), "wi": f(wi), "wo": f(wo), "u3": f(rng.random((n, 3)))}
