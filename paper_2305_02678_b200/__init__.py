@@ -10,6 +10,7 @@ All queries run in the CUDA kernels of ``libnmq.so`` (include/nmq.h).
 from . import mlp, latent, proxy, neural  # noqa: F401
 from .latent import LatentPyramid  # noqa: F401
 from .neural import (NeuralMaterial, NeuralMaterialConfig, eval_brdf, eval_material,  # noqa: F401
+                     eval_material_multi,
                      infer_proxy, load_archive, query, sample_pdf, save_archive)
 
 __version__ = "0.1.0"

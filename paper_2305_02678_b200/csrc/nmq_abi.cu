@@ -503,17 +503,55 @@ int nm_query(const nm_material* m, int64_t n, const float* uv, const float* lod,
 
 size_t nm_multi_workspace_bytes(int64_t n, int32_t n_mats) {
   if (n < 0 || n_mats <= 0) return 0;
-  return (size_t)n * 4 + (size_t)(2 * n_mats + 64) * 4 + 256;
+  const size_t div = (size_t)n_mats * sizeof(MatParams) + 256;
+  const size_t bin = multi_workspace_bytes(n, n_mats);
+  return div > bin ? div : bin;
 }
 
 int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   const int32_t* mat_id, const float* uv, const float* lod, int32_t lod_stride,
                   const float* u_rr, const float* wi, const float* wo, float* rgb_out,
                   int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
-  (void)mats; (void)n_mats; (void)n; (void)mat_id; (void)uv; (void)lod; (void)lod_stride;
-  (void)u_rr; (void)wi; (void)wo; (void)rgb_out; (void)mode; (void)workspace;
-  (void)workspace_bytes; (void)stream;
-  return fail(NM_ERR_UNSUPPORTED, "nm_eval_multi: not built yet");
+  if (!mats || n_mats <= 0) return fail(NM_ERR_INVALID, "no materials");
+  if (n_mats > 32) return fail(NM_ERR_UNSUPPORTED, "at most 32 materials per call");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (n >= (int64_t)1 << 31) return fail(NM_ERR_UNSUPPORTED, "batch too large for one call");
+  if (!mat_id || !uv || !lod || !u_rr || !wi || !wo || !rgb_out)
+    return fail(NM_ERR_INVALID, "null input");
+  if (!workspace || workspace_bytes < nm_multi_workspace_bytes(n, n_mats))
+    return fail(NM_ERR_INVALID, "workspace too small (see nm_multi_workspace_bytes)");
+  const int dev = mats[0]->device;
+  std::vector<const MatParams*> mps(n_mats);
+  for (int k = 0; k < n_mats; ++k) {
+    if (!mats[k]) return fail(NM_ERR_INVALID, "null material");
+    if (mats[k]->device != dev) return fail(NM_ERR_INVALID, "materials on different devices");
+    if (!mats[k]->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+    mps[k] = &mats[k]->mp;
+  }
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.wo = wo; a.rgb = rgb_out;
+  DeviceGuard guard(dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e;
+  if (mode == NM_MULTI_BINNED) {
+    std::vector<int32_t> counts(n_mats);
+    int32_t bad = 0;
+    e = eval_binned(mps.data(), n_mats, a, mat_id, workspace, counts.data(), &bad, s);
+    if (e == cudaErrorInvalidValue && bad) return fail(NM_ERR_INVALID, "mat_id out of range");
+    return finish(nullptr, e, "nm_eval_multi(binned)");
+  }
+  if (mode != NM_MULTI_DIVERGENT) return fail(NM_ERR_INVALID, "unknown multi-material mode");
+  std::vector<MatParams> host(n_mats);
+  for (int k = 0; k < n_mats; ++k) host[k] = *mps[k];
+  MatParams* dev_mps = reinterpret_cast<MatParams*>(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
+  if ((e = cudaMemcpyAsync(dev_mps, host.data(), n_mats * sizeof(MatParams), cudaMemcpyHostToDevice,
+                           s)) != cudaSuccess)
+    return cuda_fail(e, "upload material table");
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "upload material table");
+  return finish(nullptr, launch_eval_divergent(mps.data(), dev_mps, n_mats, mat_id, a, s),
+                "nm_eval_multi(divergent)");
 }
 
 }  // extern "C"

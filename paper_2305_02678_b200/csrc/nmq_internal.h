@@ -102,11 +102,13 @@ cudaError_t launch_sample(int64_t n, const float* p9, const float* wi, const flo
                           float* wo, cudaStream_t s);
 cudaError_t launch_pdf(int64_t n, const float* p9, const float* wi, const float* wo, float* pdf,
                        cudaStream_t s);
-// binning for multi-material (counts -> offsets -> scatter of query indices)
-cudaError_t launch_bin(int64_t n, int32_t n_mats, const int32_t* mat_id, int32_t* counts,
-                       int32_t* offsets, int32_t* order, cudaStream_t s);
-cudaError_t launch_eval_divergent(const MatParams* mps_dev, int32_t n_mats, const int32_t* mat_id,
-                                  const QueryArgs& a, uint32_t max_wblob, int32_t dmax,
+// multi-material (nmq_multi.cu / nmq_kernels.cu)
+size_t multi_workspace_bytes(int64_t n, int32_t n_mats);
+cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const QueryArgs& a,
+                        const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
+                        cudaStream_t s);
+cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatParams* mps_dev,
+                                  int32_t n_mats, const int32_t* mat_id, const QueryArgs& a,
                                   cudaStream_t s);
 int smem_bytes_for(const MatParams& mp);
 extern int64_t g_launches;

@@ -338,6 +338,139 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
   }
 }
 
+// --- DIVERGENT multi-material eval --------------------------------------------
+// Every material's parameter block and weights live in SMEM.  Each thread
+// fetches its latent code from its own material's pyramid; the tile then
+// loops over the materials present in it (warp ballots OR-ed across the
+// tile group) and decodes all 128 rows with each, keeping its own.
+__global__ void __launch_bounds__(384, 1)
+divergent_eval_kernel(const MatParams* __restrict__ mps_g, int32_t n_mats,
+                      const __grid_constant__ QueryArgs a, const int32_t* __restrict__ mat_id,
+                      uint32_t tmem_cols, uint32_t group_cols) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  __shared__ uint64_t bars[8];
+  __shared__ uint32_t tbase_sh;
+  __shared__ uint32_t mask_sh[8];
+  __shared__ uint32_t boff_sh[32];
+  const int tid = threadIdx.x;
+  const int G = blockDim.x / 128;
+  const int gi = tid / 128, r = tid % 128;
+  const int warp = tid / 32;
+
+  MatParams* mps = reinterpret_cast<MatParams*>(smem);
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(mps_g);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
+    const uint32_t n16 = (uint32_t)(n_mats * sizeof(MatParams) / 16);
+    for (uint32_t i = tid; i < n16; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t off = ((uint32_t)(n_mats * sizeof(MatParams)) + 127u) & ~127u;
+    for (int k = 0; k < n_mats; ++k) {
+      boff_sh[k] = off;
+      off += (mps[k].wblob_bytes + 127u) & ~127u;
+    }
+  }
+  __syncthreads();
+  for (int k = 0; k < n_mats; ++k) {
+    const uint4* src = mps[k].wblob;
+    uint4* dst = reinterpret_cast<uint4*>(smem + boff_sh[k]);
+    for (uint32_t i = tid; i < mps[k].wblob_bytes / 16; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+  if (tid < G) tc::mbar_init(&bars[tid], 1);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     tc::smem_u32(&tbase_sh)), "r"(tmem_cols) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_proxy_async_smem();
+  tc::fence_mbar_init();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tb = tbase_sh;
+  const uint32_t bias_col = tb + (uint32_t)G * group_cols;
+  if (warp < 4) {
+    const uint32_t v[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tc::tmem_st8(bias_col + ((uint32_t)(warp * 32) << 16), v);
+    tc::tmem_st_wait();
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+
+  Group g;
+  g.d0 = tb + (uint32_t)gi * group_cols;
+  g.a0 = g.d0 + group_cols / 2;
+  g.lane = (uint32_t)((warp & 3) * 32) << 16;
+  g.bias_col = bias_col;
+  g.bar = &bars[gi];
+  g.phase = 0;
+  g.bar_id = 1 + gi;
+  g.leader = (r == 0);
+  const uint32_t smem_base = tc::smem_u32(smem);
+
+  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  for (int64_t tile = (int64_t)blockIdx.x * G + gi; tile < ntiles;
+       tile += (int64_t)gridDim.x * G) {
+    const int64_t q = tile * kTile + r;
+    const int m0 = q < a.n ? __ldg(mat_id + q) : -1;
+    const bool valid = m0 >= 0 && m0 < n_mats;  // out-of-range ids are skipped
+    const int m = valid ? m0 : -1;
+    V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
+    float z[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) z[k] = 0.f;
+    if (valid) {
+      const MatParams& mm = mps[m];
+      const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + q);
+      const float lod = __ldg(a.lod + (a.lod_stride ? q : 0));
+      const int level = choose_level(mm, lod, __ldg(a.u_rr + q));
+      const Taps t = make_taps(mm, level, uv.x, uv.y);
+      fetch_taps(mm, t, z);
+      wi = ldg3(a.wi, q);
+      wo = ldg3(a.wo, q);
+      if (a.level) a.level[q] = level;
+    }
+    // materials present in this tile
+    const uint32_t wmask = __reduce_or_sync(0xffffffffu, valid ? (1u << m) : 0u);
+    if (r == 0) mask_sh[gi] = 0u;
+    tc::named_bar(g.bar_id, 128);
+    if ((r & 31) == 0) atomicOr(&mask_sh[gi], wmask);
+    tc::named_bar(g.bar_id, 128);
+    uint32_t mask = mask_sh[gi];
+    float y[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) y[j] = 0.f;
+    while (mask) {
+      const int k = __ffs(mask) - 1;
+      mask &= mask - 1;
+      g.smem_w = smem_base + boff_sh[k];
+      float yk[16];
+      brdf_decode(mps[k], g, z, wi, wo, yk);
+      if (m == k) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) y[j] = yk[j];
+      }
+    }
+    if (valid) {
+      const bool up = (wi.z > 0.f) && (wo.z > 0.f);
+      const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
+                      : v3(0.f, 0.f, 0.f);
+      stg3(a.rgb, q, f);
+    }
+  }
+
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp == 0) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(tmem_cols)
+                 : "memory");
+  }
+}
+
 // --- plain SIMT kernels ------------------------------------------------------
 __global__ void __launch_bounds__(256) fetch_kernel(const __grid_constant__ MatParams mp,
                                                     const __grid_constant__ QueryArgs a) {
@@ -453,6 +586,34 @@ cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cuda
     case kModeQuery: return launch_mode<kModeQuery>(mp, a, s, groups);
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatParams* mps_dev,
+                                  int32_t n_mats, const int32_t* mat_id, const QueryArgs& a,
+                                  cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  uint32_t smem = ((uint32_t)(n_mats * sizeof(MatParams)) + 127u) & ~127u;
+  int dmax = 16;
+  for (int k = 0; k < n_mats; ++k) {
+    smem += (mps_host[k]->wblob_bytes + 127u) & ~127u;
+    dmax = dmax > mps_host[k]->dmax ? dmax : mps_host[k]->dmax;
+  }
+  if (smem > 220u * 1024u) return cudaErrorInvalidValue;
+  const uint32_t group_cols = 2u * (uint32_t)dmax;
+  const int G = 3;
+  uint32_t need = G * group_cols + 8u, cols = 32;
+  while (cols < need) cols <<= 1;
+  if (cols > 512) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(divergent_eval_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  int64_t grid = num_sms();
+  if (grid > (ntiles + G - 1) / G) grid = (ntiles + G - 1) / G;
+  divergent_eval_kernel<<<(int)grid, G * 128, smem, s>>>(mps_dev, n_mats, a, mat_id, cols,
+                                                          group_cols);
+  ++g_launches;
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fetch(const MatParams& mp, const QueryArgs& a, cudaStream_t s) {

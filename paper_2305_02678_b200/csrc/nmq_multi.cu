@@ -1,2 +1,192 @@
-// multi-material (binned / divergent) kernels — see nmq_abi.cu
+// nmq_multi.cu — multi-material queries (reference: render.py:352-356 groups
+// the hits of one path vertex by material and runs each group through its
+// own network).  Two execution modes, as in the paper:
+//
+//  * BINNED: queries are binned by material id with warp-aggregated
+//    counting (__match_any_sync + __popc, one atomic per distinct id per
+//    warp), an exclusive scan, and a warp-aggregated scatter that permutes
+//    the inputs into contiguous per-material segments; the coherent fused
+//    kernel then runs once per segment and a final pass scatters the outputs
+//    back to query order.
+//  * DIVERGENT: no reordering; every 128-query tile loops over the
+//    materials present in it and decodes the whole tile with each of them,
+//    keeping each row's own material (nmq_kernels.cu, kModeEvalMulti).
+#include <cstdint>
 #include "nmq_internal.h"
+
+namespace nmq {
+namespace {
+
+constexpr int kMaxMats = 64;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mats,
+                                                        const int32_t* __restrict__ mat_id,
+                                                        int32_t* __restrict__ counts,
+                                                        int32_t* __restrict__ bad) {
+  __shared__ int32_t sc[kMaxMats];
+  for (int i = threadIdx.x; i < n_mats; i += blockDim.x) sc[i] = 0;
+  __syncthreads();
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool in = i < n;
+    int m = in ? __ldg(mat_id + i) : -1;
+    if (in && (m < 0 || m >= n_mats)) {
+      atomicExch(bad, 1);
+      m = -1;
+    }
+    const uint32_t active = __ballot_sync(0xffffffffu, m >= 0);
+    if (m >= 0) {
+      const uint32_t peers = __match_any_sync(active, m);
+      if ((peers & lanemask_lt()) == 0) atomicAdd(&sc[m], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_mats; i += blockDim.x)
+    if (sc[i]) atomicAdd(counts + i, sc[i]);
+}
+
+__global__ void bin_scan_kernel(int32_t n_mats, const int32_t* __restrict__ counts,
+                                int32_t* __restrict__ offsets, int32_t* __restrict__ cursor) {
+  if (threadIdx.x == 0) {
+    int32_t acc = 0;
+    for (int m = 0; m < n_mats; ++m) {
+      offsets[m] = acc;
+      cursor[m] = acc;
+      acc += counts[m];
+    }
+    offsets[n_mats] = acc;
+  }
+}
+
+// Each query claims a slot in its material's segment (one atomic per
+// distinct id per warp) and copies its inputs there.
+__global__ void __launch_bounds__(256) bin_scatter_kernel(
+    int64_t n, const int32_t* __restrict__ mat_id, int32_t* __restrict__ cursor,
+    int32_t* __restrict__ order, const float* __restrict__ uv, const float* __restrict__ lod,
+    int32_t lod_stride, const float* __restrict__ urr, const float* __restrict__ wi,
+    const float* __restrict__ wo, float* __restrict__ p_uv, float* __restrict__ p_lod,
+    float* __restrict__ p_urr, float* __restrict__ p_wi, float* __restrict__ p_wo) {
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool in = i < n;
+    const int m = in ? __ldg(mat_id + i) : -1;
+    const uint32_t active = __ballot_sync(0xffffffffu, in);
+    if (!in) continue;
+    const uint32_t peers = __match_any_sync(active, m);
+    const int leader = __ffs(peers) - 1;
+    int32_t slot0 = 0;
+    if ((int)(threadIdx.x & 31) == leader) slot0 = atomicAdd(cursor + m, __popc(peers));
+    slot0 = __shfl_sync(peers, slot0, leader);
+    const int64_t s = slot0 + __popc(peers & lanemask_lt());
+    order[s] = (int32_t)i;
+    reinterpret_cast<float2*>(p_uv)[s] = __ldg(reinterpret_cast<const float2*>(uv) + i);
+    p_lod[s] = __ldg(lod + (lod_stride ? i : 0));
+    p_urr[s] = __ldg(urr + i);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      p_wi[3 * s + k] = __ldg(wi + 3 * i + k);
+      p_wo[3 * s + k] = __ldg(wo + 3 * i + k);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) unpermute3_kernel(int64_t n, const int32_t* __restrict__ order,
+                                                         const float* __restrict__ src,
+                                                         float* __restrict__ dst) {
+  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = __ldg(order + s);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) dst[3 * i + k] = __ldg(src + 3 * s + k);
+  }
+}
+
+int grid256(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+size_t multi_workspace_bytes(int64_t n, int32_t n_mats) {
+  // counts, offsets(+1), cursor, bad flag | order | uv lod urr wi wo | rgb
+  return 256 + (size_t)(3 * n_mats + 2) * 4 + (size_t)n * (4 + 40 + 12) + 64 * 8;
+}
+
+struct MultiWs {
+  int32_t *counts, *offsets, *cursor, *bad, *order;
+  float *uv, *lod, *urr, *wi, *wo, *rgb;
+};
+
+static MultiWs carve(void* ws, int64_t n, int32_t n_mats) {
+  auto align = [](uintptr_t p) { return (p + 255) & ~(uintptr_t)255; };
+  uintptr_t p = align((uintptr_t)ws);
+  MultiWs w;
+  w.counts = (int32_t*)p; p += n_mats * 4;
+  w.offsets = (int32_t*)p; p += (n_mats + 1) * 4;
+  w.cursor = (int32_t*)p; p += n_mats * 4;
+  w.bad = (int32_t*)p; p += 4;
+  p = align(p); w.order = (int32_t*)p; p += n * 4;
+  p = align(p); w.uv = (float*)p; p += n * 8;
+  p = align(p); w.lod = (float*)p; p += n * 4;
+  p = align(p); w.urr = (float*)p; p += n * 4;
+  p = align(p); w.wi = (float*)p; p += n * 12;
+  p = align(p); w.wo = (float*)p; p += n * 12;
+  p = align(p); w.rgb = (float*)p;
+  return w;
+}
+
+// BINNED eval.  `host_counts` receives the per-material counts (the host
+// needs them to size the per-segment launches: one D2H sync per call).
+cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const QueryArgs& a,
+                        const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
+                        cudaStream_t s) {
+  if (n_mats > kMaxMats) return cudaErrorInvalidValue;
+  MultiWs w = carve(ws, a.n, n_mats);
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(w.counts, 0, (3 * n_mats + 2) * 4, s)) != cudaSuccess) return e;
+  bin_count_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
+  bin_scan_kernel<<<1, 32, 0, s>>>(n_mats, w.counts, w.offsets, w.cursor);
+  bin_scatter_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, mat_id, w.cursor, w.order, a.uv, a.lod,
+                                                  a.lod_stride, a.u_rr, a.wi, a.wo, w.uv, w.lod,
+                                                  w.urr, w.wi, w.wo);
+  g_launches += 3;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaMemcpyAsync(host_counts, w.counts, n_mats * 4, cudaMemcpyDeviceToHost, s)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaMemcpyAsync(bad, w.bad, 4, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return e;
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return e;
+  if (*bad) return cudaErrorInvalidValue;
+  int64_t off = 0;
+  for (int m = 0; m < n_mats; ++m) {
+    const int64_t c = host_counts[m];
+    if (c > 0) {
+      QueryArgs sa{};
+      sa.n = c;
+      sa.uv = w.uv + 2 * off;
+      sa.lod = w.lod + off;
+      sa.lod_stride = 1;
+      sa.u_rr = w.urr + off;
+      sa.wi = w.wi + 3 * off;
+      sa.wo = w.wo + 3 * off;
+      sa.rgb = w.rgb + 3 * off;
+      if ((e = launch_fused(*mps[m], kModeEval, sa, s)) != cudaSuccess) return e;
+    }
+    off += c;
+  }
+  unpermute3_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, w.order, w.rgb, a.rgb);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+}  // namespace nmq

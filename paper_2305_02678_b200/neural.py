@@ -17,6 +17,7 @@ inputs, fp32 accumulation and fp32 hidden activations), reproduced on the
 tensor cores with a hi/lo split of the hidden activations.
 """
 
+import ctypes
 import io
 import json
 import os
@@ -301,6 +302,49 @@ def query(mat, uv, level, u_rr, wi, wo, u, fp16=True, return_level=False):
     if return_level:
         res = res + (_io.out(lv, q.np_mode, np.int64),)
     return res
+
+
+MULTI_MODES = {"divergent": _lib.NM_MULTI_DIVERGENT, "binned": _lib.NM_MULTI_BINNED}
+
+
+def eval_material_multi(mats, mat_id, uv, level, wi, wo, u_rr, mode="binned", fp16=True, out=None):
+    """Per-query material selection (the renderer's per-vertex material groups,
+    render.py:352-356): f[i] = eval_material(mats[mat_id[i]], ...)[0][i].
+    mode "binned" sorts queries into per-material segments with warp-level
+    counting and runs the coherent fused kernel per segment; "divergent"
+    decodes mixed tiles directly.  Returns f (B, 3)."""
+    _require_fp16(fp16)
+    if mode not in MULTI_MODES:
+        raise ValueError(f"mode must be one of {sorted(MULTI_MODES)}")
+    mats = list(mats)
+    if not mats:
+        raise ValueError("no materials")
+    np_mode = _io.is_numpy_like(uv)
+    handles = [m.device_material(None if np_mode else uv.device) for m in mats]
+    dev = handles[0].device
+    if any(h.device != dev for h in handles):
+        raise ValueError("materials must live on the same device")
+    uv_t = _io.as_rows(uv, 2, dev, "uv")
+    n = uv_t.shape[0]
+    lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
+    urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+    wi_t = _io.as_rows(wi, 3, dev, "wi")
+    wo_t = _io.as_rows(wo, 3, dev, "wo")
+    if isinstance(mat_id, torch.Tensor):
+        ids = mat_id.to(device=dev, dtype=torch.int32).reshape(-1).contiguous()
+    else:
+        ids = torch.from_numpy(np.ascontiguousarray(np.asarray(mat_id).reshape(-1), np.int32)).to(dev)
+    if ids.numel() != n or wi_t.shape[0] != n or wo_t.shape[0] != n:
+        raise ValueError("mat_id, uv, wi and wo must share the batch size")
+    f = out if isinstance(out, torch.Tensor) and out.is_cuda else _io.empty(n, 3, dev)
+    lib = _lib.load()
+    ws_bytes = int(lib.nm_multi_workspace_bytes(n, len(handles)))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ptrs = (ctypes.c_void_p * len(handles))(*[h.ptr for h in handles])
+    _launch(lib.nm_eval_multi, ptrs, len(handles), n, ids.data_ptr(), uv_t.data_ptr(),
+            lod_t.data_ptr(), lod_stride, urr_t.data_ptr(), wi_t.data_ptr(), wo_t.data_ptr(),
+            f.data_ptr(), MULTI_MODES[mode], ws.data_ptr(), ws_bytes, _io.stream_ptr(dev))
+    return _io.out(f, np_mode)
 
 
 # --- archive (NMATARC1, neural.py:368-419) -------------------------------------

@@ -1,0 +1,90 @@
+"""Multi-material eval (render.py:352-356 per-material groups): BINNED
+(warp-aggregated binning + coherent kernel per segment) and DIVERGENT
+(per-tile material loop) against the oracle, per query."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def _materials(rng):
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+
+    specs = [({}, (64, 64)), ({"brdf_hidden": "2x16"}, (32, 32)), ({"albedo_head": True}, (24, 20)),
+             ({"brdf_hidden": "3x64"}, (16, 16)), ({"use_frames": False}, (32, 16))]
+    mats, omats = [], []
+    for cfg, (w, h) in specs:
+        m = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(**cfg), rng)
+        m.latent = LatentPyramid(O.random_pyramid(rng, w, h).levels)
+        mats.append(m)
+
+        def net(x):
+            return None if x is None else O.Net([(l.w, l.b, l.act) for l in x.layers])
+
+        om = O.Material(O.Config(**m.cfg.to_json()), net(m.frame_layer), net(m.brdf_decoder),
+                        net(m.sampler_decoder))
+        om.latent = O.Pyramid(m.latent.levels)
+        omats.append(om)
+    return mats, omats
+
+
+def _queries(rng, n, n_levels_max=7):
+    from oracle import nm_oracle as O
+    uv = rng.random((n, 2)).astype(np.float32)
+    lod = (rng.random(n) * n_levels_max).astype(np.float32)
+    urr = rng.random(n).astype(np.float32)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    return uv, lod, urr, wi.astype(np.float32), wo.astype(np.float32)
+
+
+def _oracle_multi(omats, ids, uv, lod, urr, wi, wo):
+    from oracle import nm_oracle as O
+    f = np.zeros((len(ids), 3))
+    for k, om in enumerate(omats):
+        m = ids == k
+        if m.any():
+            f[m] = O.eval_material(om, uv[m], lod[m], wi[m], wo[m], urr[m], fp16=True)[0]
+    return f
+
+
+@pytest.mark.parametrize("mode", ["binned", "divergent"])
+@pytest.mark.parametrize("pattern", ["random", "coherent", "blocks"])
+def test_multi_material_matches_oracle(mode, pattern):
+    from paper_2305_02678_b200 import neural
+
+    rng = np.random.default_rng(42)
+    mats, omats = _materials(rng)
+    n = 9001
+    uv, lod, urr, wi, wo = _queries(rng, n)
+    if pattern == "random":
+        ids = rng.integers(0, len(mats), n).astype(np.int32)
+    elif pattern == "coherent":
+        ids = np.full(n, 2, np.int32)
+    else:
+        ids = (np.arange(n) // 700 % len(mats)).astype(np.int32)
+    f = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode=mode)
+    ref = _oracle_multi(omats, ids, uv, lod, urr, wi, wo)
+    from test_gpu_parity import check_rel
+    check_rel(f, ref, what=f"{mode}/{pattern}")
+
+
+def test_multi_modes_agree_and_reject_bad_ids():
+    from paper_2305_02678_b200 import neural
+
+    rng = np.random.default_rng(7)
+    mats, _ = _materials(rng)
+    n = 4000
+    uv, lod, urr, wi, wo = _queries(rng, n)
+    ids = rng.integers(0, len(mats), n).astype(np.int32)
+    a = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode="binned")
+    b = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode="divergent")
+    np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+    bad = ids.copy()
+    bad[17] = len(mats)
+    with pytest.raises(ValueError):
+        neural.eval_material_multi(mats, bad, uv, lod, wi, wo, urr, mode="binned")
