@@ -20,6 +20,7 @@ oracle/nm_oracle.py) on the host cores for a bounded sample.
 """
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -300,7 +301,134 @@ def io_bytes(workload):
     return {"c2": 40 + 12, "c3": 40 + 16, "full": 52 + 28}[workload]
 
 
+def _time_loop(fn, steps, warmup, stream, world):
+    for i in range(warmup):
+        fn(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        fn(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier(world)
+    return max_over_ranks(e0.elapsed_time(e1), world) / steps
+
+
+def run_c4(args):
+    """C4: five materials mixed per query (Table-1-sized pyramids, 8.3 GB of
+    fp16 latents), 1920x1080 eval queries with i.i.d. material ids; BINNED
+    (headline) vs DIVERGENT."""
+    rank, world, local = dist_init(args.gpus)
+    device = torch.device("cuda", local)
+    from paper_2305_02678_b200 import _lib, synth
+    from paper_2305_02678_b200.synth import C4_RESOLUTIONS
+    lib = _lib.load()
+    mats = [synth.material("2x32", w, h, seed=10 + k, device=device)
+            for k, (w, h) in enumerate(C4_RESOLUTIONS)]
+    handles = [m.device_material(device) for m in mats]
+    n = C2_N
+    max_levels = min(m.latent.n_levels for m in mats)
+    sets = [synth.queries(n, max_levels, seed=1 + 100 * rank + s, device=device)
+            for s in range(args.sets)]
+    g = torch.Generator(device=device)
+    g.manual_seed(5 + rank)
+    ids = [torch.randint(0, len(mats), (n,), device=device, generator=g, dtype=torch.int32)
+           for _ in range(args.sets)]
+    rgb = torch.empty((n, 3), device=device)
+    ws_bytes = int(lib.nm_multi_workspace_bytes(n, len(mats)))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device)
+    ptrs = (ctypes.c_void_p * len(mats))(*[h.ptr for h in handles])
+    stream = torch.cuda.current_stream(device)
+
+    def step(mode):
+        def fn(i):
+            q, mid = sets[i % len(sets)], ids[i % len(sets)]
+            _lib.check(lib.nm_eval_multi(ptrs, len(mats), n, mid.data_ptr(), q["uv"].data_ptr(),
+                                         q["lod"].data_ptr(), 1, q["u_rr"].data_ptr(),
+                                         q["wi"].data_ptr(), q["wo"].data_ptr(), rgb.data_ptr(),
+                                         mode, ws.data_ptr(), ws_bytes, stream.cuda_stream))
+        return fn
+
+    steps = max(3, args.steps // 10)
+    ms_b = _time_loop(step(_lib.NM_MULTI_BINNED), steps, args.warmup, stream, world)
+    ms_d = _time_loop(step(_lib.NM_MULTI_DIVERGENT), max(3, steps // 4), 2, stream, world)
+    if rank == 0:
+        texels = sum(int(h.info.latent_texels) for h in handles)
+        print(json.dumps({
+            "metric": METRIC, "value": n * world / (ms_b / 1e3), "unit": "queries/s",
+            "n_gpus": world, "steps": steps, "warmup": args.warmup, "ms_per_step": ms_b,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "fp16 x fp16 -> fp32 tensor-core (hi/lo split), fp32 SIMT",
+            "data": "synthetic: 5 random-init 2x32 materials, N(0,1) fp16 latents",
+            "config": {"workload": "C4 eval, 5 materials mixed per query (i.i.d. ids), 1920x1080",
+                       "pyramids": [f"{w}x{h}" for w, h in C4_RESOLUTIONS],
+                       "latent_gb": texels * 16 / 1e9, "mode": "binned (headline)"},
+            "divergent": {"value": n * world / (ms_d / 1e3), "ms_per_step": ms_d},
+            "binned_over_divergent": ms_d / ms_b,
+        }))
+
+
+def run_c5(args):
+    """C5: 3840x2160 x 64 spp eval (530.8M queries) sharded by pixel-row band
+    across ranks (replicated material), per-pixel spp reduction on each rank
+    and one gather of the 99.5 MB image to rank 0."""
+    rank, world, local = dist_init(args.gpus)
+    device = torch.device("cuda", local)
+    from paper_2305_02678_b200 import _lib, shard, synth
+    lib = _lib.load()
+    H, W, SPP = 2160, 3840, 64
+    mat = synth.material("2x32", RES, RES, seed=0, device=device)
+    h = mat.device_material(device)
+    q0, q1 = shard.band_queries(rank, world, H, W, SPP)
+    n = q1 - q0
+    chunk = 1 << 24
+    q = {k: torch.empty((n,) + s, device=device) for k, s in
+         (("uv", (2,)), ("lod", ()), ("u_rr", ()), ("wi", (3,)), ("wo", (3,)))}
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        part = synth.queries(c1 - c0, mat.latent.n_levels, seed=1000 + rank * 4096 + c0 // chunk,
+                             device=device, need=tuple(q))
+        for k in q:
+            q[k][c0:c1] = part[k]
+    rgb = torch.empty((n, 3), device=device)
+    stream = torch.cuda.current_stream(device)
+
+    def compute(i):
+        _lib.check(lib.nm_eval(h.ptr, n, q["uv"].data_ptr(), q["lod"].data_ptr(), 1,
+                               q["u_rr"].data_ptr(), q["wi"].data_ptr(), q["wo"].data_ptr(),
+                               rgb.data_ptr(), None, None, stream.cuda_stream))
+
+    def frame(i):
+        compute(i)
+        band = shard.reduce_spp(rgb, SPP).view(-1, W, 3)
+        if world > 1:
+            shard.gather_bands(band, H, W)
+
+    steps = max(2, args.steps // 50)
+    ms_c = _time_loop(compute, steps, 2, stream, world)
+    ms_f = _time_loop(frame, steps, 1, stream, world)
+    if rank == 0:
+        total = H * W * SPP
+        print(json.dumps({
+            "metric": METRIC, "value": total / (ms_c / 1e3), "unit": "queries/s",
+            "n_gpus": world, "steps": steps, "warmup": 2, "ms_per_step": ms_c,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp16 x fp16 -> fp32 tensor-core (hi/lo split), fp32 SIMT",
+            "data": "synthetic: random-init 2x32 material, 4096^2 N(0,1) fp16 latents",
+            "config": {"workload": "C5 eval 3840x2160x64spp sharded by pixel-row band",
+                       "queries_per_frame": total, "parallelism": f"pixel-tile x{world}"},
+            "with_spp_reduce_and_gather": {"value": total / (ms_f / 1e3), "ms_per_frame": ms_f},
+        }))
+
+
 def run_ours(args):
+    if args.workload == "c4":
+        return run_c4(args)
+    if args.workload == "c5":
+        return run_c5(args)
     rank, world, local = dist_init(args.gpus)
     device = torch.device("cuda", local)
     from paper_2305_02678_b200 import _lib, neural
@@ -471,7 +599,7 @@ def main():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3", "full"], default="c2")
+    ap.add_argument("--workload", choices=["c2", "c3", "full", "c4", "c5"], default="c2")
     ap.add_argument("--sets", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-sample", type=int, default=C2_N)
