@@ -592,8 +592,8 @@ def run_ours(args):
                          "texel_bytes_per_query": texel_bytes_per_q,
                          "tensor_tflops_achieved": flops_per_q * n / kernel_s / 1e12,
                          "tensor_frac": flops_per_q * n / kernel_s / 1e12 / tflops,
-                         "kernel": "fused_kernel<%s>" % {"c2": "kModeEval", "c3": "kModeSamplePdf",
-                                                         "full": "kModeQuery"}[args.workload]},
+                         "kernel": "fast_kernel<%s> (csrc/nmq_fast.cu)" % {
+                             "c2": "kModeEval", "c3": "kModeSamplePdf", "full": "kModeQuery"}[args.workload]},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
