@@ -162,15 +162,27 @@ float h2f(uint16_t bits) {
   return __half2float(__half(r));
 }
 
-// fp32 copies of the frame layer and the BRDF output layer for the FFMA2
-// paths of the specialized kernels (see MatParams::fw / ow).
-void fill_simt_layers(MatParams& mp, const NetView& fv, const NetView& bv) {
+// Layers of the specialized kernels (see MatParams::fast_frame_off):
+// re-packed frame layer and BRDF first layer for the shared input chunks,
+// fp32 copy of the BRDF output layer for the FFMA2 path.
+void fill_fast_layers(MatParams& mp, Packer& pk, const NetView& fv, const NetView& bv) {
   {
     const uint16_t* w = fv.packed + fv.ofs[0];  // [12][8 + 1]
-    for (int p = 0; p < 6; ++p) {
-      for (int k = 0; k < 8; ++k)
-        mp.fw[p][k] = make_float2(h2f(w[(2 * p) * 9 + k]), h2f(w[(2 * p + 1) * 9 + k]));
-      mp.fb[p] = make_float2(h2f(w[(2 * p) * 9 + 8]), h2f(w[(2 * p + 1) * 9 + 8]));
+    mp.fast_frame_off = pk.append(16, 2);
+    for (int n = 0; n < 12; ++n) {
+      for (int k = 0; k < 8; ++k) pk.set(mp.fast_frame_off, 16, n, k, w[n * 9 + k]);
+      pk.set(mp.fast_frame_off, 16, n, 11, w[n * 9 + 8]);
+    }
+  }
+  {
+    const int fi = bv.fi[0], fo = bv.fo[0];  // 20 = [z(8), T.wi(6), T.wo(6)]
+    const int n_pad = round_up(fo, 16);
+    const uint16_t* w = bv.packed + bv.ofs[0];  // [fo][fi + 1]
+    mp.fast_l1_off = pk.append(n_pad, 4);
+    for (int n = 0; n < fo; ++n) {
+      for (int k = 0; k < 8; ++k) pk.set(mp.fast_l1_off, n_pad, n, k, w[n * (fi + 1) + k]);
+      for (int k = 8; k < 20; ++k) pk.set(mp.fast_l1_off, n_pad, n, k + 8, w[n * (fi + 1) + k]);
+      pk.set(mp.fast_l1_off, n_pad, n, 11, w[n * (fi + 1) + fi]);
     }
   }
   const int l = bv.n_layers - 1;
@@ -310,9 +322,9 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     m->sampler_width = m->sampler_width > mp.layers[l].n_pad ? m->sampler_width : mp.layers[l].n_pad;
   if (mp.dmax < 16) mp.dmax = 16;
   if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
-  mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
   mp.fast_arch = detect_fast_arch(mp, bv, sv, d);
-  if (mp.fast_arch >= 0) fill_simt_layers(mp, fv, bv);
+  if (mp.fast_arch >= 0) fill_fast_layers(mp, pk, fv, bv);
+  mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
   if (mp.wblob_bytes > 200 * 1024) {
     delete m;
     return fail(NM_ERR_UNSUPPORTED, "weights exceed shared memory");

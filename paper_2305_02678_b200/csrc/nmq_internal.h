@@ -51,12 +51,15 @@ struct MatParams {
   int32_t dmax;                   // max n_pad / in_pad over all layers (16/32/48/64)
   int32_t fast_arch;              // specialized pipelined kernel id (nmq_fast.cu), -1 = generic
   LayerDesc layers[kMaxLayers];
-  // fp32 copies (exact) of the two smallest layers, evaluated with packed
-  // FFMA2 on the CUDA cores in the specialized kernels:
-  //   frame layer 8 -> 12: fw[p][k] = (W[2p][k], W[2p+1][k]), fb[p] = (b[2p], b[2p+1])
-  //   BRDF output layer W -> 3|6: ow[j][q] = (W[j][2q], W[j][2q+1]), ob[j]
-  float2 fw[6][8];
-  float2 fb[6];
+  // Specialized kernels (nmq_fast.cu) share one K=16 input chunk between the
+  // frame layer, the sampler's first layer and the BRDF decoder's first
+  // layer: chunk 0 = [z(8), wi(3), 1, 0 x 4], chunk 1 = [T.wi(6), T.wo(6), 0 x 4].
+  // B operands re-packed for that K order (zero weights against wi where
+  // the layer does not read it; bias against the 1 at K = 11):
+  uint32_t fast_frame_off;  // frame layer, N = 16 (12 used), K = 16
+  uint32_t fast_l1_off;     // BRDF first layer, N = hidden width, K = 32
+  // fp32 copy (exact) of the BRDF output layer W -> 3|6, evaluated with packed
+  // FFMA2 on the CUDA cores: ow[j][q] = (W[j][2q], W[j][2q+1]), ob[j]
   float2 ow[6][32];
   float ob[6];
 };
