@@ -159,9 +159,14 @@ const char* nm_last_error(void);
 int nm_version(void);
 /* number of fused-kernel launches issued by this process (for bench claims) */
 int64_t nm_launch_count(void);
-/* test hook: 0 = use the architecture-specialized pipelined kernels when the
- * material matches one (default), 1 = always the runtime-generic kernel */
+/* test hook: 0 = auto (default: the pipelined tcgen05 kernels, then the
+ * warp-tile mma.sync kernels, for materials matching a specialized
+ * architecture), 1 = always the runtime-generic kernel, 2 = pipelined tcgen05,
+ * 3 = warp-tile (2 and 3 fall back to the generic kernel when inapplicable) */
 int nm_set_kernel_path(int path);
+/* which kernel family ran the last query launch of this process:
+ * 1 = generic, 2 = pipelined tcgen05, 3 = warp-tile mma.sync */
+int nm_last_kernel_path(void);
 
 #ifdef __cplusplus
 }

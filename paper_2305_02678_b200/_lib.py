@@ -96,6 +96,7 @@ SIGNATURES = {
     "nm_version": (c_i32, []),
     "nm_launch_count": (c_i64, []),
     "nm_set_kernel_path": (c_i32, [c_i32]),
+    "nm_last_kernel_path": (c_i32, []),
 }
 
 _lib = None
@@ -119,6 +120,8 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    if os.environ.get("NMQ_KERNEL_PATH"):  # experiments: force a kernel family (see nmq.h)
+        lib.nm_set_kernel_path(int(os.environ["NMQ_KERNEL_PATH"]))
     _lib = lib
     return lib
 

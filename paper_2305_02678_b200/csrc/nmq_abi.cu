@@ -1,6 +1,7 @@
 // nmq_abi.cu — C ABI (include/nmq.h): material creation (re-tiling the
 // reference's packed fp16 weights into the UMMA B-operand layout, latent
 // upload) and the query entry points.
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -199,6 +200,65 @@ void fill_fast_layers(MatParams& mp, Packer& pk, const NetView& fv, const NetVie
   }
 }
 
+// Warp-tile layout (see MatParams::wk_blob).  Packs every specialized
+// layer into `wk` (fp16 B operands, then fp32 biases scaled by c^depth).
+void fill_warp_layers(MatParams& mp, Packer& wk, const NetView& fv, const NetView& bv,
+                      const NetView& sv) {
+  auto W = [](const NetView& v, int l, int n, int k) {  // fp16 bits of W_l[n][k] (k == fi: bias)
+    return v.packed[v.ofs[l] + (size_t)n * (v.fi[l] + 1) + k];
+  };
+  auto dense = [&](const NetView& v, int l, int n_pad) {  // K = fan_in (padded to 16), N = n_pad
+    const int fi = v.fi[l], fo = v.fo[l];
+    const uint32_t off = wk.append(n_pad, round_up(fi, 16) / 8);
+    for (int n = 0; n < fo; ++n)
+      for (int k = 0; k < fi; ++k) wk.set(off, n_pad, n, k, W(v, l, n, k));
+    return off;
+  };
+  // frame layer: input chunk 0 = [z 0-7, wi 8-10, 1 @ 11]
+  mp.wk_fr = wk.append(16, 2);
+  for (int n = 0; n < 12; ++n) {
+    for (int k = 0; k < 8; ++k) wk.set(mp.wk_fr, 16, n, k, W(fv, 0, n, k));
+    wk.set(mp.wk_fr, 16, n, 11, W(fv, 0, n, 8));
+  }
+  {  // BRDF layer 1 on [z | T.wi(6), T.wo(6), 1 @ 12]
+    const int fi = bv.fi[0], fo = bv.fo[0], n_pad = round_up(fo, 16);
+    mp.wk_b1z = wk.append(n_pad, 1);
+    mp.wk_b1t = wk.append(n_pad, 2);
+    for (int n = 0; n < fo; ++n) {
+      for (int k = 0; k < 8; ++k) wk.set(mp.wk_b1z, n_pad, n, k, W(bv, 0, n, k));
+      for (int k = 8; k < 20; ++k) wk.set(mp.wk_b1t, n_pad, n, k - 8, W(bv, 0, n, k));
+      wk.set(mp.wk_b1t, n_pad, n, 12, W(bv, 0, n, fi));
+    }
+  }
+  for (int l = 1; l < bv.n_layers - 1; ++l) mp.wk_bh[l - 1] = dense(bv, l, round_up(bv.fo[l], 16));
+  mp.wk_bo = dense(bv, bv.n_layers - 1, 8);
+  mp.wk_s1 = wk.append(round_up(sv.fo[0], 16), 2);  // [z 0-7, wi 8-10, 1 @ 11]
+  for (int n = 0; n < sv.fo[0]; ++n)
+    for (int k = 0; k <= 11; ++k) wk.set(mp.wk_s1, round_up(sv.fo[0], 16), n, k, W(sv, 0, n, k));
+  for (int l = 1; l < sv.n_layers - 1; ++l) mp.wk_sh[l - 1] = dense(sv, l, round_up(sv.fo[l], 16));
+  mp.wk_so = dense(sv, sv.n_layers - 1, 16);
+  // fp32 biases of layers >= 1, times c^l (the scaled-leaky activations)
+  auto bias = [&](const NetView& v, int l, int n_pad) {
+    while (wk.blob.size() % 8) wk.blob.push_back(0);
+    const uint32_t off = (uint32_t)(wk.blob.size() * 2);
+    const double sc = std::pow(kLeakyScale, l);
+    for (int n = 0; n < n_pad; ++n) {
+      const float b = n < v.fo[l] ? (float)(sc * (double)h2f(W(v, l, n, v.fi[l]))) : 0.f;
+      uint32_t u;
+      std::memcpy(&u, &b, 4);
+      wk.blob.push_back((uint16_t)(u & 0xFFFFu));
+      wk.blob.push_back((uint16_t)(u >> 16));
+    }
+    return off;
+  };
+  for (int l = 1; l < bv.n_layers - 1; ++l) mp.wk_bias_bh[l - 1] = bias(bv, l, round_up(bv.fo[l], 16));
+  mp.wk_bias_bo = bias(bv, bv.n_layers - 1, 8);
+  for (int l = 1; l < sv.n_layers - 1; ++l) mp.wk_bias_sh[l - 1] = bias(sv, l, round_up(sv.fo[l], 16));
+  mp.wk_bias_so = bias(sv, sv.n_layers - 1, 16);
+  while (wk.blob.size() % 8) wk.blob.push_back(0);
+  mp.wk_bytes = (uint32_t)(wk.blob.size() * 2);
+}
+
 }  // namespace
 
 struct nm_material {
@@ -206,6 +266,7 @@ struct nm_material {
   MatParams mp{};
   void* latent = nullptr;
   void* wblob = nullptr;
+  void* wkblob = nullptr;
   int64_t texels = 0;
   int brdf_width = 0, sampler_width = 0;
 };
@@ -215,8 +276,9 @@ extern "C" {
 const char* nm_last_error(void) { return t_err.c_str(); }
 int nm_version(void) { return NMQ_VERSION; }
 int64_t nm_launch_count(void) { return g_launches; }
+int nm_last_kernel_path(void) { return g_last_path; }
 int nm_set_kernel_path(int path) {
-  if (path != 0 && path != 1) return fail(NM_ERR_INVALID, "kernel path must be 0 or 1");
+  if (path < 0 || path > 3) return fail(NM_ERR_INVALID, "kernel path must be 0..3");
   g_kernel_path = path;
   return NM_OK;
 }
@@ -323,7 +385,11 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
   if (mp.dmax < 16) mp.dmax = 16;
   if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
   mp.fast_arch = detect_fast_arch(mp, bv, sv, d);
-  if (mp.fast_arch >= 0) fill_fast_layers(mp, pk, fv, bv);
+  Packer wk;
+  if (mp.fast_arch >= 0) {
+    fill_fast_layers(mp, pk, fv, bv);
+    fill_warp_layers(mp, wk, fv, bv, sv);
+  }
   mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
   if (mp.wblob_bytes > 200 * 1024) {
     delete m;
@@ -354,8 +420,20 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     delete m;
     return cuda_fail(e, "upload weights");
   }
+  if (mp.wk_bytes) {
+    if ((e = cudaMalloc(&m->wkblob, mp.wk_bytes)) != cudaSuccess ||
+        (e = cudaMemcpy(m->wkblob, wk.blob.data(), mp.wk_bytes, cudaMemcpyHostToDevice)) !=
+            cudaSuccess) {
+      cudaFree(m->latent);
+      cudaFree(m->wblob);
+      if (m->wkblob) cudaFree(m->wkblob);
+      delete m;
+      return cuda_fail(e, "upload warp-tile weights");
+    }
+  }
   mp.latent = reinterpret_cast<const uint4*>(m->latent);
   mp.wblob = reinterpret_cast<const uint4*>(m->wblob);
+  mp.wk_blob = reinterpret_cast<const uint4*>(m->wkblob);
   *out = m;
   return NM_OK;
 }
@@ -365,6 +443,7 @@ int nm_material_destroy(nm_material* m) {
   DeviceGuard guard(m->device);
   if (m->latent) cudaFree(m->latent);
   if (m->wblob) cudaFree(m->wblob);
+  if (m->wkblob) cudaFree(m->wkblob);
   delete m;
   return NM_OK;
 }

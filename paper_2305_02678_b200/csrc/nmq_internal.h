@@ -62,6 +62,21 @@ struct MatParams {
   // FFMA2 on the CUDA cores: ow[j][q] = (W[j][2q], W[j][2q+1]), ob[j]
   float2 ow[6][32];
   float ob[6];
+  // Warp-tile kernels (nmq_warp.cu): one blob of fp16 B operands (chunk-major
+  // K-major: 16-byte K-chunk c of row n at off + c*n_pad*16 + n*16, read with
+  // ldmatrix) and fp32 biases pre-scaled by c^depth (accumulator init).
+  // Byte offsets into wk_blob.  Input chunks as above; BRDF layer 1 is split
+  // into a K=8 part on z and a K=16 part on [T.wi, T.wo, 1 @ 12].
+  const uint4* wk_blob;
+  uint32_t wk_bytes;
+  uint32_t wk_fr;          // frame layer N16 K16
+  uint32_t wk_b1z, wk_b1t; // BRDF layer 1: K8 (z), K16 (T.wi, T.wo, bias), N = BW
+  uint32_t wk_bh[3];       // BRDF hidden layers 2.. (K = N = BW)
+  uint32_t wk_bo;          // BRDF output, N = 8, K = BW
+  uint32_t wk_s1;          // sampler layer 1 (input chunk 0), N = SW
+  uint32_t wk_sh[3];       // sampler hidden layers 2..
+  uint32_t wk_so;          // sampler output, N = 16, K = SW
+  uint32_t wk_bias_bh[3], wk_bias_bo, wk_bias_sh[3], wk_bias_so;  // fp32 [N] each
 };
 
 enum Mode : int {
@@ -95,8 +110,12 @@ struct QueryArgs {
   float* wts;
 };
 
-// pipelined specialized kernels (nmq_fast.cu); cudaErrorNotSupported = use generic
+// pipelined tcgen05 kernels (nmq_fast.cu) and warp-tile mma.sync kernels
+// (nmq_warp.cu); cudaErrorNotSupported = not applicable, try the next path
 cudaError_t launch_fast(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s);
+cudaError_t launch_warp(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s);
+// scale of the leaky-ReLU trick shared by the specialized kernels: c = 1 + k
+constexpr double kLeakyScale = 1.0 + 0.98019802570343017578;
 // launchers (nmq_kernels.cu); return cudaError_t of the launch
 cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s,
                          int groups_override = 0);
@@ -115,6 +134,9 @@ cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatPar
                                   cudaStream_t s);
 int smem_bytes_for(const MatParams& mp);
 extern int64_t g_launches;
-extern int g_kernel_path;  // 0 = specialized when available, 1 = generic only
+// kernel path: 0 = auto (tcgen05 pipelined, then warp-tile, then generic),
+// 1 = generic only, 2 = tcgen05 pipelined, 3 = warp-tile (each falls back to generic)
+extern int g_kernel_path;
+extern int g_last_path;  // family of the last launch_fused (1/2/3 as above)
 
 }  // namespace nmq

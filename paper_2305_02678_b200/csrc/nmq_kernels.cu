@@ -24,6 +24,7 @@ namespace nmq {
 
 int64_t g_launches = 0;
 int g_kernel_path = 0;
+int g_last_path = 0;
 
 namespace {
 
@@ -573,11 +574,17 @@ int smem_bytes_for(const MatParams& mp) { return (int)((mp.wblob_bytes + 127) / 
 cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s,
                          int groups) {
   if (a.n <= 0) return cudaSuccess;
-  if (groups == 0 && g_kernel_path == 0) {
+  if (groups == 0 && (g_kernel_path == 0 || g_kernel_path == 2)) {
     const cudaError_t e = launch_fast(mp, mode, a, s);
-    if (e != cudaErrorNotSupported) return e;
+    if (e != cudaErrorNotSupported) return g_last_path = 2, e;
     (void)cudaGetLastError();
   }
+  if (groups == 0 && (g_kernel_path == 0 || g_kernel_path == 3)) {
+    const cudaError_t e = launch_warp(mp, mode, a, s);
+    if (e != cudaErrorNotSupported) return g_last_path = 3, e;
+    (void)cudaGetLastError();
+  }
+  g_last_path = 1;
   switch (mode) {
     case kModeEval: return launch_mode<kModeEval>(mp, a, s, groups);
     case kModeEvalZ: return launch_mode<kModeEvalZ>(mp, a, s, groups);

@@ -208,7 +208,12 @@ def test_proxy_sample_pdf_kat():
 
 # --- both kernel paths, partial tiles, multi-tile pipelines --------------------
 
-@pytest.fixture(params=[0, 1], ids=["specialized", "generic"])
+def _last_path():
+    from paper_2305_02678_b200 import _lib
+    return _lib.load().nm_last_kernel_path()
+
+
+@pytest.fixture(params=[3, 2, 1], ids=["warp_tile", "tcgen05", "generic"])
 def kernel_path(request):
     from paper_2305_02678_b200 import _lib
     lib = _lib.load()
@@ -225,6 +230,7 @@ def test_golden_both_paths(name, kernel_path):
     mat = our_material(g)
     f, ws, pdf, chosen = neural.query(mat, g["uv"], g["lod"], g["u_rr"], g["wi"], g["wo"], g["u3"],
                                       return_level=True)
+    assert _last_path() == kernel_path  # the family under test really ran
     assert np.array_equal(chosen, g["chosen"])
     check_rel(f, g["f"], what=f"{name} rgb path{kernel_path}")
     guard = np.abs(g["u3"][:, 0].astype(np.float64) - g["params"][:, 0]) >= 1e-3
@@ -267,6 +273,7 @@ def test_fast_pipeline_sizes_vs_oracle(n, arch, kernel_path):
     om = _oracle_from(mat)
     f_ref, ws_ref, pdf_ref, p_ref, ch_ref = O.full_query(om, uv, lod, urr, wi, wo, u3)
     f, ws, pdf, ch = neural.query(mat, uv, lod, urr, wi, wo, u3, return_level=True)
+    assert _last_path() == kernel_path
     assert np.array_equal(ch, ch_ref)
     check_rel(f, f_ref, what="query rgb")
     check_dirs(ws, ws_ref, u3, p_ref, wi)
