@@ -222,11 +222,46 @@ class _QueryInputs:
             setattr(self, k, t)
 
 
+def _stream_eval(mat, uv, level, wi, wo, u_rr, out):
+    """eval_material for a large host batch: chunked H2D / fused kernel / D2H
+    overlapped on two streams (see _io.streamed).  None if not applicable."""
+    if mat.cfg.albedo_head:
+        return None
+    n = np.shape(uv)[0] if np.ndim(uv) == 2 else 0
+    if n < 2 * _io.STREAM_CHUNK:
+        return None
+    h_uv, h_wi, h_wo = _io.host_rows(uv, 2, "uv"), _io.host_rows(wi, 3, "wi"), _io.host_rows(wo, 3, "wo")
+    h_lod = np.ascontiguousarray(np.asarray(level, dtype=np.float32)).reshape(-1, 1)
+    h_urr = np.ascontiguousarray(np.asarray(u_rr, dtype=np.float32)).reshape(-1, 1)
+    if h_uv is None or h_wi is None or h_wo is None or h_lod.shape[0] != n or h_urr.shape[0] != n \
+            or h_wi.shape[0] != n or h_wo.shape[0] != n:
+        return None
+    if out is not None and (out.dtype != np.float32 or out.shape != (n, 3) or not out.flags.c_contiguous):
+        return None
+    f_host = out if out is not None else np.empty((n, 3), np.float32)
+    h = mat.device_material(None)
+    lib = _lib.load()
+
+    def launch(d_in, d_out, count, stream):
+        d_uv, d_lod, d_urr, d_wi, d_wo = d_in
+        _launch(lib.nm_eval, h.ptr, count, d_uv.data_ptr(), d_lod.data_ptr(), 1, d_urr.data_ptr(),
+                d_wi.data_ptr(), d_wo.data_ptr(), d_out[0].data_ptr(), None, None, stream)
+
+    _io.streamed(n, h.device, [h_uv, h_lod, h_urr, h_wi, h_wo], [f_host], launch)
+    return f_host if out is not None else f_host.astype(np.float64)
+
+
 def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, out=None):
     """Fetch (Russian-roulette level + bilinear) and decode in ONE fused
     kernel, returning (f, albedo, chosen_level) (neural.py:303-309).
-    `out` may pass a preallocated (B,3) fp32 device tensor for f."""
+    `out` may pass a preallocated (B,3) fp32 device tensor, or a host (ideally
+    pinned) fp32 buffer, for f.  Large host batches without albedo or level
+    outputs stream through the GPU in overlapped chunks."""
     _require_fp16(fp16)
+    if not return_level and _io.is_numpy_like(uv) and (out is None or isinstance(out, np.ndarray)):
+        f = _stream_eval(mat, uv, level, wi, wo, u_rr, out)
+        if f is not None:
+            return f, None, None
     q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), wi=wi, wo=wo)
     on_dev = isinstance(out, torch.Tensor) and out.is_cuda
     f = out if on_dev else _io.empty(q.n, 3, q.dev)

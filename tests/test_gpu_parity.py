@@ -296,3 +296,25 @@ def test_scalar_lod_broadcast(kernel_path):
     f, _, ch = neural.eval_material(mat, g["uv"], 2.5, g["wi"], g["wo"], g["u_rr"], fp16=True)
     assert np.array_equal(ch, ch_ref)
     check_rel(f, f_ref, what="scalar lod")
+
+
+def test_streamed_host_eval_matches_device_path():
+    """Large host batches take the chunked two-stream H2D / kernel / D2H
+    pipeline; its results equal the one-shot device path bit for bit."""
+    import torch
+    from paper_2305_02678_b200 import _io, neural, synth
+
+    dev = torch.device("cuda", 0)
+    mat = synth.material("2x32", 256, 256, seed=3, device=dev)
+    n = 2 * _io.STREAM_CHUNK + 123
+    q = synth.queries(n, mat.latent.n_levels, seed=4, device=dev)
+    f_dev, _, _ = neural.eval_material(mat, q["uv"], q["lod"], q["wi"], q["wo"], q["u_rr"], fp16=True)
+    host = {k: v.cpu().numpy() for k, v in q.items()}
+    out = torch.empty((n, 3), dtype=torch.float32, pin_memory=True).numpy()
+    f_h, alb, lv = neural.eval_material(mat, host["uv"], host["lod"], host["wi"], host["wo"],
+                                        host["u_rr"], fp16=True, return_level=False, out=out)
+    assert f_h is out and alb is None and lv is None
+    assert np.array_equal(out, f_dev.cpu().numpy())
+    f64, _, _ = neural.eval_material(mat, host["uv"], host["lod"], host["wi"], host["wo"],
+                                     host["u_rr"], fp16=True, return_level=False)
+    assert f64.dtype == np.float64 and np.array_equal(f64, f_dev.cpu().numpy().astype(np.float64))
