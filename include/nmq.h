@@ -155,6 +155,19 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   void* stream);
 
 /* --- misc -------------------------------------------------------------- */
+/* Level of detail from ray cones (replaces render.footprint_to_level,
+ * render.py:334-337, and the footprint in render._surface_frames_and_level,
+ * render.py:436-443).  float64 like the reference.
+ *   nm_footprint_level: level = clip(0.5 log2(max(area, 1)), 0, n_levels-1)
+ *   nm_cone_level:      area = ((w + s t) / max(|cos_hit|, 0.05) * density)^2,
+ *                       level as above, rounded to the fp32 lod the query
+ *                       entry points take; density_stride 0 = one density. */
+int nm_footprint_level(int64_t n, const double* area_texels, int32_t n_levels, double* level_out,
+                       void* stream);
+int nm_cone_level(int64_t n, const float* cone_w, const float* cone_s, const float* t,
+                  const float* cos_hit, const float* density, int32_t density_stride,
+                  int32_t n_levels, float* lod_out, void* stream);
+
 const char* nm_last_error(void);
 int nm_version(void);
 /* number of fused-kernel launches issued by this process (for bench claims) */

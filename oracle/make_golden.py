@@ -142,6 +142,36 @@ def make_archive(name="archive_albedo"):
     print(name)
 
 
+def make_lod_case(name="lod", n=4096, seed=31):
+    """LoD from ray cones through the reference renderer itself:
+    render._surface_frames_and_level on a one-quad scene bound to a neural
+    material, plus render.footprint_to_level on raw areas (incl. < 1 and
+    beyond the top level).  Inputs are fp32-representable (the GPU takes fp32)."""
+    geom, latent, neural, proxy = _ref()
+    from types import SimpleNamespace
+    from neuralmat import render
+    rng = np.random.default_rng(seed)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), np.random.default_rng(seed + 1))
+    mat.latent = latent.LatentPyramid.zeros(512, 512)
+    quad = render.Quad([-1.0, 0.0, -1.0], [2.0, 0.0, 0.0], [0.0, 0.0, 2.0], material="m",
+                       uv_scale=(3.0, 2.0))
+    scene = render.Scene(None, [quad], {"m": render.NeuralBinding(mat)})
+    d = geom.normalize(np.stack([rng.uniform(-1, 1, n), -rng.uniform(0.02, 1, n), rng.uniform(-1, 1, n)], -1))
+    d = np.asarray(_f32(d), np.float64)
+    t = np.asarray(_f32(rng.uniform(0.01, 50.0, n)), np.float64)
+    cone_w = np.asarray(_f32(rng.uniform(0.0, 0.05, n)), np.float64)
+    cone_s = np.asarray(_f32(rng.uniform(0.0, 0.01, n)), np.float64)
+    hits = SimpleNamespace(pos=np.zeros((n, 3)) + t[:, None] * d, obj=np.zeros(n, dtype=np.int64), t=t)
+    frames, level = render._surface_frames_and_level(scene, SimpleNamespace(), hits, d, cone_w, cone_s)
+    cos_hit = np.abs(np.sum(frames.n * d, axis=-1))
+    area = np.asarray(_f32(np.exp(rng.uniform(-3.0, 30.0, n))), np.float64)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), cone_w=cone_w, cone_s=cone_s, t=t,
+                        cos_hit=cos_hit, density=np.float64(quad.texel_density((512, 512))),
+                        n_levels=np.int64(mat.latent.n_levels), level=level, area=area,
+                        area_level=render.footprint_to_level(area, mat.latent.n_levels))
+    print(name)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     make_case("c1_2x32", {}, n=4096, taps=True, fp32_path=True)
@@ -154,6 +184,7 @@ def main():
     make_case("npot_wrap", {}, res=(24, 20), seed=21, uv_lo=-2.0, uv_hi=3.0, taps=True)
     make_proxy_case()
     make_archive()
+    make_lod_case()
 
 
 if __name__ == "__main__":

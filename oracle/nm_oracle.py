@@ -610,3 +610,22 @@ def full_query(mat, uv, lod, u_rr, wi, wo, u3, fp16=True):
     p = infer_proxy(mat, z, wi, fp16=fp16)
     ws = sample(p, wi, u3)
     return f, ws, pdf(p, wi, ws), p, chosen
+
+
+# ---------------------------------------------------------------------------
+# LoD from ray cones (render.py) — the step that produces the query's lod
+
+def footprint_to_level(area_texels, n_levels):
+    """render.py:334-337: fractional mip level of a footprint area given in
+    level-0 texels^2."""
+    lvl = 0.5 * np.log2(np.maximum(np.asarray(area_texels, dtype=np.float64), 1.0))
+    return np.clip(lvl, 0.0, n_levels - 1)
+
+
+def cone_level(cone_w, cone_s, t, cos_hit, density, n_levels):
+    """render.py:436-443 (_surface_frames_and_level): ray-cone width at the hit,
+    foreshortened by the hit cosine (floored at 0.05), squared in texels."""
+    width = np.asarray(cone_w, np.float64) + np.asarray(cone_s, np.float64) * np.asarray(t, np.float64)
+    diam = width / np.maximum(np.abs(np.asarray(cos_hit, np.float64)), 0.05)
+    area = (diam * np.asarray(density, np.float64)) ** 2
+    return footprint_to_level(area, n_levels)

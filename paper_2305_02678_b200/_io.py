@@ -2,6 +2,8 @@
 the device pointers the C ABI takes.  torch is used only for device memory
 and streams."""
 
+import os
+
 import numpy as np
 import torch
 
@@ -82,7 +84,7 @@ def out(t, numpy_mode, np_dtype=np.float64):
 # engines + the SMs busy).  Host buffers should be pinned for real overlap;
 # pageable memory still works (the driver stages it synchronously).
 
-STREAM_CHUNK = 1 << 18
+STREAM_CHUNK = int(os.environ.get("NMQ_STREAM_CHUNK", 1 << 19))  # queries per chunk
 _STREAMS = {}
 
 

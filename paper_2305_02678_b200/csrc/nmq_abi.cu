@@ -592,6 +592,30 @@ int nm_query(const nm_material* m, int64_t n, const float* uv, const float* lod,
   return finish(m, launch_fused(m->mp, kModeQuery, a, (cudaStream_t)stream), "nm_query");
 }
 
+int nm_footprint_level(int64_t n, const double* area_texels, int32_t n_levels, double* level_out,
+                       void* stream) {
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!area_texels || !level_out) return fail(NM_ERR_INVALID, "null input");
+  if (n_levels < 1) return fail(NM_ERR_INVALID, "n_levels must be >= 1");
+  return finish(nullptr, launch_footprint_level(n, area_texels, n_levels, level_out, (cudaStream_t)stream),
+                "nm_footprint_level");
+}
+
+int nm_cone_level(int64_t n, const float* cone_w, const float* cone_s, const float* t,
+                  const float* cos_hit, const float* density, int32_t density_stride,
+                  int32_t n_levels, float* lod_out, void* stream) {
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!cone_w || !cone_s || !t || !cos_hit || !density || !lod_out)
+    return fail(NM_ERR_INVALID, "null input");
+  if (n_levels < 1) return fail(NM_ERR_INVALID, "n_levels must be >= 1");
+  return finish(nullptr, launch_cone_level(n, cone_w, cone_s, t, cos_hit, density,
+                                           density_stride ? 1 : 0, n_levels, lod_out,
+                                           (cudaStream_t)stream),
+                "nm_cone_level");
+}
+
 size_t nm_multi_workspace_bytes(int64_t n, int32_t n_mats) {
   if (n < 0 || n_mats <= 0) return 0;
   const size_t div = (size_t)n_mats * sizeof(MatParams) + 256;

@@ -133,6 +133,12 @@ cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatPar
                                   int32_t n_mats, const int32_t* mat_id, const QueryArgs& a,
                                   cudaStream_t s);
 int smem_bytes_for(const MatParams& mp);
+// level of detail from ray cones (nmq_lod.cu)
+cudaError_t launch_footprint_level(int64_t n, const double* area, int32_t n_levels, double* out,
+                                   cudaStream_t s);
+cudaError_t launch_cone_level(int64_t n, const float* cone_w, const float* cone_s, const float* t,
+                              const float* cos_hit, const float* density, int32_t density_stride,
+                              int32_t n_levels, float* lod, cudaStream_t s);
 extern int64_t g_launches;
 // kernel path: 0 = auto (tcgen05 pipelined, then warp-tile, then generic),
 // 1 = generic only, 2 = tcgen05 pipelined, 3 = warp-tile (each falls back to generic)

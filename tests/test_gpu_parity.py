@@ -318,3 +318,37 @@ def test_streamed_host_eval_matches_device_path():
     f64, _, _ = neural.eval_material(mat, host["uv"], host["lod"], host["wi"], host["wo"],
                                      host["u_rr"], fp16=True, return_level=False)
     assert f64.dtype == np.float64 and np.array_equal(f64, f_dev.cpu().numpy().astype(np.float64))
+
+
+def test_lod_from_ray_cones_vs_reference_goldens():
+    """GPU LoD from ray cones (csrc/nmq_lod.cu) against the reference renderer:
+    footprint levels within 1 ulp of float64, cone levels equal to the
+    reference's float64 level rounded to fp32 (the query API's lod type), and
+    the chosen mip level through the fused eval identical to the reference's."""
+    import torch
+    from paper_2305_02678_b200 import render
+
+    g = load_golden("lod")
+    L = int(g["n_levels"])
+    lvl = render.footprint_to_level(g["area"], L)
+    assert lvl.dtype == np.float64
+    assert np.all(np.abs(lvl - g["area_level"]) <= 4 * np.spacing(np.maximum(g["area_level"], 1e-300)))
+    f32 = {k: g[k].astype(np.float32) for k in ("cone_w", "cone_s", "t", "cos_hit")}
+    lod = render.cone_level(f32["cone_w"], f32["cone_s"], f32["t"], f32["cos_hit"],
+                            float(np.float32(g["density"])), L)
+    assert lod.dtype == np.float32
+    # the reference's float64 level on the same (fp32) inputs, rounded to fp32
+    from oracle import nm_oracle as O
+    ref = O.cone_level(f32["cone_w"], f32["cone_s"], f32["t"], f32["cos_hit"],
+                       np.float32(g["density"]), L).astype(np.float32)
+    assert np.array_equal(lod, ref)
+    # and the reference renderer's own levels (f64 cos_hit) to fp32 rounding
+    assert np.abs(lod - g["level"]).max() <= 2e-6
+    # device tensors in -> device tensor out, per-hit densities
+    dev = torch.device("cuda", 0)
+    T = lambda a: torch.from_numpy(np.asarray(a, np.float32)).to(dev)  # noqa: E731
+    dens = np.full(len(g["t"]), float(g["density"]), np.float32)
+    lod_t = render.cone_level(T(g["cone_w"]), T(g["cone_s"]), T(g["t"]), T(g["cos_hit"]), T(dens), L)
+    assert lod_t.is_cuda and np.array_equal(lod_t.cpu().numpy(), lod)
+    with pytest.raises(ValueError):
+        render.cone_level(g["cone_w"], g["cone_s"][:5], g["t"], g["cos_hit"], 1.0, L)

@@ -92,3 +92,13 @@ def test_oracle_zenith_pdf_goldens():
     assert O.pdf(mk(1.0, (0.5, 0.5)), z, z)[0] == pytest.approx(1 / np.pi, rel=1e-12)
     assert O.pdf(mk(0.0, (1.0, 1.0)), z, z)[0] == pytest.approx(1 / (4 * np.pi), rel=1e-9)
     assert O.pdf(mk(0.5, (1.0, 1.0)), z, z)[0] == pytest.approx(0.5 / np.pi + 0.5 / (4 * np.pi), rel=1e-9)
+
+
+def test_lod_from_ray_cones_matches_reference():
+    """render._surface_frames_and_level / footprint_to_level goldens
+    (produced by the reference renderer itself, oracle/make_golden.py)."""
+    from oracle import nm_oracle as O
+    g = load_golden("lod")
+    lv = O.cone_level(g["cone_w"], g["cone_s"], g["t"], g["cos_hit"], g["density"], int(g["n_levels"]))
+    assert np.array_equal(lv, g["level"])
+    assert np.array_equal(O.footprint_to_level(g["area"], int(g["n_levels"])), g["area_level"])
