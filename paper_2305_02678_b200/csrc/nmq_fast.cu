@@ -50,7 +50,7 @@ using namespace dev;
 #define NMQ_G_EVAL 7
 #endif
 #ifndef NMQ_G_SAMPLE
-#define NMQ_G_SAMPLE 5
+#define NMQ_G_SAMPLE 6  // with SMEM texel staging (NMQ_TEX_SMEM); 5 with register prefetch
 #endif
 #ifndef NMQ_G_QUERY
 #define NMQ_G_QUERY 5
@@ -306,6 +306,33 @@ __device__ __forceinline__ void prefetch_texels(const MatParams& mp, const Query
   for (int k = 0; k < 4; ++k) p.tex[k] = __ldg(mp.latent + tap_index(t, k));
 }
 
+// SMEM variant (TS): the four texels go to this row's 64-byte slot in SMEM
+// by cp.async (LDGSTS, L1-allocating) — no registers held across the MLP
+// chain; only (fx, fy, level) stay live.
+template <int MODE>
+__device__ __forceinline__ void prefetch_texels_smem(const MatParams& mp, const QueryArgs& a,
+                                                     const InBuf<MODE>& ib, int r, float lod0,
+                                                     uint32_t row_smem, TexPrefetch& p) {
+  const float u = ib.uv[2 * r], v = ib.uv[2 * r + 1];
+  const float lod = a.lod_stride ? ib.lod[r] : lod0;
+  p.level = choose_level(mp, lod, ib.urr[r]);
+  const Taps t = make_taps(mp, p.level, u, v);
+  p.fx = t.fx;
+  p.fy = t.fy;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tc::cp_async16(row_smem + 16 * k, mp.latent + tap_index(t, k));
+  tc::cp_async_commit();
+}
+__device__ __forceinline__ void land_texels_smem(uint32_t row_smem, TexPrefetch& p) {
+  tc::cp_async_wait<0>();
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(p.tex[k].x), "=r"(p.tex[k].y), "=r"(p.tex[k].z), "=r"(p.tex[k].w)
+                 : "r"(row_smem + 16 * k)
+                 : "memory");
+}
+
 // blended latent code of one row, packed fp16 pairs (the MLP input rounding)
 __device__ __forceinline__ void blend_pack(const TexPrefetch& p, uint32_t (&zp)[4]) {
   float2 z[4];
@@ -330,7 +357,7 @@ struct SlotSt {
   TexPrefetch nx;   // texels of the slot's next tile
 };
 
-template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS>
+template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS>
 __global__ void __launch_bounds__(G * 128, 1)
 fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
             const __grid_constant__ FastConsts fc) {
@@ -362,6 +389,9 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
 
   const uint32_t wbytes = (mp.wblob_bytes + 127) & ~127u;
   InBuf<MODE>* ibuf = reinterpret_cast<InBuf<MODE>*>(smem + wbytes) + gi * NS * 2;
+  // TS: per-row 64-byte texel slots after all input buffers
+  const uint32_t tex_row = tc::smem_u32(smem + wbytes + G * NS * 2 * sizeof(InBuf<MODE>)) +
+                           (uint32_t)((gi * NS) * kTile + tid % 128) * 64u;
 
   // --- CTA setup --------------------------------------------------------------
   if (tid < G * NS) {
@@ -501,7 +531,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           // the slot's next tile: texel loads now, blended at the last stage
           if (S.t + sstride < ntiles) {
             wait_in(S, s, b ^ 1, S.t + sstride);
-            prefetch_texels<MODE>(mp, a, buf(s, b ^ 1), r, lod0, S.nx);
+            if constexpr (TS)
+              prefetch_texels_smem<MODE>(mp, a, buf(s, b ^ 1), r, lod0, tex_row + s * kTile * 64u, S.nx);
+            else
+              prefetch_texels<MODE>(mp, a, buf(s, b ^ 1), r, lod0, S.nx);
           }
           auto refill = [&]() {  // after the barrier: every row of buffer b was read
             if (t2 < last_full) {
@@ -608,6 +641,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           // the slot's next tile: blend its texels, issue its first MMA
           const int tn = S.t + sstride;
           if (tn < ntiles) {
+            if constexpr (TS) land_texels_smem(tex_row + s * kTile * 64u, S.nx);
             blend_pack(S.nx, S.zp);
             S.level = S.nx.level;
             issue_first(S, buf(s, b ^ 1), std::integral_constant<int, LW>{});
@@ -647,15 +681,24 @@ FastConsts make_consts(int brdf_nh, int samp_nh) {
 
 int g_sms = 0;
 
-template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS>
+#ifndef NMQ_TEX_SMEM
+// bit per mode (1 << MODE): stage texel prefetches in SMEM by cp.async
+// instead of registers — frees ~19 registers/thread; pays off only where it
+// buys a tile group (sample+pdf: G 5 -> 6, +3 % on C3; eval/query: no gain)
+#define NMQ_TEX_SMEM (1 << kModeSamplePdf)
+#endif
+
+template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS,
+          bool TS = ((NMQ_TEX_SMEM >> MODE) & 1) != 0>
 cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t s) {
   if (!g_sms) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  auto kern = fast_kernel<MODE, BW, BNH, SW, SNH, G, NS>;
-  const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>));
+  auto kern = fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS>;
+  const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>) +
+                         (TS ? G * NS * kTile * 64 : 0));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
