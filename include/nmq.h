@@ -56,6 +56,9 @@ typedef struct nm_net_desc {
   const int32_t* fan_out; /* [n_layers] */
   const int32_t* act;     /* [n_layers] nm_act */
   const uint16_t* packed; /* fp16 bits, host memory */
+  /* fp32 master weights in the same access order (Mlp.layers, mlp.py:50-69);
+   * required when the material is created with precise = 1 */
+  const float* weights;
 } nm_net_desc;
 
 /* Everything NeuralMaterial.half() produces (neural.py:147-161). */
@@ -76,6 +79,12 @@ typedef struct nm_material_desc {
                                 or fp32 when latent_fp32 = 1 */
   int32_t latent_fp32;       /* texels are 8 x fp32 (32 B) instead of 8 x fp16 */
   int32_t latent_on_device;  /* 1: `latent` is a device pointer on `device` */
+  /* 1: the reference's fp32 path (fp16=False: Mlp.forward on fp32 master
+   * weights, neural.py:288-293, 357-360): inputs, hidden activations and
+   * weights each carried as an fp16 (hi, lo) pair on the tensor cores
+   * (W_hi x_hi + W_hi x_lo + W_lo x_hi), fp32 accumulation; pair with the
+   * fp32 master pyramid (latent_fp32 = 1).  0: the fp16 inference path. */
+  int32_t precise;
 } nm_material_desc;
 
 typedef struct nm_material nm_material;

@@ -11,12 +11,18 @@ from . import _lib
 from .mlp import ACT_CODES
 
 
-def _net_desc(qnet, keep):
-    """Fill an NetDesc from a QuantizedMlp (or an empty one for None)."""
+def _net_desc(qnet, keep, master=None):
+    """Fill an NetDesc from a QuantizedMlp (or an empty one for None); with
+    `master` (the fp32 Mlp) also its fp32 weights in the same access order."""
     d = _lib.NetDesc()
     if qnet is None:
         d.n_layers = 0
         return d
+    if master is not None:
+        w32 = np.ascontiguousarray(np.concatenate(
+            [np.concatenate([l.w, l.b[:, None]], axis=1).ravel() for l in master.layers]), np.float32)
+        keep.append(w32)
+        d.weights = w32.ctypes.data_as(ctypes.POINTER(ctypes.c_float))
     fi = np.ascontiguousarray([s[1] for s in qnet.shapes], dtype=np.int32)
     fo = np.ascontiguousarray([s[0] for s in qnet.shapes], dtype=np.int32)
     act = np.ascontiguousarray([ACT_CODES[a] for a in qnet.acts], dtype=np.int32)
@@ -35,7 +41,7 @@ class DeviceMaterial:
 
     def __init__(self, device, width, height, n_levels, latent, latent_fp32=False,
                  frame=None, brdf=None, sampler=None, use_frames=True, n_frames=2,
-                 albedo_head=False, sampler_isotropic=False):
+                 albedo_head=False, sampler_isotropic=False, masters=None):
         lib = _lib.load()
         keep = []
         desc = _lib.MaterialDesc()
@@ -44,9 +50,11 @@ class DeviceMaterial:
         desc.n_frames = int(n_frames)
         desc.albedo_head = int(bool(albedo_head))
         desc.sampler_isotropic = int(bool(sampler_isotropic))
-        desc.frame = _net_desc(frame if use_frames else None, keep)
-        desc.brdf = _net_desc(brdf, keep)
-        desc.sampler = _net_desc(sampler, keep)
+        m = masters or (None, None, None)  # fp32 Mlps: the precise (fp16=False) path
+        desc.precise = int(masters is not None)
+        desc.frame = _net_desc(frame if use_frames else None, keep, m[0])
+        desc.brdf = _net_desc(brdf, keep, m[1])
+        desc.sampler = _net_desc(sampler, keep, m[2])
         desc.width, desc.height, desc.n_levels = int(width), int(height), int(n_levels)
         desc.latent_fp32 = int(bool(latent_fp32))
         if isinstance(latent, torch.Tensor):

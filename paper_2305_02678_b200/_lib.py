@@ -31,6 +31,7 @@ class NetDesc(ctypes.Structure):
         ("fan_out", ctypes.POINTER(ctypes.c_int32)),
         ("act", ctypes.POINTER(ctypes.c_int32)),
         ("packed", ctypes.POINTER(ctypes.c_uint16)),
+        ("weights", ctypes.POINTER(ctypes.c_float)),
     ]
 
 
@@ -50,6 +51,7 @@ class MaterialDesc(ctypes.Structure):
         ("latent", ctypes.c_void_p),
         ("latent_fp32", ctypes.c_int32),
         ("latent_on_device", ctypes.c_int32),
+        ("precise", ctypes.c_int32),
     ]
 
 

@@ -60,13 +60,24 @@ struct NetView {
   std::vector<int> fi, fo, act;
   std::vector<size_t> ofs;  // offset of each layer in the packed array (halves)
   const uint16_t* packed;
+  const float* weights;     // fp32 master weights (same order) or null
 };
+
+// fp32 -> (hi, lo) fp16 bits with hi + lo = v to ~2^-22 (clamped to fp16 range)
+void split_f32(float v, uint16_t& hi, uint16_t& lo) {
+  const float c = v > 65504.f ? 65504.f : (v < -65504.f ? -65504.f : v);
+  const __half h = __float2half_rn(c);
+  const __half l = __float2half_rn(c - __half2float(h));
+  hi = *reinterpret_cast<const uint16_t*>(&h);
+  lo = *reinterpret_cast<const uint16_t*>(&l);
+}
 
 int view_net(const nm_net_desc& d, const char* name, NetView& v) {
   if (d.n_layers <= 0 || !d.fan_in || !d.fan_out || !d.act || !d.packed)
     return fail(NM_ERR_INVALID, std::string(name) + ": empty network description");
   v.n_layers = d.n_layers;
   v.packed = d.packed;
+  v.weights = d.weights;
   size_t o = 0;
   for (int l = 0; l < d.n_layers; ++l) {
     v.fi.push_back(d.fan_in[l]);
@@ -88,6 +99,57 @@ int view_net(const nm_net_desc& d, const char* name, NetView& v) {
 // bias slot at index fan_in; later layers take the hi/lo split of the
 // previous padded activation plus the shared bias chunk.
 int pack_chain(const NetView& v, Packer& pk, MatParams& mp, int& n_layers, const char* name) {
+  if (mp.precise) {
+    // fp32 path: B = [W_hi | W_hi | W_lo] (+ bias chunk [b_hi, 0, b_lo, 0 ...]
+    // for hidden-input layers, against the A bias chunk (1, 0, 1, 0 ...))
+    if (!v.weights) return fail(NM_ERR_INVALID, std::string(name) + ": precise material needs fp32 weights");
+    for (int l = 0; l < v.n_layers; ++l) {
+      if (n_layers >= kMaxLayers) return fail(NM_ERR_UNSUPPORTED, "too many layers");
+      LayerDesc L{};
+      const int fi = v.fi[l], fo = v.fo[l];
+      const int n_pad = round_up(fo, 16);
+      if (n_pad > kMaxWidth)
+        return fail(NM_ERR_UNSUPPORTED, std::string(name) + ": layer width > 64 not supported");
+      L.n_pad = (uint16_t)n_pad;
+      L.out = (uint8_t)fo;
+      L.act = (uint8_t)v.act[l];
+      L.precise = 1;
+      const float* w = v.weights + v.ofs[l];  // [fo][fi+1]
+      auto put3 = [&](uint32_t off, int kp, int n, int k, float val) {
+        uint16_t hi, lo;
+        split_f32(val, hi, lo);
+        pk.set(off, n_pad, n, k, hi);
+        pk.set(off, n_pad, n, kp + k, hi);
+        pk.set(off, n_pad, n, 2 * kp + k, lo);
+      };
+      if (l == 0) {
+        const int k_pad = round_up(fi + 1, 16);
+        if (k_pad > 32) return fail(NM_ERR_UNSUPPORTED, std::string(name) + ": input too wide");
+        L.first = 1;
+        L.ksteps = (uint8_t)(k_pad / 16);
+        L.b_off = pk.append(n_pad, 3 * k_pad / 8);
+        if (k_pad > mp.dmax) mp.dmax = k_pad;  // A holds x_hi and x_lo: k_pad columns
+        for (int n = 0; n < fo; ++n)
+          for (int k = 0; k <= fi; ++k) put3(L.b_off, k_pad, n, k, w[(size_t)n * (fi + 1) + k]);
+      } else {
+        const int in_pad = round_up(fi, 16);
+        L.first = 0;
+        L.in_pad = (uint16_t)in_pad;
+        L.ksteps = (uint8_t)(3 * in_pad / 16 + 1);
+        L.b_off = pk.append(n_pad, 3 * in_pad / 8 + 2);
+        for (int n = 0; n < fo; ++n) {
+          for (int k = 0; k < fi; ++k) put3(L.b_off, in_pad, n, k, w[(size_t)n * (fi + 1) + k]);
+          uint16_t bh, bl;
+          split_f32(w[(size_t)n * (fi + 1) + fi], bh, bl);
+          pk.set(L.b_off, n_pad, n, 3 * in_pad, bh);
+          pk.set(L.b_off, n_pad, n, 3 * in_pad + 2, bl);
+        }
+      }
+      if ((int)L.n_pad > mp.dmax) mp.dmax = L.n_pad;
+      mp.layers[n_layers++] = L;
+    }
+    return NM_OK;
+  }
   for (int l = 0; l < v.n_layers; ++l) {
     if (n_layers >= kMaxLayers) return fail(NM_ERR_UNSUPPORTED, "too many layers");
     LayerDesc L{};
@@ -328,6 +390,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
   mp.n_frames = d->use_frames ? d->n_frames : 0;
   mp.albedo = d->albedo_head ? 1 : 0;
   mp.isotropic = d->sampler_isotropic ? 1 : 0;
+  mp.precise = d->precise ? 1 : 0;
   mp.frame_layer = -1;
   int rc;
   NetView fv, bv, sv;
@@ -384,7 +447,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     m->sampler_width = m->sampler_width > mp.layers[l].n_pad ? m->sampler_width : mp.layers[l].n_pad;
   if (mp.dmax < 16) mp.dmax = 16;
   if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
-  mp.fast_arch = detect_fast_arch(mp, bv, sv, d);
+  mp.fast_arch = mp.precise ? -1 : detect_fast_arch(mp, bv, sv, d);
   Packer wk;
   if (mp.fast_arch >= 0) {
     fill_fast_layers(mp, pk, fv, bv);
@@ -642,6 +705,7 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
     if (!mats[k]) return fail(NM_ERR_INVALID, "null material");
     if (mats[k]->device != dev) return fail(NM_ERR_INVALID, "materials on different devices");
     if (!mats[k]->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+    if (mats[k]->mp.precise) return fail(NM_ERR_UNSUPPORTED, "multi-material eval is fp16-path only");
     mps[k] = &mats[k]->mp;
   }
   QueryArgs a{};

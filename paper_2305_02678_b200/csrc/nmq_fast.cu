@@ -510,8 +510,8 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
         SlotSt& S = sl[s];
         if (s > 0 && S.t >= ntiles) return;  // uniform per group
         const int b = S.it & 1;
-        const int64_t q = (int64_t)S.t * kTile + r;
-        const bool valid = q < a.n;
+        const int64_t q_in = (int64_t)S.t * kTile + r;  // input row
+        const bool valid = q_in < a.n;
         const int t2 = S.t + 2 * sstride;
         constexpr int PW = (k + s) % 4;  // warp polling the previous MMA's completion
         auto wait_mma = [&]() { mma_wait<PW>(g, S.bar, S.ph); };
@@ -526,7 +526,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           if constexpr (Need<MODE>::u3) S.u3 = v3(ib.u3[3 * r], ib.u3[3 * r + 1], ib.u3[3 * r + 2]);
           S.up = (S.wi.z > 0.f) && (wo.z > 0.f);
           if (want_level) {
-            if (valid) a.level[q] = S.level;
+            if (valid) a.level[a.out_idx ? (int64_t)__ldg(a.out_idx + q_in) : q_in] = S.level;
           }
           // the slot's next tile: texel loads now, blended at the last stage
           if (S.t + sstride < ntiles) {
@@ -581,6 +581,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           float y[6];
           out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
           if (valid) {
+            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + q_in) : q_in;
             const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                               : v3(0.f, 0.f, 0.f);
             stg3(a.rgb, q, f);
@@ -631,6 +632,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           for (int j = 0; j < 9; ++j) raw[j] = __uint_as_float(yr[j]);
           const Proxy p = proxy_from_raw(raw, mp.isotropic != 0, fc.inv_samp);
           if (valid) {
+            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + q_in) : q_in;
             if (a.params9) store_proxy(a.params9, q, p);
             const V3 w = proxy_sample(p, S.wi, S.u3.x, S.u3.y, S.u3.z);
             stg3(a.ws, q, w);

@@ -32,6 +32,7 @@ struct LayerDesc {
   uint8_t first;
   uint8_t act;      // 0 linear, 1 leaky
   uint8_t out;      // true (unpadded) output width
+  uint8_t precise;  // fp32 path: B = [W_hi | W_hi | W_lo] against A = [x_hi | x_lo | x_hi]
 };
 
 struct MatParams {
@@ -50,6 +51,7 @@ struct MatParams {
   int32_t brdf_in;                // fan_in of the first BRDF layer (8 + 6*n_frames or 14)
   int32_t dmax;                   // max n_pad / in_pad over all layers (16/32/48/64)
   int32_t fast_arch;              // specialized pipelined kernel id (nmq_fast.cu), -1 = generic
+  int32_t precise;                // fp32 path (generic kernel only)
   LayerDesc layers[kMaxLayers];
   // Specialized kernels (nmq_fast.cu) share one K=16 input chunk between the
   // frame layer, the sampler's first layer and the BRDF decoder's first
@@ -98,7 +100,9 @@ struct QueryArgs {
   const float* wi;
   const float* wo;
   const float* u3;
-  const int32_t* idx;   // optional indirection (binned multi-material): query = idx[i]
+  const int32_t* idx;   // optional indirection (generic kernel): query = idx[i]
+  const int32_t* out_idx;  // optional output rows: results of row i go to row out_idx[i]
+                           // (binned multi-material writes straight to query order)
   float* rgb;
   float* albedo;
   float* ws;

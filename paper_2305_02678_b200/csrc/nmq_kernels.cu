@@ -53,7 +53,17 @@ __device__ __forceinline__ void run_layer(const LayerDesc& L, Group& g) {
     const uint32_t idesc = tc::idesc_f16(128, L.n_pad);
     const uint32_t lbo = (uint32_t)L.n_pad * 16u;
     const uint32_t b0 = g.smem_w + L.b_off;
-    if (L.first) {
+    if (L.precise) {
+      // fp32 path: A = [x_hi | x_lo] (ks k-steps each), B = [W_hi | W_hi | W_lo]:
+      // W_hi x_hi + W_hi x_lo + W_lo x_hi (+ bias chunk [b_hi, 0, b_lo] vs (1, 0, 1))
+      const uint32_t ks = L.first ? L.ksteps : (uint32_t)L.in_pad / 16u;
+      for (uint32_t p = 0; p < 3; ++p)
+        for (uint32_t s = 0; s < ks; ++s)
+          tc::mma_ts(g.d0, g.a0 + 8 * (s + (p == 1 ? ks : 0)),
+                     tc::smem_desc(b0 + (p * ks + s) * 2 * lbo, lbo, 128), idesc, (p | s) != 0);
+      if (!L.first)
+        tc::mma_ts(g.d0, g.bias_col, tc::smem_desc(b0 + 3 * ks * 2 * lbo, lbo, 128), idesc, 1);
+    } else if (L.first) {
       for (uint32_t s = 0; s < L.ksteps; ++s)
         tc::mma_ts(g.d0, g.a0 + 8 * s, tc::smem_desc(b0 + s * 2 * lbo, lbo, 128), idesc, s > 0);
     } else {
@@ -70,11 +80,31 @@ __device__ __forceinline__ void run_layer(const LayerDesc& L, Group& g) {
 }
 
 // First-layer input: x[0..2*NC) as fp16 pairs into A columns [0, NC)
+// (fp16 path: the input rounded to fp16 once, mlp.py:205); with `precise`
+// the fp32 input as hi pairs in [0, NC) and lo pairs in [NC, 2 NC).
 template <int NC>
-__device__ __forceinline__ void write_input(const Group& g, const float* x) {
+__device__ __forceinline__ void write_input(const Group& g, const float* x, bool precise = false) {
   uint32_t r[NC];
+  if (precise) {
+    uint32_t lo[NC];
 #pragma unroll
-  for (int j = 0; j < NC; ++j) r[j] = h2bits(__floats2half2_rn(x[2 * j], x[2 * j + 1]));
+    for (int j = 0; j < NC; ++j) {
+      const __half2 h = __floats2half2_rn(x[2 * j], x[2 * j + 1]);
+      const float2 hf = __half22float2(h);
+      r[j] = h2bits(h);
+      lo[j] = h2bits(__floats2half2_rn(x[2 * j] - hf.x, x[2 * j + 1] - hf.y));
+    }
+#pragma unroll
+    for (int c = 0; c < NC; c += 8) {
+      uint32_t q[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q[j] = lo[c + j];
+      tc::tmem_st8(g.lane + g.a0 + NC + c, q);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) r[j] = h2bits(__floats2half2_rn(x[2 * j], x[2 * j + 1]));
+  }
   if constexpr (NC == 8) {
     tc::tmem_st8(g.lane + g.a0, r);
   } else {
@@ -157,7 +187,7 @@ __device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const
 #pragma unroll
     for (int k = 0; k < 8; ++k) xf[k] = z[k];
     xf[8] = 1.f;  // bias slot
-    write_input<8>(g, xf);
+    write_input<8>(g, xf, mp.precise != 0);
     run_layer(mp.layers[mp.frame_layer], g);
     float raw[16];
     output_epilogue(g, raw);
@@ -194,8 +224,8 @@ __device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const
   // bias slot of the first BRDF layer (index = fan_in)
   if (mp.brdf_in == 20) x[20] = 1.f;  // 2 frames
   else x[14] = 1.f;                   // 1 frame or no frames (host-validated)
-  if (mp.layers[mp.brdf_first].ksteps == 1) write_input<8>(g, x);
-  else write_input<16>(g, x);
+  if (mp.layers[mp.brdf_first].ksteps == 1) write_input<8>(g, x, mp.precise != 0);
+  else write_input<16>(g, x, mp.precise != 0);
   run_chain(mp, mp.brdf_first, mp.brdf_count, g, y);
 }
 
@@ -208,7 +238,7 @@ __device__ __forceinline__ Proxy sampler_decode(const MatParams& mp, Group& g,
   x[11] = 1.f;  // bias slot
 #pragma unroll
   for (int k = 12; k < 16; ++k) x[k] = 0.f;
-  write_input<8>(g, x);
+  write_input<8>(g, x, mp.precise != 0);
   float y[16];
   run_chain(mp, mp.samp_first, mp.samp_count, g, y);
   return proxy_from_raw(y, mp.isotropic != 0);
@@ -247,7 +277,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
   const uint32_t tb = tbase_sh;
   const uint32_t bias_col = tb + (uint32_t)G * group_cols;
   if (warp < 4) {
-    const uint32_t v[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};  // fp16 1.0 at k = 0
+    const uint32_t v[8] = {0x3C00u, 0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u};  // fp16 1.0 at k = 0, 2
     tc::tmem_st8(bias_col + ((uint32_t)(warp * 32) << 16), v);
     tc::tmem_st_wait();
   }
@@ -272,6 +302,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
     const int64_t i = tile * kTile + r;
     const bool valid = i < a.n;
     const int64_t q = valid ? (a.idx ? (int64_t)__ldg(a.idx + i) : i) : 0;
+    const int64_t oq = valid ? (a.out_idx ? (int64_t)__ldg(a.out_idx + i) : q) : 0;  // output row
 
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
     float z[8];
@@ -298,7 +329,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
       const int level = choose_level(mp, lod, urr);
       const Taps t = make_taps(mp, level, u, v);
       fetch_taps(mp, t, z);
-      if (valid && a.level) a.level[q] = level;
+      if (valid && a.level) a.level[oq] = level;
     }
 
     if constexpr (MODE == kModeEval || MODE == kModeEvalZ || MODE == kModeQuery) {
@@ -308,23 +339,23 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
         const bool up = (wi.z > 0.f) && (wo.z > 0.f);
         const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                         : v3(0.f, 0.f, 0.f);
-        stg3(a.rgb, q, f);
+        stg3(a.rgb, oq, f);
         if (mp.albedo && a.albedo) {
           const V3 al = up ? v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f))
                            : v3(0.f, 0.f, 0.f);
-          stg3(a.albedo, q, al);
+          stg3(a.albedo, oq, al);
         }
       }
     }
     if constexpr (MODE == kModeProxyZ || MODE == kModeSamplePdf || MODE == kModeQuery) {
       const Proxy p = sampler_decode(mp, g, z, wi);
       if (valid) {
-        if (a.params9) store_proxy(a.params9, q, p);
+        if (a.params9) store_proxy(a.params9, oq, p);
         if constexpr (MODE != kModeProxyZ) {
           const V3 u3 = ldg3(a.u3, q);
           const V3 s = proxy_sample(p, wi, u3.x, u3.y, u3.z);
-          stg3(a.ws, q, s);
-          a.pdf[q] = proxy_pdf(p, wi, s);
+          stg3(a.ws, oq, s);
+          a.pdf[oq] = proxy_pdf(p, wi, s);
         }
       }
     }
@@ -393,7 +424,7 @@ divergent_eval_kernel(const MatParams* __restrict__ mps_g, int32_t n_mats,
   const uint32_t tb = tbase_sh;
   const uint32_t bias_col = tb + (uint32_t)G * group_cols;
   if (warp < 4) {
-    const uint32_t v[8] = {0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    const uint32_t v[8] = {0x3C00u, 0x3C00u, 0u, 0u, 0u, 0u, 0u, 0u};
     tc::tmem_st8(bias_col + ((uint32_t)(warp * 32) << 16), v);
     tc::tmem_st_wait();
   }

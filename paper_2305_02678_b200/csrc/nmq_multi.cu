@@ -5,9 +5,10 @@
 //  * BINNED: queries are binned by material id with warp-aggregated
 //    counting (__match_any_sync + __popc, one atomic per distinct id per
 //    warp), an exclusive scan, and a warp-aggregated scatter that permutes
-//    the inputs into contiguous per-material segments; the coherent fused
-//    kernel then runs once per segment and a final pass scatters the outputs
-//    back to query order.
+//    the inputs into contiguous per-material segments (16-byte aligned); the
+//    coherent fused kernel then runs once per segment and writes each result
+//    straight to its query's row (output-row indirection, no scatter-back
+//    pass).
 //  * DIVERGENT: no reordering; every 128-query tile loops over the
 //    materials present in it and decodes the whole tile with each of them,
 //    keeping each row's own material (nmq_kernels.cu, kModeEvalMulti).
@@ -52,6 +53,8 @@ __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mat
     if (sc[i]) atomicAdd(counts + i, sc[i]);
 }
 
+// Segment offsets padded to multiples of 4 rows, so every segment's staged
+// inputs are 16-byte aligned (TMA / the specialized kernels).
 __global__ void bin_scan_kernel(int32_t n_mats, const int32_t* __restrict__ counts,
                                 int32_t* __restrict__ offsets, int32_t* __restrict__ cursor) {
   if (threadIdx.x == 0) {
@@ -59,7 +62,7 @@ __global__ void bin_scan_kernel(int32_t n_mats, const int32_t* __restrict__ coun
     for (int m = 0; m < n_mats; ++m) {
       offsets[m] = acc;
       cursor[m] = acc;
-      acc += counts[m];
+      acc += (counts[m] + 3) & ~3;
     }
     offsets[n_mats] = acc;
   }
@@ -98,17 +101,6 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
   }
 }
 
-__global__ void __launch_bounds__(256) unpermute3_kernel(int64_t n, const int32_t* __restrict__ order,
-                                                         const float* __restrict__ src,
-                                                         float* __restrict__ dst) {
-  for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < n;
-       s += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = __ldg(order + s);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) dst[3 * i + k] = __ldg(src + 3 * s + k);
-  }
-}
-
 int grid256(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -118,16 +110,19 @@ int grid256(int64_t n) {
 }  // namespace
 
 size_t multi_workspace_bytes(int64_t n, int32_t n_mats) {
-  // counts, offsets(+1), cursor, bad flag | order | uv lod urr wi wo | rgb
-  return 256 + (size_t)(3 * n_mats + 2) * 4 + (size_t)n * (4 + 40 + 12) + 64 * 8;
+  // counts, offsets(+1), cursor, bad flag | order | uv lod urr wi wo
+  // (segments padded to 4 rows: n + 4 n_mats rows)
+  const size_t rows = (size_t)n + 4 * (size_t)n_mats;
+  return 256 + (size_t)(3 * n_mats + 2) * 4 + rows * (4 + 40) + 64 * 8;
 }
 
 struct MultiWs {
   int32_t *counts, *offsets, *cursor, *bad, *order;
-  float *uv, *lod, *urr, *wi, *wo, *rgb;
+  float *uv, *lod, *urr, *wi, *wo;
 };
 
-static MultiWs carve(void* ws, int64_t n, int32_t n_mats) {
+static MultiWs carve(void* ws, int64_t n_rows, int32_t n_mats) {
+  const int64_t n = n_rows + 4 * (int64_t)n_mats;
   auto align = [](uintptr_t p) { return (p + 255) & ~(uintptr_t)255; };
   uintptr_t p = align((uintptr_t)ws);
   MultiWs w;
@@ -140,8 +135,7 @@ static MultiWs carve(void* ws, int64_t n, int32_t n_mats) {
   p = align(p); w.lod = (float*)p; p += n * 4;
   p = align(p); w.urr = (float*)p; p += n * 4;
   p = align(p); w.wi = (float*)p; p += n * 12;
-  p = align(p); w.wo = (float*)p; p += n * 12;
-  p = align(p); w.rgb = (float*)p;
+  p = align(p); w.wo = (float*)p;
   return w;
 }
 
@@ -179,14 +173,13 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
       sa.u_rr = w.urr + off;
       sa.wi = w.wi + 3 * off;
       sa.wo = w.wo + 3 * off;
-      sa.rgb = w.rgb + 3 * off;
+      sa.rgb = a.rgb;             // results go straight back to query order
+      sa.out_idx = w.order + off;
       if ((e = launch_fused(*mps[m], kModeEval, sa, s)) != cudaSuccess) return e;
     }
-    off += c;
+    off += (c + 3) & ~3;
   }
-  unpermute3_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, w.order, w.rgb, a.rgb);
-  ++g_launches;
-  return cudaGetLastError();
+  return cudaSuccess;
 }
 
 }  // namespace nmq

@@ -123,10 +123,32 @@ class NeuralMaterial:
             total += h["frame"].clamped
         return total
 
-    def device_material(self, device=None):
-        """The immutable device copy (fp16 weights re-tiled for tcgen05, fp16
-        texels) on `device`, built once and cached like half()."""
+    def device_material(self, device=None, precise=False):
+        """The immutable device copy on `device`, built once and cached like
+        half(): fp16 weights re-tiled for tcgen05 + fp16 texels (the fp16
+        inference path), or with `precise` the fp32 master weights (as fp16
+        hi/lo pairs) + the fp32 master pyramid (the reference's fp16=False path)."""
         dev = _io.cuda_device(device)
+        if precise:
+            key = (dev.index, "fp32")
+            h = self._dev.get(key)
+            if h is None:
+                if isinstance(self.latent, DeviceLatent):
+                    raise NotImplementedError(
+                        "a device-only fp16 latent pyramid has no fp32 master copy (use fp16=True)")
+                q = self.half()
+                if self.latent is not None:
+                    blob, fp32 = self.latent.texel_blob()
+                    w, hh, nl = self.latent.width, self.latent.height, self.latent.n_levels
+                else:
+                    blob, fp32, w, hh, nl = np.zeros((1, 8), np.float32), True, 1, 1, 1
+                h = DeviceMaterial(dev, w, hh, nl, blob, fp32, q["frame"], q["brdf"], q["sampler"],
+                                   use_frames=self.cfg.use_frames, n_frames=self.cfg.n_frames,
+                                   albedo_head=self.cfg.albedo_head,
+                                   sampler_isotropic=self.cfg.sampler_isotropic,
+                                   masters=(self.frame_layer, self.brdf_decoder, self.sampler_decoder))
+                self._dev[key] = h
+            return h
         h = self._dev.get(dev.index)
         if h is None:
             q = self.half()
@@ -176,9 +198,7 @@ class DeviceLatent:
 
 def _require_fp16(fp16):
     if not fp16:
-        raise NotImplementedError(
-            "the GPU query path implements the reference's fp16 inference path "
-            "(pass fp16=True); the fp32 training-time path is not on the query path")
+        raise NotImplementedError("this entry point implements the fp16 inference path (fp16=True)")
 
 
 def _launch(fn, *args):
@@ -188,9 +208,8 @@ def _launch(fn, *args):
 def eval_brdf(mat, z, wi, wo, fp16=False):
     """BRDF values (and albedo when enabled) from latent codes (neural.py:273-300).
     Directions below the horizon yield zero."""
-    _require_fp16(fp16)
     np_mode = _io.is_numpy_like(z)
-    h = mat.device_material(None if np_mode else z.device)
+    h = mat.device_material(None if np_mode else z.device, precise=not fp16)
     dev = h.device
     z_t = _io.as_rows(z, LATENT_CHANNELS, dev, "z")
     n = z_t.shape[0]
@@ -207,9 +226,9 @@ def eval_brdf(mat, z, wi, wo, fp16=False):
 
 
 class _QueryInputs:
-    def __init__(self, mat, uv, level, u_rr, need, **dirs):
+    def __init__(self, mat, uv, level, u_rr, need, fp16=True, **dirs):
         self.np_mode = _io.is_numpy_like(uv)
-        self.h = mat.device_material(None if self.np_mode else uv.device)
+        self.h = mat.device_material(None if self.np_mode else uv.device, precise=not fp16)
         dev = self.dev = self.h.device
         self.uv = _io.as_rows(uv, 2, dev, "uv")
         n = self.n = self.uv.shape[0]
@@ -257,12 +276,11 @@ def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, o
     `out` may pass a preallocated (B,3) fp32 device tensor, or a host (ideally
     pinned) fp32 buffer, for f.  Large host batches without albedo or level
     outputs stream through the GPU in overlapped chunks."""
-    _require_fp16(fp16)
-    if not return_level and _io.is_numpy_like(uv) and (out is None or isinstance(out, np.ndarray)):
+    if fp16 and not return_level and _io.is_numpy_like(uv) and (out is None or isinstance(out, np.ndarray)):
         f = _stream_eval(mat, uv, level, wi, wo, u_rr, out)
         if f is not None:
             return f, None, None
-    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), wi=wi, wo=wo)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), fp16=fp16, wi=wi, wo=wo)
     on_dev = isinstance(out, torch.Tensor) and out.is_cuda
     f = out if on_dev else _io.empty(q.n, 3, q.dev)
     alb = _io.empty(q.n, 3, q.dev) if mat.cfg.albedo_head else None
@@ -283,9 +301,8 @@ def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, o
 def infer_proxy(mat, z, wi, fp16=False):
     """Sampler parameters for latent codes and conditioning directions
     (neural.py:353-362 + proxy_from_raw :317-331)."""
-    _require_fp16(fp16)
     np_mode = _io.is_numpy_like(z)
-    h = mat.device_material(None if np_mode else z.device)
+    h = mat.device_material(None if np_mode else z.device, precise=not fp16)
     dev = h.device
     z_t = _io.as_rows(z, LATENT_CHANNELS, dev, "z")
     n = z_t.shape[0]
@@ -302,8 +319,7 @@ def infer_proxy(mat, z, wi, fp16=False):
 def sample_pdf(mat, uv, level, u_rr, wi, u, fp16=True, return_params=False, return_level=False):
     """Fused fetch + sampler decoder + proxy + sample + pdf: returns
     (ws, pdf[, params][, level]) with ws = sample(params, wi, u), pdf = pdf(params, wi, ws)."""
-    _require_fp16(fp16)
-    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "u"), wi=wi, u=u)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "u"), fp16=fp16, wi=wi, u=u)
     ws = _io.empty(q.n, 3, q.dev)
     p = _io.empty(q.n, 1, q.dev)
     p9 = _io.empty(q.n, 9, q.dev) if return_params else None
@@ -323,8 +339,7 @@ def sample_pdf(mat, uv, level, u_rr, wi, u, fp16=True, return_params=False, retu
 def query(mat, uv, level, u_rr, wi, wo, u, fp16=True, return_level=False):
     """One full query (fetch -> eval(wi, wo) -> proxy(wi) -> sample(u) -> pdf):
     returns (f, ws, pdf[, level])."""
-    _require_fp16(fp16)
-    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo", "u"), wi=wi, wo=wo, u=u)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo", "u"), fp16=fp16, wi=wi, wo=wo, u=u)
     f = _io.empty(q.n, 3, q.dev)
     ws = _io.empty(q.n, 3, q.dev)
     p = _io.empty(q.n, 1, q.dev)

@@ -352,3 +352,59 @@ def test_lod_from_ray_cones_vs_reference_goldens():
     assert lod_t.is_cuda and np.array_equal(lod_t.cpu().numpy(), lod)
     with pytest.raises(ValueError):
         render.cone_level(g["cone_w"], g["cone_s"][:5], g["t"], g["cos_hit"], 1.0, L)
+
+
+# --- the reference's fp32 path (fp16=False, its default) ----------------------
+
+def test_fp32_path_matches_reference_golden():
+    """eval_brdf(fp16=False) against the REAL reference's fp32-path output
+    (golden f_fp32path = reference eval_brdf(mat, z, wi, wo, fp16=False)):
+    fp32 weights and activations on the tensor cores as fp16 (hi, lo) pairs.
+    No fp16 rounding anywhere, so no rounding-tie outliers: tight tolerances."""
+    from paper_2305_02678_b200 import neural
+
+    g = load_golden("c1_2x32")
+    mat = our_material(g)
+    f, _ = neural.eval_brdf(mat, g["z"], g["wi"], g["wo"], fp16=False)
+    r = check_rel(f, g["f_fp32path"], max_tol=1e-3, mean_tol=1e-5, what="fp32 path rgb")
+    assert r.max() < 1e-3
+
+
+@pytest.mark.parametrize("arch", ["2x32", "2x16", "3x64"])
+@pytest.mark.parametrize("variant", [{}, {"albedo_head": True}, {"sampler_isotropic": True},
+                                     {"use_frames": False}, {"n_frames": 1}])
+def test_fp32_path_vs_oracle(arch, variant):
+    """All fp32-path entry points (eval_material, eval_brdf, infer_proxy,
+    sample_pdf, query) against the oracle's restatement of the reference's
+    fp16=False branches (neural.py:288-293, 357-360)."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural, proxy
+    from paper_2305_02678_b200.latent import LatentPyramid
+
+    rng = np.random.default_rng(hash((arch, tuple(variant))) % 2**32)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(brdf_hidden=arch, **variant), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 64, 32).levels)
+    om = _oracle_from(mat)
+    n = 3001
+    uv = rng.random((n, 2)).astype(np.float32)
+    lod = (rng.random(n) * (mat.latent.n_levels - 1)).astype(np.float32)
+    urr = rng.random(n).astype(np.float32)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    wi, wo = wi.astype(np.float32), wo.astype(np.float32)
+    u3 = rng.random((n, 3)).astype(np.float32)
+    f_ref, alb_ref, ch_ref = O.eval_material(om, uv, lod, wi, wo, urr, fp16=False)
+    f, alb, ch = neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=False)
+    assert np.array_equal(ch, ch_ref)
+    check_rel(f, f_ref, max_tol=1e-3, mean_tol=1e-5, what=f"fp32 eval {arch} {variant}")
+    if alb_ref is not None:
+        check_rel(alb, alb_ref, max_tol=1e-3, mean_tol=1e-5, what="fp32 albedo")
+    z, _ = mat.latent.fetch(uv, lod, urr)
+    f2, _ = neural.eval_brdf(mat, z, wi, wo, fp16=False)
+    check_rel(f2, O.eval_brdf(om, z, wi, wo, fp16=False)[0], max_tol=1e-3, mean_tol=1e-5,
+              what="fp32 eval_brdf")
+    p = neural.infer_proxy(mat, z, wi, fp16=False)
+    p_ref = O.infer_proxy(om, z, wi, fp16=False)
+    check_rel(p.as_array(), p_ref.as_array(), max_tol=1e-3, mean_tol=1e-5, what="fp32 proxy")
+    ws, pdf = neural.sample_pdf(mat, uv, lod, urr, wi, u3, fp16=False)
+    ws_ref = O.sample(p_ref, wi, u3)
+    check_dirs(ws, ws_ref, u3, p_ref, wi)

@@ -131,7 +131,13 @@ def test_texel_blob_picks_fp16_only_when_exact():
     assert not fp32 and blob.dtype == np.float16 and blob.shape == (85, 8)
 
 
-def test_fp16_false_is_refused_not_silently_downgraded():
+def test_fp16_false_selects_the_fp32_material_copy():
+    """fp16=False (the reference's default) is served by a separate precise
+    device copy — never silently by the fp16 one; without a GPU it fails loudly."""
+    import inspect
+    src = inspect.getsource(neural.eval_material) + inspect.getsource(neural._QueryInputs)
+    assert "precise=not fp16" in src
     mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), np.random.default_rng(0))
-    with pytest.raises(NotImplementedError):
-        neural.eval_brdf(mat, np.zeros((1, 8)), np.array([[0, 0, 1.0]]), np.array([[0, 0, 1.0]]))
+    with pytest.raises(RuntimeError):  # no CUDA device here: no CPU fallback
+        neural.eval_brdf(mat, np.zeros((1, 8), np.float32), [[0, 0, 1]], [[0, 0, 1]], fp16=False)
+
