@@ -402,6 +402,7 @@ def run_c4(args):
 
     steps = max(3, args.steps // 10)
     ms_b = _time_loop(step(_lib.NM_MULTI_BINNED), steps, args.warmup, stream, world)
+    ms_a = _time_loop(step(_lib.NM_MULTI_BINNED_ASYNC), steps, args.warmup, stream, world)
     ms_d = _time_loop(step(_lib.NM_MULTI_DIVERGENT), max(3, steps // 4), 2, stream, world)
     if rank == 0:
         texels = sum(int(h.info.latent_texels) for h in handles)
@@ -414,6 +415,8 @@ def run_c4(args):
             "config": {"workload": "C4 eval, 5 materials mixed per query (i.i.d. ids), 1920x1080",
                        "pyramids": [f"{w}x{h}" for w, h in C4_RESOLUTIONS],
                        "latent_gb": texels * 16 / 1e9, "mode": "binned (headline)"},
+            "binned_async": {"value": n * world / (ms_a / 1e3), "ms_per_step": ms_a,
+                             "note": "no host round trip (segment sizes stay on the device)"},
             "divergent": {"value": n * world / (ms_d / 1e3), "ms_per_step": ms_d},
             "binned_over_divergent": ms_d / ms_b,
         }))

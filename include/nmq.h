@@ -45,7 +45,11 @@ enum nm_status {
 
 enum nm_act { NM_ACT_LINEAR = 0, NM_ACT_LEAKY = 1 }; /* mlp.py:22 _ACT_CODES */
 
-enum nm_multi_mode { NM_MULTI_DIVERGENT = 0, NM_MULTI_BINNED = 1 };
+/* DIVERGENT: mixed tiles decoded directly; BINNED: sort into per-material
+ * segments, coherent kernel per segment, ids validated (one host round trip);
+ * BINNED_ASYNC: the same without the host round trip (segment sizes stay on
+ * the device; rows with out-of-range ids are left untouched). */
+enum nm_multi_mode { NM_MULTI_DIVERGENT = 0, NM_MULTI_BINNED = 1, NM_MULTI_BINNED_ASYNC = 2 };
 
 /* One quantized network exactly as the reference holds it
  * (QuantizedMlp, mlp.py:165-233): per layer, per output neuron,

@@ -18,6 +18,7 @@ NM_ERR_UNSUPPORTED = -3
 
 NM_MULTI_DIVERGENT = 0
 NM_MULTI_BINNED = 1
+NM_MULTI_BINNED_ASYNC = 2
 
 c_float_p = ctypes.c_void_p  # device pointers are passed as raw addresses
 c_i64 = ctypes.c_int64

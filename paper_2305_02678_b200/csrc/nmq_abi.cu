@@ -714,10 +714,11 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
   DeviceGuard guard(dev);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  if (mode == NM_MULTI_BINNED) {
+  if (mode == NM_MULTI_BINNED || mode == NM_MULTI_BINNED_ASYNC) {
     std::vector<int32_t> counts(n_mats);
     int32_t bad = 0;
-    e = eval_binned(mps.data(), n_mats, a, mat_id, workspace, counts.data(), &bad, s);
+    e = eval_binned(mps.data(), n_mats, a, mat_id, workspace, counts.data(), &bad,
+                    mode == NM_MULTI_BINNED, s);
     if (e == cudaErrorInvalidValue && bad) return fail(NM_ERR_INVALID, "mat_id out of range");
     return finish(nullptr, e, "nm_eval_multi(binned)");
   }

@@ -248,10 +248,10 @@ __device__ __forceinline__ void out_layer_simt(uint32_t dl, const MatParams& mp,
 // by one thread), direct per-row copies for the partial last tile.
 // Returns true if TMA was used (consumers then wait on `bar`).
 template <int MODE>
-__device__ __forceinline__ bool stage_inputs(const QueryArgs& a, int tile, InBuf<MODE>& ib,
-                                             uint64_t* bar, int r, bool issuer) {
-  const int64_t q0 = (int64_t)tile * kTile;
-  if (q0 + kTile <= a.n) {
+__device__ __forceinline__ bool stage_inputs(const QueryArgs& a, int64_t base, int64_t n, int tile,
+                                             InBuf<MODE>& ib, uint64_t* bar, int r, bool issuer) {
+  const int64_t q0 = base + (int64_t)tile * kTile;
+  if ((int64_t)tile * kTile + kTile <= n) {
     if (issuer) {
       uint32_t bytes = kTile * (8 + 4 + 12);
       if (a.lod_stride) bytes += kTile * 4;
@@ -270,7 +270,7 @@ __device__ __forceinline__ bool stage_inputs(const QueryArgs& a, int tile, InBuf
     return true;
   }
   const int64_t q = q0 + r;
-  const bool v = q < a.n;
+  const bool v = (int64_t)tile * kTile + r < n;
   ib.uv[2 * r] = v ? a.uv[2 * q] : 0.f;
   ib.uv[2 * r + 1] = v ? a.uv[2 * q + 1] : 0.f;
   if (a.lod_stride) ib.lod[r] = v ? a.lod[q] : 0.f;
@@ -440,8 +440,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
 
   const float lod0 = a.lod_stride ? 0.f : __ldg(a.lod);
-  const int ntiles = (int)((a.n + kTile - 1) / kTile);  // host guarantees < 2^31
-  const int last_full = (int)(a.n / kTile);                // tiles [0, last_full) are full
+  const int64_t seg_base = a.seg ? (int64_t)__ldg(a.seg) : 0;  // binned segment rows
+  const int64_t n_rows = a.seg ? (int64_t)__ldg(a.seg + 1) : a.n;
+  const int ntiles = (int)((n_rows + kTile - 1) / kTile);  // host guarantees < 2^31
+  const int last_full = (int)(n_rows / kTile);                // tiles [0, last_full) are full
   const int stride = gridDim.x * G;                        // between a group's tiles
   const int sstride = stride * NS;                         // between a slot's tiles
   const bool want_level = a.level != nullptr;
@@ -487,9 +489,9 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     constexpr int s = decltype(sc)::value;
     SlotSt& S = sl[s];
     if (S.t < ntiles) {
-      stage_inputs<MODE>(a, S.t, buf(s, 0), &in_bar[gi][s][0], r, r == 64);
+      stage_inputs<MODE>(a, seg_base, n_rows, S.t, buf(s, 0), &in_bar[gi][s][0], r, r == 64);
       if (S.t + sstride < ntiles)
-        stage_inputs<MODE>(a, S.t + sstride, buf(s, 1), &in_bar[gi][s][1], r, r == 64);
+        stage_inputs<MODE>(a, seg_base, n_rows, S.t + sstride, buf(s, 1), &in_bar[gi][s][1], r, r == 64);
       wait_in(S, s, 0, S.t);
       TexPrefetch p0;
       prefetch_texels<MODE>(mp, a, buf(s, 0), r, lod0, p0);
@@ -511,7 +513,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
         if (s > 0 && S.t >= ntiles) return;  // uniform per group
         const int b = S.it & 1;
         const int64_t q_in = (int64_t)S.t * kTile + r;  // input row
-        const bool valid = q_in < a.n;
+        const bool valid = q_in < n_rows;
         const int t2 = S.t + 2 * sstride;
         constexpr int PW = (k + s) % 4;  // warp polling the previous MMA's completion
         auto wait_mma = [&]() { mma_wait<PW>(g, S.bar, S.ph); };
@@ -526,7 +528,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           if constexpr (Need<MODE>::u3) S.u3 = v3(ib.u3[3 * r], ib.u3[3 * r + 1], ib.u3[3 * r + 2]);
           S.up = (S.wi.z > 0.f) && (wo.z > 0.f);
           if (want_level) {
-            if (valid) a.level[a.out_idx ? (int64_t)__ldg(a.out_idx + q_in) : q_in] = S.level;
+            if (valid) a.level[a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
           }
           // the slot's next tile: texel loads now, blended at the last stage
           if (S.t + sstride < ntiles) {
@@ -538,9 +540,9 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           }
           auto refill = [&]() {  // after the barrier: every row of buffer b was read
             if (t2 < last_full) {
-              if (r == 32 * ((LW + 2) % 4)) stage_inputs<MODE>(a, t2, buf(s, b), &in_bar[gi][s][b], r, true);
+              if (r == 32 * ((LW + 2) % 4)) stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
             } else if (t2 < ntiles) {
-              stage_inputs<MODE>(a, t2, buf(s, b), &in_bar[gi][s][b], r, false);  // own row
+              stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, false);  // own row
             }
           };
           wait_mma();
@@ -581,7 +583,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           float y[6];
           out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
           if (valid) {
-            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + q_in) : q_in;
+            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                               : v3(0.f, 0.f, 0.f);
             stg3(a.rgb, q, f);
@@ -632,7 +634,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           for (int j = 0; j < 9; ++j) raw[j] = __uint_as_float(yr[j]);
           const Proxy p = proxy_from_raw(raw, mp.isotropic != 0, fc.inv_samp);
           if (valid) {
-            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + q_in) : q_in;
+            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             if (a.params9) store_proxy(a.params9, q, p);
             const V3 w = proxy_sample(p, S.wi, S.u3.x, S.u3.y, S.u3.z);
             stg3(a.ws, q, w);

@@ -103,6 +103,9 @@ struct QueryArgs {
   const int32_t* idx;   // optional indirection (generic kernel): query = idx[i]
   const int32_t* out_idx;  // optional output rows: results of row i go to row out_idx[i]
                            // (binned multi-material writes straight to query order)
+  const int32_t* seg;      // optional device {base, count}: the launch covers input rows
+                           // [base, base + count) (n is then only a capacity bound);
+                           // lets binned segments launch without a host round trip
   float* rgb;
   float* albedo;
   float* ws;
@@ -132,7 +135,7 @@ cudaError_t launch_pdf(int64_t n, const float* p9, const float* wi, const float*
 size_t multi_workspace_bytes(int64_t n, int32_t n_mats);
 cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const QueryArgs& a,
                         const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
-                        cudaStream_t s);
+                        bool checked, cudaStream_t s);
 cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatParams* mps_dev,
                                   int32_t n_mats, const int32_t* mat_id, const QueryArgs& a,
                                   cudaStream_t s);

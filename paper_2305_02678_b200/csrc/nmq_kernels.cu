@@ -296,13 +296,15 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
   g.smem_w = tc::smem_u32(smem);
   g.leader = (r == 0);
 
-  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  const int64_t seg_base = a.seg ? (int64_t)__ldg(a.seg) : 0;  // binned segment rows
+  const int64_t n_rows = a.seg ? (int64_t)__ldg(a.seg + 1) : a.n;
+  const int64_t ntiles = (n_rows + kTile - 1) / kTile;
   for (int64_t tile = (int64_t)blockIdx.x * G + gi; tile < ntiles;
        tile += (int64_t)gridDim.x * G) {
     const int64_t i = tile * kTile + r;
-    const bool valid = i < a.n;
-    const int64_t q = valid ? (a.idx ? (int64_t)__ldg(a.idx + i) : i) : 0;
-    const int64_t oq = valid ? (a.out_idx ? (int64_t)__ldg(a.out_idx + i) : q) : 0;  // output row
+    const bool valid = i < n_rows;
+    const int64_t q = valid ? (a.idx ? (int64_t)__ldg(a.idx + i) : seg_base + i) : 0;
+    const int64_t oq = valid ? (a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + i) : q) : 0;  // output row
 
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
     float z[8];

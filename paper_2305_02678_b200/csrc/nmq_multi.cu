@@ -56,12 +56,15 @@ __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mat
 // Segment offsets padded to multiples of 4 rows, so every segment's staged
 // inputs are 16-byte aligned (TMA / the specialized kernels).
 __global__ void bin_scan_kernel(int32_t n_mats, const int32_t* __restrict__ counts,
-                                int32_t* __restrict__ offsets, int32_t* __restrict__ cursor) {
+                                int32_t* __restrict__ offsets, int32_t* __restrict__ cursor,
+                                int32_t* __restrict__ seg) {
   if (threadIdx.x == 0) {
     int32_t acc = 0;
     for (int m = 0; m < n_mats; ++m) {
       offsets[m] = acc;
       cursor[m] = acc;
+      seg[2 * m] = acc;  // {base, count} of segment m, read by the segment launch
+      seg[2 * m + 1] = counts[m];
       acc += (counts[m] + 3) & ~3;
     }
     offsets[n_mats] = acc;
@@ -113,11 +116,11 @@ size_t multi_workspace_bytes(int64_t n, int32_t n_mats) {
   // counts, offsets(+1), cursor, bad flag | order | uv lod urr wi wo
   // (segments padded to 4 rows: n + 4 n_mats rows)
   const size_t rows = (size_t)n + 4 * (size_t)n_mats;
-  return 256 + (size_t)(3 * n_mats + 2) * 4 + rows * (4 + 40) + 64 * 8;
+  return 512 + (size_t)(5 * n_mats + 2) * 4 + rows * (4 + 40) + 64 * 8;
 }
 
 struct MultiWs {
-  int32_t *counts, *offsets, *cursor, *bad, *order;
+  int32_t *counts, *offsets, *cursor, *bad, *seg, *order;
   float *uv, *lod, *urr, *wi, *wo;
 };
 
@@ -130,6 +133,7 @@ static MultiWs carve(void* ws, int64_t n_rows, int32_t n_mats) {
   w.offsets = (int32_t*)p; p += (n_mats + 1) * 4;
   w.cursor = (int32_t*)p; p += n_mats * 4;
   w.bad = (int32_t*)p; p += 4;
+  p = align(p); w.seg = (int32_t*)p; p += 2 * n_mats * 4;
   p = align(p); w.order = (int32_t*)p; p += n * 4;
   p = align(p); w.uv = (float*)p; p += n * 8;
   p = align(p); w.lod = (float*)p; p += n * 4;
@@ -139,22 +143,42 @@ static MultiWs carve(void* ws, int64_t n_rows, int32_t n_mats) {
   return w;
 }
 
-// BINNED eval.  `host_counts` receives the per-material counts (the host
-// needs them to size the per-segment launches: one D2H sync per call).
+// BINNED eval.  checked: `host_counts` / `bad` come back to the host (one
+// D2H sync per call) so out-of-range ids are reported and empty segments are
+// skipped.  !checked: no host round trip — every segment launch reads its
+// {base, count} from the device (QueryArgs::seg); ids out of range are
+// dropped (their rows are left untouched).
 cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const QueryArgs& a,
                         const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
-                        cudaStream_t s) {
+                        bool checked, cudaStream_t s) {
   if (n_mats > kMaxMats) return cudaErrorInvalidValue;
   MultiWs w = carve(ws, a.n, n_mats);
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.counts, 0, (3 * n_mats + 2) * 4, s)) != cudaSuccess) return e;
   bin_count_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
-  bin_scan_kernel<<<1, 32, 0, s>>>(n_mats, w.counts, w.offsets, w.cursor);
+  bin_scan_kernel<<<1, 32, 0, s>>>(n_mats, w.counts, w.offsets, w.cursor, w.seg);
   bin_scatter_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, mat_id, w.cursor, w.order, a.uv, a.lod,
                                                   a.lod_stride, a.u_rr, a.wi, a.wo, w.uv, w.lod,
                                                   w.urr, w.wi, w.wo);
   g_launches += 3;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (!checked) {
+    for (int m = 0; m < n_mats; ++m) {
+      QueryArgs sa{};
+      sa.n = a.n;  // capacity bound; the segment's rows come from w.seg
+      sa.seg = w.seg + 2 * m;
+      sa.uv = w.uv;
+      sa.lod = w.lod;
+      sa.lod_stride = 1;
+      sa.u_rr = w.urr;
+      sa.wi = w.wi;
+      sa.wo = w.wo;
+      sa.rgb = a.rgb;
+      sa.out_idx = w.order;
+      if ((e = launch_fused(*mps[m], kModeEval, sa, s)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   if ((e = cudaMemcpyAsync(host_counts, w.counts, n_mats * 4, cudaMemcpyDeviceToHost, s)) !=
       cudaSuccess)
     return e;

@@ -585,7 +585,8 @@ bool aligned16w(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 }  // namespace
 
 cudaError_t launch_warp(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s) {
-  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx || a.out_idx || !mp.wk_blob) return cudaErrorNotSupported;
+  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx || a.out_idx || a.seg || !mp.wk_blob)
+    return cudaErrorNotSupported;
   if (mode != kModeEval && mode != kModeSamplePdf && mode != kModeQuery) return cudaErrorNotSupported;
   if (!aligned16w(a.uv) || !aligned16w(a.u_rr) || !aligned16w(a.wi) ||
       (a.lod_stride && !aligned16w(a.lod)) || (a.wo && !aligned16w(a.wo)) ||

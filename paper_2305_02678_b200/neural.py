@@ -354,15 +354,18 @@ def query(mat, uv, level, u_rr, wi, wo, u, fp16=True, return_level=False):
     return res
 
 
-MULTI_MODES = {"divergent": _lib.NM_MULTI_DIVERGENT, "binned": _lib.NM_MULTI_BINNED}
+MULTI_MODES = {"divergent": _lib.NM_MULTI_DIVERGENT, "binned": _lib.NM_MULTI_BINNED,
+               "binned_async": _lib.NM_MULTI_BINNED_ASYNC}
 
 
 def eval_material_multi(mats, mat_id, uv, level, wi, wo, u_rr, mode="binned", fp16=True, out=None):
     """Per-query material selection (the renderer's per-vertex material groups,
     render.py:352-356): f[i] = eval_material(mats[mat_id[i]], ...)[0][i].
     mode "binned" sorts queries into per-material segments with warp-level
-    counting and runs the coherent fused kernel per segment; "divergent"
-    decodes mixed tiles directly.  Returns f (B, 3)."""
+    counting and runs the coherent fused kernel per segment (ids validated:
+    one host round trip); "binned_async" skips the round trip (segment sizes
+    stay on the device; out-of-range ids leave their rows untouched);
+    "divergent" decodes mixed tiles directly.  Returns f (B, 3)."""
     _require_fp16(fp16)
     if mode not in MULTI_MODES:
         raise ValueError(f"mode must be one of {sorted(MULTI_MODES)}")

@@ -52,7 +52,7 @@ def _oracle_multi(omats, ids, uv, lod, urr, wi, wo):
     return f
 
 
-@pytest.mark.parametrize("mode", ["binned", "divergent"])
+@pytest.mark.parametrize("mode", ["binned", "binned_async", "divergent"])
 @pytest.mark.parametrize("pattern", ["random", "coherent", "blocks"])
 def test_multi_material_matches_oracle(mode, pattern):
     from paper_2305_02678_b200 import neural
