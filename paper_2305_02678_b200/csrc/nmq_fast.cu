@@ -707,6 +707,7 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   int64_t grid = g_sms;
+  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid > (ntiles + G - 1) / G) grid = (ntiles + G - 1) / G;
   if (grid < 1) grid = 1;
   const FastConsts fc = make_consts(BNH, SNH);

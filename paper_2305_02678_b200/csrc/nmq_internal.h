@@ -106,6 +106,8 @@ struct QueryArgs {
   const int32_t* seg;      // optional device {base, count}: the launch covers input rows
                            // [base, base + count) (n is then only a capacity bound);
                            // lets binned segments launch without a host round trip
+  int32_t max_ctas;        // optional cap on the persistent grid (0 = one CTA per SM):
+                           // concurrent segment launches on disjoint SM subsets
   float* rgb;
   float* albedo;
   float* ws;

@@ -592,6 +592,7 @@ cudaError_t launch_mode(const MatParams& mp, const QueryArgs& a, cudaStream_t s,
   if (e != cudaSuccess) return e;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   int64_t grid = (int64_t)num_sms() * ctas_per_sm;
+  if (a.max_ctas > 0 && grid > (int64_t)a.max_ctas * ctas_per_sm) grid = (int64_t)a.max_ctas * ctas_per_sm;
   const int64_t need_ctas = (ntiles + G - 1) / G;
   if (grid > need_ctas) grid = need_ctas;
   if (grid < 1) grid = 1;

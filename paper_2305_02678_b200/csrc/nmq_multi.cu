@@ -104,6 +104,54 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
   }
 }
 
+int num_sms_multi() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+// Side streams for concurrent segment launches (per device, created once).
+constexpr int kMaxSide = 32;
+struct SideStreams {
+  cudaStream_t st[kMaxSide] = {};
+  cudaEvent_t ev[kMaxSide + 1] = {};
+  bool ready = false;
+};
+SideStreams g_side[16];
+
+SideStreams& sides() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  SideStreams& S = g_side[dev & 15];
+  if (!S.ready) {
+    for (int i = 0; i < kMaxSide; ++i) {
+      cudaStreamCreateWithFlags(&S.st[i], cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&S.ev[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&S.ev[kMaxSide], cudaEventDisableTiming);
+    S.ready = true;
+  }
+  return S;
+}
+cudaStream_t side_stream(int m) { return sides().st[m % kMaxSide]; }
+void fork_streams(cudaStream_t s, int k) {
+  SideStreams& S = sides();
+  cudaEventRecord(S.ev[kMaxSide], s);
+  for (int i = 0; i < k && i < kMaxSide; ++i) cudaStreamWaitEvent(S.st[i], S.ev[kMaxSide], 0);
+}
+cudaError_t join_streams(cudaStream_t s, int k) {
+  SideStreams& S = sides();
+  for (int i = 0; i < k && i < kMaxSide; ++i) {
+    cudaEventRecord(S.ev[i], S.st[i]);
+    cudaStreamWaitEvent(s, S.ev[i], 0);
+  }
+  return cudaGetLastError();
+}
+
 int grid256(int64_t n) {
   int64_t b = (n + 255) / 256;
   if (b > 148 * 32) b = 148 * 32;
@@ -163,6 +211,12 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
   g_launches += 3;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (!checked) {
+    // one launch per material on its own stream, each on ~1/n_mats of the
+    // SMs, so the segments run side by side (no serialized pipeline
+    // fill/drain); forked from and joined back into `s` with events
+    const int nsm = num_sms_multi();
+    const int per = nsm / n_mats > 0 ? nsm / n_mats : 1;
+    fork_streams(s, n_mats);
     for (int m = 0; m < n_mats; ++m) {
       QueryArgs sa{};
       sa.n = a.n;  // capacity bound; the segment's rows come from w.seg
@@ -175,9 +229,10 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
       sa.wo = w.wo;
       sa.rgb = a.rgb;
       sa.out_idx = w.order;
-      if ((e = launch_fused(*mps[m], kModeEval, sa, s)) != cudaSuccess) return e;
+      sa.max_ctas = per;
+      if ((e = launch_fused(*mps[m], kModeEval, sa, side_stream(m))) != cudaSuccess) return e;
     }
-    return cudaSuccess;
+    return join_streams(s, n_mats);
   }
   if ((e = cudaMemcpyAsync(host_counts, w.counts, n_mats * 4, cudaMemcpyDeviceToHost, s)) !=
       cudaSuccess)
