@@ -168,6 +168,15 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   void* stream);
 
 /* --- misc -------------------------------------------------------------- */
+/* nm_eval with HOST buffers (pinned for full PCIe overlap; pageable works):
+ * the batch streams through the GPU in `chunk`-query pieces (0 = 512k) on two
+ * internal streams, H2D / fused kernel / D2H overlapped; blocking (rgb_out is
+ * complete on return); ordered after prior work on `stream`.  The reference
+ * call it replaces is eval_material on numpy arrays (neural.py:303). */
+int nm_eval_host(const nm_material* mat, int64_t n, const float* uv, const float* lod,
+                 int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+                 float* rgb_out, int64_t chunk, void* stream);
+
 /* Level of detail from ray cones (replaces render.footprint_to_level,
  * render.py:334-337, and the footprint in render._surface_frames_and_level,
  * render.py:436-443).  float64 like the reference.

@@ -78,21 +78,11 @@ def out(t, numpy_mode, np_dtype=np.float64):
 
 
 # ---------------------------------------------------------------------------
-# Streaming host <-> device pipeline for large host (numpy) batches: chunks of
-# the batch alternate between two CUDA streams, so the H2D copy of chunk c+1,
-# the kernel of chunk c and the D2H copy of chunk c-1 overlap (both copy
-# engines + the SMs busy).  Host buffers should be pinned for real overlap;
-# pageable memory still works (the driver stages it synchronously).
+# Large host (numpy) batches stream through the GPU inside the native library
+# (nm_eval_host: chunks on two internal streams, H2D / kernel / D2H
+# overlapped).  Host buffers should be pinned for full overlap.
 
 STREAM_CHUNK = int(os.environ.get("NMQ_STREAM_CHUNK", 1 << 19))  # queries per chunk
-_STREAMS = {}
-
-
-def _streams(dev):
-    key = dev.index
-    if key not in _STREAMS:
-        _STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    return _STREAMS[key]
 
 
 def host_rows(x, cols, name):
@@ -102,31 +92,3 @@ def host_rows(x, cols, name):
     if a.ndim != 2 or a.shape[1] != cols:
         return None
     return np.ascontiguousarray(a, dtype=np.float32)
-
-
-def streamed(n, dev, host_in, host_out, launch, chunk=STREAM_CHUNK):
-    """Run `launch(dev_in_slices, dev_out_slices, count, stream_ptr)` over
-    chunks of the batch with double-buffered streams.  host_in / host_out are
-    lists of host numpy arrays with n rows; outputs are complete on return."""
-    d_in = [torch.empty(a.shape, device=dev, dtype=torch.float32) for a in host_in]
-    d_out = [torch.empty(o.shape, device=dev, dtype=torch.from_numpy(o[:0]).dtype) for o in host_out]
-    h_in = [torch.from_numpy(a) for a in host_in]
-    h_out = [torch.from_numpy(o) for o in host_out]
-    cur = torch.cuda.current_stream(dev)
-    ss = _streams(dev)
-    start = torch.cuda.Event()
-    start.record(cur)
-    for s in ss:
-        s.wait_event(start)
-    for ci, c0 in enumerate(range(0, n, chunk)):
-        c1 = min(n, c0 + chunk)
-        s = ss[ci & 1]
-        with torch.cuda.stream(s):
-            for d, h in zip(d_in, h_in):
-                d[c0:c1].copy_(h[c0:c1], non_blocking=True)
-            launch([d[c0:c1] for d in d_in], [o[c0:c1] for o in d_out], c1 - c0, s.cuda_stream)
-            for o, h in zip(d_out, h_out):
-                h[c0:c1].copy_(o[c0:c1], non_blocking=True)
-    for s in ss:
-        cur.wait_stream(s)
-    cur.synchronize()

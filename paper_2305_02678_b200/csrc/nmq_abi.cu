@@ -3,6 +3,7 @@
 // upload) and the query entry points.
 #include <cmath>
 #include <cstdio>
+#include <mutex>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -573,6 +574,77 @@ int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
   DeviceGuard guard(m->device);
   if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
   return finish(m, launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream), "nm_eval");
+}
+
+// Host-buffer eval: the batch streams through the GPU in chunks on two
+// internal streams — H2D of chunk c+1, the fused kernel of chunk c and the
+// D2H of chunk c-1 overlap (copy engines + SMs).  Blocking: returns when
+// rgb_out (host) is complete.  Device staging is per device, grow-only.
+namespace {
+struct HostStage {
+  std::mutex mu;
+  char* buf = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st[2] = {};
+  cudaEvent_t ev_start = nullptr;
+};
+HostStage g_stage[16];
+}  // namespace
+
+int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* lod,
+                 int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+                 float* rgb_out, int64_t chunk, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !wo || !rgb_out) return fail(NM_ERR_INVALID, "null input");
+  if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  if (chunk <= 0) chunk = (int64_t)1 << 19;
+  chunk = (chunk + 127) / 128 * 128;
+  DeviceGuard guard(m->device);
+  HostStage& H = g_stage[m->device & 15];
+  std::lock_guard<std::mutex> lock(H.mu);
+  cudaError_t e;
+  const size_t per_row = 8 + 4 + 4 + 12 + 12 + 12;  // uv lod u_rr wi wo | rgb
+  const size_t need = 2 * (size_t)chunk * per_row + 1024;
+  if (H.bytes < need) {
+    if (H.buf) cudaFree(H.buf);
+    H.buf = nullptr;
+    H.bytes = 0;
+    if ((e = cudaMalloc(&H.buf, need)) != cudaSuccess) return cuda_fail(e, "host-eval staging");
+    H.bytes = need;
+  }
+  if (!H.st[0]) {
+    for (auto& st : H.st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&H.ev_start, cudaEventDisableTiming);
+  }
+  cudaEventRecord(H.ev_start, (cudaStream_t)stream);  // after prior work on the caller's stream
+  for (auto& st : H.st) cudaStreamWaitEvent(st, H.ev_start, 0);
+  for (int64_t c0 = 0, ci = 0; c0 < n; c0 += chunk, ++ci) {
+    const int64_t c = n - c0 < chunk ? n - c0 : chunk;
+    cudaStream_t st = H.st[ci & 1];
+    char* base = H.buf + (size_t)(ci & 1) * chunk * per_row;
+    float* d_uv = (float*)base;
+    float* d_lod = d_uv + 2 * chunk;
+    float* d_urr = d_lod + chunk;
+    float* d_wi = d_urr + chunk;
+    float* d_wo = d_wi + 3 * chunk;
+    float* d_rgb = d_wo + 3 * chunk;
+    cudaMemcpyAsync(d_uv, uv + 2 * c0, c * 8, cudaMemcpyHostToDevice, st);
+    if (lod_stride) cudaMemcpyAsync(d_lod, lod + c0, c * 4, cudaMemcpyHostToDevice, st);
+    else cudaMemcpyAsync(d_lod, lod, 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_urr, u_rr + c0, c * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_wi, wi + 3 * c0, c * 12, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_wo, wo + 3 * c0, c * 12, cudaMemcpyHostToDevice, st);
+    QueryArgs a{};
+    a.n = c; a.uv = d_uv; a.lod = d_lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = d_urr;
+    a.wi = d_wi; a.wo = d_wo; a.rgb = d_rgb;
+    if ((e = launch_fused(m->mp, kModeEval, a, st)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
+    cudaMemcpyAsync(rgb_out + 3 * c0, d_rgb, c * 12, cudaMemcpyDeviceToHost, st);
+  }
+  for (auto& st : H.st)
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
+  return NM_OK;
 }
 
 int nm_eval_z(const nm_material* m, int64_t n, const float* z, const float* wi, const float* wo,

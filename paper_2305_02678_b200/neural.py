@@ -242,31 +242,28 @@ class _QueryInputs:
 
 
 def _stream_eval(mat, uv, level, wi, wo, u_rr, out):
-    """eval_material for a large host batch: chunked H2D / fused kernel / D2H
-    overlapped on two streams (see _io.streamed).  None if not applicable."""
+    """eval_material for a large host batch through nm_eval_host: chunked
+    H2D / fused kernel / D2H overlapped on two internal streams, all in native
+    code.  None if not applicable (albedo head, non-contiguous shapes...)."""
     if mat.cfg.albedo_head:
         return None
     n = np.shape(uv)[0] if np.ndim(uv) == 2 else 0
     if n < 2 * _io.STREAM_CHUNK:
         return None
     h_uv, h_wi, h_wo = _io.host_rows(uv, 2, "uv"), _io.host_rows(wi, 3, "wi"), _io.host_rows(wo, 3, "wo")
-    h_lod = np.ascontiguousarray(np.asarray(level, dtype=np.float32)).reshape(-1, 1)
-    h_urr = np.ascontiguousarray(np.asarray(u_rr, dtype=np.float32)).reshape(-1, 1)
-    if h_uv is None or h_wi is None or h_wo is None or h_lod.shape[0] != n or h_urr.shape[0] != n \
-            or h_wi.shape[0] != n or h_wo.shape[0] != n:
+    h_lod = np.ascontiguousarray(np.asarray(level, dtype=np.float32)).reshape(-1)
+    h_urr = np.ascontiguousarray(np.asarray(u_rr, dtype=np.float32)).reshape(-1)
+    if h_uv is None or h_wi is None or h_wo is None or h_urr.shape[0] != n \
+            or h_lod.shape[0] not in (1, n) or h_wi.shape[0] != n or h_wo.shape[0] != n:
         return None
     if out is not None and (out.dtype != np.float32 or out.shape != (n, 3) or not out.flags.c_contiguous):
         return None
     f_host = out if out is not None else np.empty((n, 3), np.float32)
     h = mat.device_material(None)
     lib = _lib.load()
-
-    def launch(d_in, d_out, count, stream):
-        d_uv, d_lod, d_urr, d_wi, d_wo = d_in
-        _launch(lib.nm_eval, h.ptr, count, d_uv.data_ptr(), d_lod.data_ptr(), 1, d_urr.data_ptr(),
-                d_wi.data_ptr(), d_wo.data_ptr(), d_out[0].data_ptr(), None, None, stream)
-
-    _io.streamed(n, h.device, [h_uv, h_lod, h_urr, h_wi, h_wo], [f_host], launch)
+    _launch(lib.nm_eval_host, h.ptr, n, h_uv.ctypes.data, h_lod.ctypes.data, int(h_lod.shape[0] == n),
+            h_urr.ctypes.data, h_wi.ctypes.data, h_wo.ctypes.data, f_host.ctypes.data,
+            _io.STREAM_CHUNK, _io.stream_ptr(h.device))
     return f_host if out is not None else f_host.astype(np.float64)
 
 
