@@ -475,9 +475,69 @@ def run_c5(args):
         }))
 
 
+def run_train(args):
+    """SURVEY §8 f4 (training-side kernels), not the headline: one baking
+    iteration's worth of network forward_cached + backward (BRDF 20-32-32-3
+    and sampler 11-32-32-32-9 on 65,536 rows each, training.py batch) and the
+    latent-gradient scatter of 65,536 queries into the 4096^2 pyramid; rows/s
+    with the numpy oracle (the reference's algorithm) timed beside it."""
+    rank, world, local = dist_init(args.gpus)
+    device = torch.device("cuda", local)
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import mlp, synth, train  # noqa: F401
+    rng = np.random.default_rng(3)
+    B = 65536
+    nets = {"brdf": mlp.Mlp.create((20, 32, 32, 3), rng), "sampler": mlp.Mlp.create((11, 32, 32, 32, 9), rng)}
+    xs = {k: torch.randn((B, n.layers[0].w.shape[1]), device=device) for k, n in nets.items()}
+    gs = {k: torch.randn((B, n.layers[-1].w.shape[0]), device=device) for k, n in nets.items()}
+    mat = synth.material("2x32", RES, RES, seed=0, device=device)
+    q = synth.queries(B, mat.latent.n_levels, seed=1, device=device)
+    lv = torch.randint(0, mat.latent.n_levels, (B,), device=device, dtype=torch.int32)
+    zg = torch.randn((B, 8), device=device)
+    texels = mat.latent.texels.shape[0]
+    grad = torch.zeros((texels, 8), device=device)
+    h = mat.device_material(device)
+    from paper_2305_02678_b200 import _lib
+    lib = _lib.load()
+    stream = torch.cuda.current_stream(device)
+
+    def step(i):
+        for k, n in nets.items():
+            _, cache = train.forward_cached(n, xs[k])
+            train.backward(n, cache, gs[k])
+        _lib.check(lib.nm_texel_grads(h.ptr, B, q["uv"].data_ptr(), lv.data_ptr(), zg.data_ptr(),
+                                      grad.data_ptr(), stream.cuda_stream))
+
+    steps = max(5, args.steps // 100)
+    ms = _time_loop(step, steps, args.warmup, stream, world)
+    # CPU: the oracle's restatement of the reference on the same shapes (1 core)
+    onets = {k: O.Net([(l.w, l.b, l.act) for l in n.layers]) for k, n in nets.items()}
+    xh = {k: v.cpu().numpy() for k, v in xs.items()}
+    gh = {k: v.cpu().numpy() for k, v in gs.items()}
+    t0 = time.perf_counter()
+    for k, n in onets.items():
+        _, c = O.forward_cached(n, xh[k])
+        O.backward(n, c, gh[k])
+    t_mlp = time.perf_counter() - t0
+    if rank == 0:
+        print(json.dumps({
+            "metric": "training-side rows/s (forward_cached + backward of both decoders + texel-grad scatter)",
+            "value": B / (ms / 1e3), "unit": "rows/s", "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 forward, fp64 backward chain / reductions",
+            "data": "synthetic: random-init networks, N(0,1) inputs and gradients",
+            "config": {"workload": "train (SURVEY §8 f4)", "rows": B, "latent": f"{RES}x{RES}"},
+            "cpu_baseline": {"value": B / t_mlp, "unit": "rows/s", "cores": 1, "kind": "port",
+                             "sample": "forward_cached + backward of both decoders (oracle, numpy, 1 core); "
+                                       "texel scatter not included"},
+        }))
+
+
 def run_ours(args):
     if args.workload == "c4":
         return run_c4(args)
+    if args.workload == "train":
+        return run_train(args)
     if args.workload == "c5":
         return run_c5(args)
     rank, world, local = dist_init(args.gpus)
@@ -653,7 +713,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3", "full", "c4", "c5"], default="c2")
+    ap.add_argument("--workload", choices=["c2", "c3", "full", "c4", "c5", "train"], default="c2")
     ap.add_argument("--sets", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-sample", type=int, default=C2_N)

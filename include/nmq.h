@@ -177,6 +177,29 @@ int nm_eval_host(const nm_material* mat, int64_t n, const float* uv, const float
                  int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
                  float* rgb_out, int64_t chunk, void* stream);
 
+/* Training-side kernels (device pointers, async on `stream`).
+ *  nm_texel_grads: exact adjoint of the fetch (latent.py:109-119
+ *    accumulate_texel_grads): z_grad (n, 8) scattered onto the four bilinear
+ *    taps of each query at its level (int32) and ADDED into grad_texels
+ *    (texels, 8) fp32, laid out like the material's latent (levels back to back).
+ *  nm_mlp_*: the fp32 network engine (mlp.py:90-116).  forward_cached runs
+ *    the batch (x (B, in) -> out (B, out)) keeping what backward needs in
+ *    `cache` (nm_mlp_cache_bytes); backward writes d(sum(out * out_grad)) /
+ *    d(params) into dparams (float64, the weights' access order [dW_row, db]
+ *    per neuron per layer, overwritten) and dx (B, in) float64. */
+typedef struct nm_mlp nm_mlp;
+int nm_texel_grads(const nm_material* mat, int64_t n, const float* uv, const int32_t* level,
+                   const float* z_grad, float* grad_texels, void* stream);
+int nm_mlp_create(const nm_net_desc* net, int device, nm_mlp** out);
+int nm_mlp_set_weights(nm_mlp* mlp, const float* weights);
+int nm_mlp_destroy(nm_mlp* mlp);
+int32_t nm_mlp_params(const nm_mlp* mlp);
+size_t nm_mlp_cache_bytes(const nm_mlp* mlp, int64_t batch);
+int nm_mlp_forward_cached(const nm_mlp* mlp, int64_t batch, const float* x, float* out, void* cache,
+                          void* stream);
+int nm_mlp_backward(const nm_mlp* mlp, int64_t batch, void* cache, const float* out_grad,
+                    double* dparams, double* dx, void* stream);
+
 /* Level of detail from ray cones (replaces render.footprint_to_level,
  * render.py:334-337, and the footprint in render._surface_frames_and_level,
  * render.py:436-443).  float64 like the reference.

@@ -172,6 +172,47 @@ def make_lod_case(name="lod", n=4096, seed=31):
     print(name)
 
 
+def make_train_case(name="train", seed=41):
+    """Training-side goldens from the reference itself:
+    Mlp.forward_cached / Mlp.backward on a BRDF-shaped (20-32-32-3) and a
+    sampler-shaped (11-32-32-32-9) network, and LatentPyramid.
+    accumulate_texel_grads on a 32x16 pyramid (incl. wrapped uv)."""
+    geom, latent, neural, proxy = _ref()
+    from neuralmat import mlp
+    rng = np.random.default_rng(seed)
+    d = {}
+    for tag, sizes in (("brdf", (20, 32, 32, 3)), ("samp", (11, 32, 32, 32, 9))):
+        net = mlp.Mlp.create(sizes, rng)
+        for l in net.layers:  # non-zero biases so db is exercised
+            l.b[:] = rng.normal(0, 0.1, l.b.shape).astype(np.float32)
+        x = _f32(rng.normal(0, 1, (4099, sizes[0])))
+        g = _f32(rng.normal(0, 1, (4099, sizes[-1])))
+        out, cache = net.forward_cached(x)
+        grads, dx = net.backward(cache, g)
+        d[f"{tag}_n"] = np.int64(len(net.layers))
+        for i, l in enumerate(net.layers):
+            d[f"{tag}_w{i}"] = l.w
+            d[f"{tag}_b{i}"] = l.b
+            d[f"{tag}_a{i}"] = np.int64(0 if l.act == "linear" else 1)
+            d[f"{tag}_dw{i}"] = grads[i][0]
+            d[f"{tag}_db{i}"] = grads[i][1]
+        d[f"{tag}_x"], d[f"{tag}_g"], d[f"{tag}_out"], d[f"{tag}_dx"] = x, g, out, dx
+    pyr = latent.LatentPyramid.zeros(32, 16)
+    for lvl in pyr.levels:
+        lvl[:] = rng.standard_normal(lvl.shape).astype(np.float32)
+    n = 5000
+    uv = _f32(rng.uniform(-1.5, 2.5, (n, 2)))
+    chosen = rng.integers(0, pyr.n_levels, n)
+    zg = _f32(rng.normal(0, 1, (n, 8)))
+    grads = pyr.zero_grads()
+    pyr.accumulate_texel_grads(grads, uv.astype(np.float64), chosen, zg)
+    d.update(tg_uv=uv, tg_level=chosen.astype(np.int64), tg_zgrad=zg, tg_w=np.int64(32), tg_h=np.int64(16))
+    for i, gl in enumerate(grads):
+        d[f"tg_grad{i}"] = gl
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     make_case("c1_2x32", {}, n=4096, taps=True, fp32_path=True)
@@ -185,6 +226,7 @@ def main():
     make_proxy_case()
     make_archive()
     make_lod_case()
+    make_train_case()
 
 
 if __name__ == "__main__":

@@ -179,6 +179,19 @@ class Pyramid:
             z[m] = np.sum(tex * wts[..., None], axis=-2, dtype=np.float64)
         return z, chosen
 
+    def accumulate_texel_grads(self, grad_levels, uv, chosen, z_grad):
+        """latent.py:109-119: exact adjoint of fetch — scatter z_grad onto the
+        four bilinear taps of each query (float64 contributions added into the
+        caller's float32 gradient images)."""
+        uv = np.atleast_2d(np.asarray(uv, dtype=np.float64))
+        chosen = np.broadcast_to(chosen, uv.shape[:-1])
+        z_grad = np.asarray(z_grad)
+        for l in np.unique(chosen):
+            sel = chosen == l
+            xs, ys, wts = self.taps(int(l), uv[sel])
+            contrib = wts[..., None] * z_grad[sel][..., None, :]
+            np.add.at(grad_levels[int(l)], (ys, xs), contrib)
+
     def fetch_level(self, uv, level):
         """latent.py:100-107: deterministic fetch at one integer level."""
         uv = np.atleast_2d(np.asarray(uv, dtype=np.float64))
@@ -236,6 +249,36 @@ class Net:
         for w, b, a in self.layers:
             x = _act(x @ w.T + b, a)
         return x
+
+
+def _act_grad(pre, act):
+    """mlp.py:33-36 (a float64 array for leaky layers: the reference's
+    backward promotes to float64 from the first leaky layer on)."""
+    return 1.0 if act == ACT_LINEAR else np.where(pre >= 0.0, 1.0, LEAKY_SLOPE)
+
+
+def forward_cached(net, x):
+    """mlp.py:90-101: fp32 forward keeping every layer input and pre-activation."""
+    x = np.asarray(x, dtype=np.float32)
+    inputs, pres = [x], []
+    for w, b, a in net.layers:
+        pre = inputs[-1] @ w.T + b
+        pres.append(pre)
+        inputs.append(_act(pre, a))
+    return inputs[-1], (inputs, pres)
+
+
+def backward(net, cache, out_grad):
+    """mlp.py:103-116: gradients of sum(out * out_grad) -> ([(dW, db)], dx)."""
+    inputs, pres = cache
+    g = np.asarray(out_grad, dtype=np.float32)
+    grads = [None] * len(net.layers)
+    for i in range(len(net.layers) - 1, -1, -1):
+        w, b, a = net.layers[i]
+        g = g * _act_grad(pres[i], a)
+        grads[i] = (g.T @ inputs[i], g.sum(axis=0))
+        g = g @ w
+    return grads, g
 
 
 class HalfNet:

@@ -97,6 +97,17 @@ SIGNATURES = {
                               ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
     "nm_eval_host": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p,
                              c_float_p, c_float_p, c_float_p, c_i64, ctypes.c_void_p]),
+    "nm_texel_grads": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, ctypes.c_void_p, c_float_p, c_float_p,
+                               ctypes.c_void_p]),
+    "nm_mlp_create": (c_i32, [ctypes.c_void_p, c_i32, ctypes.c_void_p]),
+    "nm_mlp_set_weights": (c_i32, [ctypes.c_void_p, ctypes.c_void_p]),
+    "nm_mlp_destroy": (c_i32, [ctypes.c_void_p]),
+    "nm_mlp_params": (c_i32, [ctypes.c_void_p]),
+    "nm_mlp_cache_bytes": (ctypes.c_size_t, [ctypes.c_void_p, c_i64]),
+    "nm_mlp_forward_cached": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, ctypes.c_void_p,
+                                      ctypes.c_void_p]),
+    "nm_mlp_backward": (c_i32, [ctypes.c_void_p, c_i64, ctypes.c_void_p, c_float_p, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_void_p]),
     "nm_footprint_level": (c_i32, [c_i64, ctypes.c_void_p, c_i32, ctypes.c_void_p, ctypes.c_void_p]),
     "nm_cone_level": (c_i32, [c_i64, c_float_p, c_float_p, c_float_p, c_float_p, c_float_p, c_i32,
                               c_i32, c_float_p, ctypes.c_void_p]),

@@ -324,6 +324,14 @@ void fill_warp_layers(MatParams& mp, Packer& wk, const NetView& fv, const NetVie
 
 }  // namespace
 
+struct nm_mlp {
+  int device = 0;
+  int n_layers = 0;
+  int32_t fi[kMaxLayers] = {}, fo[kMaxLayers] = {}, act[kMaxLayers] = {};
+  int32_t w_floats = 0;
+  float* w = nullptr;  // fp32 master weights, access order [w_row, bias] per neuron
+};
+
 struct nm_material {
   int device = 0;
   MatParams mp{};
@@ -725,6 +733,129 @@ int nm_query(const nm_material* m, int64_t n, const float* uv, const float* lod,
   if (!m->mp.has_brdf || !m->mp.has_sampler)
     return fail(NM_ERR_INVALID, "material needs both decoders");
   return finish(m, launch_fused(m->mp, kModeQuery, a, (cudaStream_t)stream), "nm_query");
+}
+
+int nm_texel_grads(const nm_material* m, int64_t n, const float* uv, const int32_t* level,
+                   const float* z_grad, float* grad_texels, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !level || !z_grad || !grad_texels) return fail(NM_ERR_INVALID, "null input");
+  DeviceGuard guard(m->device);
+  return finish(m, launch_texel_grads(m->mp, n, uv, level, z_grad, grad_texels, (cudaStream_t)stream),
+                "nm_texel_grads");
+}
+
+int nm_mlp_create(const nm_net_desc* net, int device, nm_mlp** out) {
+  if (!net || !out) return fail(NM_ERR_INVALID, "null argument");
+  *out = nullptr;
+  NetView v;
+  int rc;
+  nm_net_desc d = *net;
+  if (!d.packed) {  // fp32-only description: view_net wants a packed pointer
+    static const uint16_t dummy = 0;
+    d.packed = &dummy;
+  }
+  if ((rc = view_net(d, "network", v)) != NM_OK) return rc;
+  if (!net->weights) return fail(NM_ERR_INVALID, "fp32 weights required");
+  if (v.n_layers > kMaxLayers) return fail(NM_ERR_UNSUPPORTED, "too many layers");
+  nm_mlp* m = new nm_mlp();
+  m->device = device;
+  m->n_layers = v.n_layers;
+  int32_t floats = 0;
+  for (int l = 0; l < v.n_layers; ++l) {
+    if (v.fi[l] > 64 || v.fo[l] > 64) {
+      delete m;
+      return fail(NM_ERR_UNSUPPORTED, "training kernels handle layers up to 64 wide");
+    }
+    m->fi[l] = v.fi[l];
+    m->fo[l] = v.fo[l];
+    m->act[l] = v.act[l];
+    floats += v.fo[l] * (v.fi[l] + 1);
+  }
+  m->w_floats = floats;
+  DeviceGuard guard(device);
+  cudaError_t e;
+  if ((e = cudaMalloc(&m->w, (size_t)floats * 4)) != cudaSuccess) {
+    delete m;
+    return cuda_fail(e, "cudaMalloc(mlp weights)");
+  }
+  if ((e = cudaMemcpy(m->w, net->weights, (size_t)floats * 4, cudaMemcpyHostToDevice)) != cudaSuccess) {
+    cudaFree(m->w);
+    delete m;
+    return cuda_fail(e, "upload mlp weights");
+  }
+  *out = m;
+  return NM_OK;
+}
+
+int nm_mlp_set_weights(nm_mlp* m, const float* weights) {
+  if (!m || !weights) return fail(NM_ERR_INVALID, "null argument");
+  DeviceGuard guard(m->device);
+  const cudaError_t e = cudaMemcpy(m->w, weights, (size_t)m->w_floats * 4, cudaMemcpyHostToDevice);
+  return e == cudaSuccess ? NM_OK : cuda_fail(e, "nm_mlp_set_weights");
+}
+
+int nm_mlp_destroy(nm_mlp* m) {
+  if (!m) return NM_OK;
+  DeviceGuard guard(m->device);
+  cudaFree(m->w);
+  delete m;
+  return NM_OK;
+}
+
+int32_t nm_mlp_params(const nm_mlp* m) { return m ? m->w_floats : 0; }
+
+static size_t mlp_cache_layout(const nm_mlp* m, int64_t B, size_t* pre_off, size_t* g_off) {
+  size_t widths = 0;
+  for (int l = 0; l < m->n_layers; ++l) widths += (size_t)m->fo[l];
+  const size_t x_bytes = ((size_t)m->fi[0] * B * 4 + 255) & ~(size_t)255;
+  const size_t pre_bytes = (widths * B * 4 + 255) & ~(size_t)255;
+  *pre_off = x_bytes;
+  *g_off = x_bytes + pre_bytes;
+  return x_bytes + pre_bytes + widths * B * 8;
+}
+
+size_t nm_mlp_cache_bytes(const nm_mlp* m, int64_t batch) {
+  if (!m || batch < 0) return 0;
+  size_t a, b;
+  return mlp_cache_layout(m, batch, &a, &b);
+}
+
+int nm_mlp_forward_cached(const nm_mlp* m, int64_t batch, const float* x, float* out, void* cache,
+                          void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null network");
+  NM_CHECK_N(batch);
+  if (batch == 0) return NM_OK;
+  if (!x || !out || !cache) return fail(NM_ERR_INVALID, "null input");
+  size_t pre_off, g_off;
+  mlp_cache_layout(m, batch, &pre_off, &g_off);
+  char* c = (char*)cache;
+  DeviceGuard guard(m->device);
+  return finish(nullptr,
+                launch_mlp_forward(m->fi, m->fo, m->act, m->n_layers, m->w, m->w_floats, batch, x,
+                                   (float*)c, (float*)(c + pre_off), out, (cudaStream_t)stream),
+                "nm_mlp_forward_cached");
+}
+
+int nm_mlp_backward(const nm_mlp* m, int64_t batch, void* cache, const float* out_grad,
+                    double* dparams, double* dx, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null network");
+  NM_CHECK_N(batch);
+  if (!cache || !out_grad || !dparams || !dx) return fail(NM_ERR_INVALID, "null input");
+  size_t pre_off, g_off;
+  mlp_cache_layout(m, batch, &pre_off, &g_off);
+  char* c = (char*)cache;
+  DeviceGuard guard(m->device);
+  if (batch == 0) {
+    const cudaError_t e = cudaMemsetAsync(dparams, 0, (size_t)m->w_floats * 8, (cudaStream_t)stream);
+    return e == cudaSuccess ? NM_OK : cuda_fail(e, "nm_mlp_backward");
+  }
+  return finish(nullptr,
+                launch_mlp_backward(m->fi, m->fo, m->act, m->n_layers, m->w, m->w_floats, batch,
+                                    (const float*)c, (const float*)(c + pre_off), out_grad,
+                                    (double*)(c + g_off), dparams, dx, (cudaStream_t)stream),
+                "nm_mlp_backward");
 }
 
 int nm_footprint_level(int64_t n, const double* area_texels, int32_t n_levels, double* level_out,

@@ -142,6 +142,16 @@ cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatPar
                                   int32_t n_mats, const int32_t* mat_id, const QueryArgs& a,
                                   cudaStream_t s);
 int smem_bytes_for(const MatParams& mp);
+// training-side kernels (nmq_train.cu)
+cudaError_t launch_texel_grads(const MatParams& mp, int64_t n, const float* uv, const int32_t* level,
+                               const float* z_grad, float* grad, cudaStream_t s);
+cudaError_t launch_mlp_forward(const int32_t* fi, const int32_t* fo, const int32_t* act, int n_layers,
+                               const float* wts, int32_t w_floats, int64_t B, const float* x,
+                               float* x_cache, float* pre_cache, float* out, cudaStream_t s);
+cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int32_t* act, int n_layers,
+                                const float* wts, int32_t w_floats, int64_t B, const float* x_cache,
+                                const float* pre_cache, const float* out_grad, double* g_cache,
+                                double* dparams, double* dx, cudaStream_t s);
 // level of detail from ray cones (nmq_lod.cu)
 cudaError_t launch_footprint_level(int64_t n, const double* area, int32_t n_levels, double* out,
                                    cudaStream_t s);

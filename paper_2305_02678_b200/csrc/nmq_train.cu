@@ -1,0 +1,340 @@
+// nmq_train.cu — training-side kernels: the exact adjoint of
+// the latent fetch (latent.py:109-119 accumulate_texel_grads) and the fp32
+// network engine's forward_cached / backward (mlp.py:90-116), used by the
+// reference's offline baking loop (training.py).
+//
+//  * texel_grads_kernel: one thread per query — the same wrap-addressed taps
+//    as the fetch (bit-exact indices), float64 bilinear weights like the
+//    reference, contributions scattered with fp32 atomics into the gradient
+//    texels (levels back to back, 8 channels).  Atomic/HBM-bound.
+//  * mlp_forward_kernel: one thread per row, weights in SMEM, fp32 FMA (the
+//    reference's float32 forward); pre-activations cached column-major
+//    (coalesced per neuron) for the backward.
+//  * mlp_backward_kernel: one thread per row, the reverse chain in float64
+//    (the reference promotes to float64 at its first leaky layer), per-layer
+//    output gradients cached column-major.
+//  * mlp_dparam_kernel: dW = g^T x and db = sum g over the batch — a
+//    split-K reduction: each CTA stages 32-row tiles of g and the layer
+//    input in SMEM, accumulates its (out x in+1) partials in float64
+//    registers and adds them to the result with float64 atomics.
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "nmq_device.cuh"
+#include "nmq_internal.h"
+
+namespace nmq {
+namespace {
+
+using namespace dev;
+
+constexpr int kMaxW = 64;  // max layer width of the training kernels
+
+// ---------------------------------------------------------------------------
+// texel gradients
+
+__device__ __forceinline__ void axis_f64(double c, int32_t n, int32_t& i0, int32_t& i1, double& f) {
+  // latent.py:59-68: x = u*w - 0.5; x0 = floor(x) mod w (Python modulo); f = x - floor(x)
+  const double fl = floor(c);
+  f = c - fl;
+  int64_t i = (int64_t)fl % n;
+  if (i < 0) i += n;
+  i0 = (int32_t)i;
+  i1 = (i0 + 1 == n) ? 0 : i0 + 1;
+}
+
+__global__ void texel_grads_kernel(const __grid_constant__ MatParams mp, int64_t n,
+                                   const float* __restrict__ uv, const int32_t* __restrict__ level,
+                                   const float* __restrict__ z_grad, float* __restrict__ grad) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    int l = __ldg(level + q);
+    l = l < 0 ? 0 : (l > mp.n_levels - 1 ? mp.n_levels - 1 : l);
+    const LevelDesc L = mp.lv[l];
+    int32_t x0, x1, y0, y1;
+    double fx, fy;
+    axis_f64(fma((double)__ldg(uv + 2 * q), (double)L.w, -0.5), L.w, x0, x1, fx);
+    axis_f64(fma((double)__ldg(uv + 2 * q + 1), (double)L.h, -0.5), L.h, y0, y1, fy);
+    const double w[4] = {(1.0 - fx) * (1.0 - fy), fx * (1.0 - fy), (1.0 - fx) * fy, fx * fy};
+    const int32_t xs[4] = {x0, x1, x0, x1}, ys[4] = {y0, y0, y1, y1};  // latent.py:69-73 tap order
+    float g[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) g[c] = __ldg(z_grad + 8 * q + c);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t t = L.off + (int64_t)ys[k] * L.w + xs[k];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) atomicAdd(grad + 8 * t + c, (float)(w[k] * (double)g[c]));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// MLP forward_cached / backward
+
+struct MlpView {
+  int32_t n_layers;
+  int32_t fi[kMaxLayers], fo[kMaxLayers], act[kMaxLayers];
+  int32_t w_off[kMaxLayers];  // float offset of layer l in the access-order weights
+  int32_t w_floats;
+};
+
+template <int kMW>
+__global__ void mlp_forward_kernel(const __grid_constant__ MlpView v, int64_t B,
+                                   const float* __restrict__ wts, const float* __restrict__ x,
+                                   float* __restrict__ x_cache, float* __restrict__ pre_cache,
+                                   float* __restrict__ out) {
+  extern __shared__ float sw[];
+  for (int i = threadIdx.x; i < v.w_floats; i += blockDim.x) sw[i] = wts[i];
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < B;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    float a[kMW], p[kMW];
+    const int fi0 = v.fi[0];
+#pragma unroll
+    for (int k = 0; k < kMW; ++k)
+      if (k < fi0) {
+        a[k] = __ldg(x + r * fi0 + k);
+        x_cache[(int64_t)k * B + r] = a[k];
+      }
+    int64_t pre_base = 0;
+    for (int l = 0; l < v.n_layers; ++l) {
+      const int fi = v.fi[l], fo = v.fo[l];
+      const float* W = sw + v.w_off[l];
+#pragma unroll
+      for (int j = 0; j < kMW; ++j) {
+        if (j < fo) {
+          const float* row = W + j * (fi + 1);
+          float acc = 0.f;
+#pragma unroll
+          for (int k = 0; k < kMW; ++k)
+            if (k < fi) acc = fmaf(a[k], row[k], acc);
+          p[j] = acc + row[fi];  // x W^T + b (mlp.py:96)
+          pre_cache[pre_base + (int64_t)j * B + r] = p[j];
+        }
+      }
+      const bool leaky = v.act[l] != 0;
+#pragma unroll
+      for (int j = 0; j < kMW; ++j)
+        if (j < fo) a[j] = leaky ? (p[j] >= 0.f ? p[j] : kLeaky * p[j]) : p[j];
+      pre_base += (int64_t)fo * B;
+    }
+    const int fl = v.fo[v.n_layers - 1];
+#pragma unroll
+    for (int j = 0; j < kMW; ++j)
+      if (j < fl) out[r * fl + j] = a[j];
+  }
+}
+
+template <int kMW>
+__global__ void mlp_backward_kernel(const __grid_constant__ MlpView v, int64_t B,
+                                    const float* __restrict__ wts, const float* __restrict__ pre_cache,
+                                    const float* __restrict__ out_grad, double* __restrict__ g_cache,
+                                    double* __restrict__ dx) {
+  extern __shared__ float sw[];
+  for (int i = threadIdx.x; i < v.w_floats; i += blockDim.x) sw[i] = wts[i];
+  __syncthreads();
+  int64_t pre_off[kMaxLayers];
+  {
+    int64_t o = 0;
+    for (int l = 0; l < v.n_layers; ++l) {
+      pre_off[l] = o;
+      o += (int64_t)v.fo[l] * B;
+    }
+  }
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < B;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double g[kMW], h[kMW];
+    const int fl = v.fo[v.n_layers - 1];
+#pragma unroll
+    for (int j = 0; j < kMW; ++j)
+      if (j < fl) g[j] = (double)__ldg(out_grad + r * fl + j);
+    for (int l = v.n_layers - 1; l >= 0; --l) {
+      const int fi = v.fi[l], fo = v.fo[l];
+      const bool leaky = v.act[l] != 0;
+#pragma unroll
+      for (int j = 0; j < kMW; ++j) {
+        if (j < fo) {
+          if (leaky && __ldg(pre_cache + pre_off[l] + (int64_t)j * B + r) < 0.f) g[j] *= (double)kLeaky;
+          g_cache[pre_off[l] + (int64_t)j * B + r] = g[j];  // same column-major layout as pre
+        }
+      }
+      const float* W = sw + v.w_off[l];
+#pragma unroll
+      for (int k = 0; k < kMW; ++k) {
+        if (k < fi) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < kMW; ++j)
+            if (j < fo) acc = fma(g[j], (double)W[j * (fi + 1) + k], acc);
+          h[k] = acc;  // g @ W (mlp.py:115)
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kMW; ++k)
+        if (k < fi) g[k] = h[k];
+    }
+    const int fi0 = v.fi[0];
+#pragma unroll
+    for (int k = 0; k < kMW; ++k)
+      if (k < fi0) dx[r * fi0 + k] = g[k];
+  }
+}
+
+// dW[j][k] = sum_r g[j][r] * in[k][r], db[j] = sum_r g[j][r]   (mlp.py:114)
+// `in` = the cached input x (layer 0) or act(pre of the previous layer).
+constexpr int kRowsPerCta = 256, kTileRows = 32;  // ~B/256 CTAs of split-K partials
+
+__global__ void __launch_bounds__(256) mlp_dparam_kernel(int64_t B, int fi, int fo, int in_act,
+                                                         const float* __restrict__ in_src,
+                                                         const double* __restrict__ g,
+                                                         double* __restrict__ dp) {
+  __shared__ double sg[kMaxW][kTileRows];
+  __shared__ float sx[kMaxW + 1][kTileRows];
+  const int pairs = fo * (fi + 1);
+  constexpr int kPer = (kMaxW * (kMaxW + 1) + 255) / 256;
+  double acc[kPer];
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) acc[e] = 0.0;
+  const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
+  const int64_t r1 = r0 + kRowsPerCta < B ? r0 + kRowsPerCta : B;
+  for (int64_t t0 = r0; t0 < r1; t0 += kTileRows) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < fo * kTileRows; i += blockDim.x) {
+      const int j = i / kTileRows, rr = i % kTileRows;
+      const int64_t r = t0 + rr;
+      sg[j][rr] = r < r1 ? g[(int64_t)j * B + r] : 0.0;
+    }
+    for (int i = threadIdx.x; i < (fi + 1) * kTileRows; i += blockDim.x) {
+      const int k = i / kTileRows, rr = i % kTileRows;
+      const int64_t r = t0 + rr;
+      float xv = 0.f;
+      if (r < r1) {
+        if (k == fi) {
+          xv = 1.f;  // bias column
+        } else {
+          xv = in_src[(int64_t)k * B + r];
+          if (in_act && xv < 0.f) xv *= kLeaky;
+        }
+      }
+      sx[k][rr] = xv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < kPer; ++e) {
+      const int pidx = threadIdx.x + e * 256;
+      if (pidx < pairs) {
+        const int j = pidx / (fi + 1), k = pidx % (fi + 1);
+        double s = acc[e];
+#pragma unroll
+        for (int rr = 0; rr < kTileRows; ++rr) s = fma(sg[j][rr], (double)sx[k][rr], s);
+        acc[e] = s;
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int pidx = threadIdx.x + e * 256;
+    if (pidx < pairs) atomicAdd(dp + pidx, acc[e]);
+  }
+}
+
+int max_width(const MlpView& v) {
+  int w = 0;
+  for (int l = 0; l < v.n_layers; ++l) {
+    w = v.fi[l] > w ? v.fi[l] : w;
+    w = v.fo[l] > w ? v.fo[l] : w;
+  }
+  return w;
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return sms;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers (C ABI in nmq_abi.cu)
+
+cudaError_t launch_texel_grads(const MatParams& mp, int64_t n, const float* uv, const int32_t* level,
+                               const float* z_grad, float* grad, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
+  texel_grads_kernel<<<(int)blocks, 256, 0, s>>>(mp, n, uv, level, z_grad, grad);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mlp_forward(const int32_t* fi, const int32_t* fo, const int32_t* act, int n_layers,
+                               const float* wts, int32_t w_floats, int64_t B, const float* x,
+                               float* x_cache, float* pre_cache, float* out, cudaStream_t s) {
+  MlpView v{};
+  v.n_layers = n_layers;
+  int32_t o = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    v.fi[l] = fi[l];
+    v.fo[l] = fo[l];
+    v.act[l] = act[l];
+    v.w_off[l] = o;
+    o += fo[l] * (fi[l] + 1);
+  }
+  v.w_floats = w_floats;
+  const size_t smem = (size_t)w_floats * 4;
+  const bool wide = max_width(v) > 32;  // register arrays sized to the widest layer
+  auto kern = wide ? mlp_forward_kernel<64> : mlp_forward_kernel<32>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (B + 127) / 128;
+  if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
+  kern<<<(int)blocks, 128, smem, s>>>(v, B, wts, x, x_cache, pre_cache, out);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int32_t* act, int n_layers,
+                                const float* wts, int32_t w_floats, int64_t B, const float* x_cache,
+                                const float* pre_cache, const float* out_grad, double* g_cache,
+                                double* dparams, double* dx, cudaStream_t s) {
+  MlpView v{};
+  v.n_layers = n_layers;
+  int32_t o = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    v.fi[l] = fi[l];
+    v.fo[l] = fo[l];
+    v.act[l] = act[l];
+    v.w_off[l] = o;
+    o += fo[l] * (fi[l] + 1);
+  }
+  v.w_floats = w_floats;
+  const size_t smem = (size_t)w_floats * 4;
+  const bool wide = max_width(v) > 32;
+  auto kern = wide ? mlp_backward_kernel<64> : mlp_backward_kernel<32>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t blocks = (B + 127) / 128;
+  if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
+  kern<<<(int)blocks, 128, smem, s>>>(v, B, wts, pre_cache, out_grad, g_cache, dx);
+  ++g_launches;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(dparams, 0, (size_t)w_floats * 8, s)) != cudaSuccess) return e;
+  int64_t pre_off = 0;
+  const int grid = (int)((B + kRowsPerCta - 1) / kRowsPerCta);
+  for (int l = 0; l < n_layers; ++l) {
+    const float* in_src = l == 0 ? x_cache : pre_cache + (pre_off - (int64_t)fo[l - 1] * B);
+    const int in_act = l == 0 ? 0 : act[l - 1];
+    mlp_dparam_kernel<<<grid, 256, 0, s>>>(B, fi[l], fo[l], in_act, in_src, g_cache + pre_off,
+                                           dparams + v.w_off[l]);
+    ++g_launches;
+    pre_off += (int64_t)fo[l] * B;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace nmq

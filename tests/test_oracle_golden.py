@@ -102,3 +102,29 @@ def test_lod_from_ray_cones_matches_reference():
     lv = O.cone_level(g["cone_w"], g["cone_s"], g["t"], g["cos_hit"], g["density"], int(g["n_levels"]))
     assert np.array_equal(lv, g["level"])
     assert np.array_equal(O.footprint_to_level(g["area"], int(g["n_levels"])), g["area_level"])
+
+
+def test_training_side_oracle_matches_reference():
+    """forward_cached / backward / accumulate_texel_grads restatements
+    against the reference's own outputs (tests/golden/train.npz)."""
+    g = load_golden("train")
+    for tag in ("brdf", "samp"):
+        n = int(g[f"{tag}_n"])
+        net = O.Net([(g[f"{tag}_w{i}"], g[f"{tag}_b{i}"], "linear" if int(g[f"{tag}_a{i}"]) == 0 else "leaky_relu")
+                     for i in range(n)])
+        out, cache = O.forward_cached(net, g[f"{tag}_x"])
+        assert np.array_equal(out, g[f"{tag}_out"])
+        grads, dx = O.backward(net, cache, g[f"{tag}_g"])
+        assert np.array_equal(dx, g[f"{tag}_dx"])
+        for i in range(n):
+            assert np.array_equal(grads[i][0], g[f"{tag}_dw{i}"])
+            assert np.array_equal(grads[i][1], g[f"{tag}_db{i}"])
+    levels = []
+    i = 0
+    while f"tg_grad{i}" in g:
+        levels.append(np.zeros_like(g[f"tg_grad{i}"]))
+        i += 1
+    pyr = O.Pyramid([np.zeros_like(l) for l in levels])
+    pyr.accumulate_texel_grads(levels, g["tg_uv"].astype(np.float64), g["tg_level"], g["tg_zgrad"])
+    for i, l in enumerate(levels):
+        assert np.array_equal(l, g[f"tg_grad{i}"])
