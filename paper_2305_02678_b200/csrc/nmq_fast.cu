@@ -357,7 +357,7 @@ struct SlotSt {
   TexPrefetch nx;   // texels of the slot's next tile
 };
 
-template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS>
+template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG>
 __global__ void __launch_bounds__(G * 128, 1)
 fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
             const __grid_constant__ FastConsts fc) {
@@ -440,8 +440,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
 
   const float lod0 = a.lod_stride ? 0.f : __ldg(a.lod);
-  const int64_t seg_base = a.seg ? (int64_t)__ldg(a.seg) : 0;  // binned segment rows
-  const int64_t n_rows = a.seg ? (int64_t)__ldg(a.seg + 1) : a.n;
+  // SEG: a binned segment (device row range + output-row indirection); the
+  // plain instantiation carries none of it
+  const int64_t seg_base = SEG && a.seg ? (int64_t)__ldg(a.seg) : 0;
+  const int64_t n_rows = SEG && a.seg ? (int64_t)__ldg(a.seg + 1) : a.n;
   const int ntiles = (int)((n_rows + kTile - 1) / kTile);  // host guarantees < 2^31
   const int last_full = (int)(n_rows / kTile);                // tiles [0, last_full) are full
   const int stride = gridDim.x * G;                        // between a group's tiles
@@ -528,7 +530,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           if constexpr (Need<MODE>::u3) S.u3 = v3(ib.u3[3 * r], ib.u3[3 * r + 1], ib.u3[3 * r + 2]);
           S.up = (S.wi.z > 0.f) && (wo.z > 0.f);
           if (want_level) {
-            if (valid) a.level[a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
+            if (valid) a.level[SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
           }
           // the slot's next tile: texel loads now, blended at the last stage
           if (S.t + sstride < ntiles) {
@@ -583,7 +585,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           float y[6];
           out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
           if (valid) {
-            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
+            const int64_t q = SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                               : v3(0.f, 0.f, 0.f);
             stg3(a.rgb, q, f);
@@ -634,7 +636,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           for (int j = 0; j < 9; ++j) raw[j] = __uint_as_float(yr[j]);
           const Proxy p = proxy_from_raw(raw, mp.isotropic != 0, fc.inv_samp);
           if (valid) {
-            const int64_t q = a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
+            const int64_t q = SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             if (a.params9) store_proxy(a.params9, q, p);
             const V3 w = proxy_sample(p, S.wi, S.u3.x, S.u3.y, S.u3.z);
             stg3(a.ws, q, w);
@@ -700,7 +702,10 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  auto kern = fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS>;
+  const bool seg = a.seg || a.out_idx;
+  if (seg && MODE != kModeEval) return cudaErrorNotSupported;  // binned segments are eval-only
+  auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, (MODE == kModeEval)>
+                  : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
   const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>) +
                          (TS ? G * NS * kTile * 64 : 0));
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
