@@ -584,16 +584,19 @@ int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
   return finish(m, launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream), "nm_eval");
 }
 
-// Host-buffer eval: the batch streams through the GPU in chunks on two
-// internal streams — H2D of chunk c+1, the fused kernel of chunk c and the
+// Host-buffer eval: the batch streams through the GPU in chunks on
+// NMQ_HOST_STREAMS internal streams — H2D of chunk c+1, the fused kernel of chunk c and the
 // D2H of chunk c-1 overlap (copy engines + SMs).  Blocking: returns when
 // rgb_out (host) is complete.  Device staging is per device, grow-only.
 namespace {
+#ifndef NMQ_HOST_STREAMS
+#define NMQ_HOST_STREAMS 4  // chunks in flight: H2D can run ahead of the D2H of older chunks
+#endif
 struct HostStage {
   std::mutex mu;
   char* buf = nullptr;
   size_t bytes = 0;
-  cudaStream_t st[2] = {};
+  cudaStream_t st[NMQ_HOST_STREAMS] = {};
   cudaEvent_t ev_start = nullptr;
 };
 HostStage g_stage[16];
@@ -614,7 +617,7 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
   std::lock_guard<std::mutex> lock(H.mu);
   cudaError_t e;
   const size_t per_row = 8 + 4 + 4 + 12 + 12 + 12;  // uv lod u_rr wi wo | rgb
-  const size_t need = 2 * (size_t)chunk * per_row + 1024;
+  const size_t need = NMQ_HOST_STREAMS * (size_t)chunk * per_row + 1024;
   if (H.bytes < need) {
     if (H.buf) cudaFree(H.buf);
     H.buf = nullptr;
@@ -630,8 +633,8 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
   for (auto& st : H.st) cudaStreamWaitEvent(st, H.ev_start, 0);
   for (int64_t c0 = 0, ci = 0; c0 < n; c0 += chunk, ++ci) {
     const int64_t c = n - c0 < chunk ? n - c0 : chunk;
-    cudaStream_t st = H.st[ci & 1];
-    char* base = H.buf + (size_t)(ci & 1) * chunk * per_row;
+    cudaStream_t st = H.st[ci % NMQ_HOST_STREAMS];
+    char* base = H.buf + (size_t)(ci % NMQ_HOST_STREAMS) * chunk * per_row;
     float* d_uv = (float*)base;
     float* d_lod = d_uv + 2 * chunk;
     float* d_urr = d_lod + chunk;
