@@ -1,0 +1,40 @@
+"""Small launches of every query entry point, the multi-material modes, LoD
+and training kernels (for compute-sanitizer; partial tiles included)."""
+import os, sys
+sys.path.insert(0, os.getcwd())
+import numpy as np
+import torch
+from oracle import nm_oracle as O
+from paper_2305_02678_b200 import neural, render, train, mlp
+from paper_2305_02678_b200.latent import LatentPyramid
+
+rng = np.random.default_rng(0)
+mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), rng)
+mat.latent = LatentPyramid(O.random_pyramid(rng, 64, 32).levels)
+n = 1000 + 37
+uv = rng.random((n, 2)).astype(np.float32)
+lod = (rng.random(n) * 5).astype(np.float32)
+urr = rng.random(n).astype(np.float32)
+wi, wo = O.draw_direction_pairs(rng, n)
+wi, wo = wi.astype(np.float32), wo.astype(np.float32)
+u3 = rng.random((n, 3)).astype(np.float32)
+neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=True)
+neural.sample_pdf(mat, uv, lod, urr, wi, u3)
+neural.query(mat, uv, lod, urr, wi, wo, u3)
+neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=False)
+z, _ = mat.latent.fetch(uv, lod, urr)
+neural.eval_brdf(mat, z, wi, wo, fp16=True)
+neural.infer_proxy(mat, z, wi, fp16=True)
+mats = [mat, neural.NeuralMaterial.create(neural.NeuralMaterialConfig(brdf_hidden="2x16"), rng)]
+mats[1].latent = LatentPyramid(O.random_pyramid(rng, 32, 32).levels)
+ids = rng.integers(0, 2, n).astype(np.int32)
+for mode in ("binned", "binned_async", "divergent"):
+    neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode=mode)
+render.cone_level(rng.random(n).astype(np.float32), rng.random(n).astype(np.float32),
+                  rng.random(n).astype(np.float32), rng.random(n).astype(np.float32), 100.0, 6)
+net = mlp.Mlp.create((20, 32, 32, 3), rng)
+out, cache = train.forward_cached(net, rng.normal(size=(n, 20)).astype(np.float32))
+train.backward(net, cache, rng.normal(size=(n, 3)).astype(np.float32))
+mat.latent.accumulate_texel_grads(mat.latent.zero_grads(), uv, np.zeros(n, np.int64), rng.normal(size=(n, 8)).astype(np.float32))
+torch.cuda.synchronize()
+print("sanitize_run ok")
