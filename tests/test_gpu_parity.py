@@ -458,3 +458,68 @@ def test_texel_grad_scatter_vs_reference():
     for i, gl in enumerate(grads):
         want = g[f"tg_grad{i}"] + (1.0 if i == 0 else 0.0)
         np.testing.assert_allclose(gl, want, rtol=1e-5, atol=1e-5)
+
+
+# --- boundary inputs ------------------------------------------------------------
+
+def _edge_inputs(rng, n_levels):
+    """lod at / beyond the ends and at integers, u_rr at 0 and just below 1,
+    uv on texel centres, at 0 / 1 and far outside [0, 1) (wrap), directions
+    at and below the horizon and wi == wo."""
+    from oracle import nm_oracle as O
+    n = 4096
+    uv = rng.random((n, 2))
+    uv[:256] = np.floor(uv[:256] * 64) / 64 + 0.5 / 64            # texel centres
+    uv[256:512] = rng.choice([0.0, 1.0, -1.0, 2.0, -1000.25, 999.75], (256, 2))
+    uv[512:768] = rng.uniform(-50, 50, (256, 2))
+    lod = rng.random(n) * (n_levels - 1)
+    lod[:300] = rng.choice([-3.0, 0.0, 1.0, 2.0, n_levels - 1.0, n_levels + 4.0], 300)
+    urr = rng.random(n)
+    urr[:200] = 0.0
+    urr[200:400] = np.float32(1.0) - np.float32(2 ** -24)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    wi[800:900, 2] *= -1.0                                          # below the horizon
+    wo[900:1000, 2] *= -1.0
+    wo[1000:1100] = wi[1000:1100]                                  # wi == wo
+    wi[1100:1132] = [0.0, 0.0, 1.0]                                # zenith
+    f32 = lambda a: np.ascontiguousarray(a, np.float32)  # noqa: E731
+    return f32(uv), f32(lod), f32(urr), f32(wi), f32(wo), f32(rng.random((n, 3)))
+
+
+def test_boundary_inputs_all_paths(kernel_path):
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+
+    rng = np.random.default_rng(5)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 64, 64).levels)
+    om = _oracle_from(mat)
+    uv, lod, urr, wi, wo, u3 = _edge_inputs(rng, mat.latent.n_levels)
+    f_ref, ws_ref, pdf_ref, p_ref, ch_ref = O.full_query(om, uv, lod, urr, wi, wo, u3)
+    f, ws, pdf, ch = neural.query(mat, uv, lod, urr, wi, wo, u3, return_level=True)
+    assert np.array_equal(ch, ch_ref)
+    assert np.all(f[800:1000] == 0.0)  # below the horizon -> zero (neural.py:295-296)
+    check_rel(f, f_ref, what="boundary rgb")
+    check_dirs(ws, ws_ref, u3, p_ref, wi)
+    assert np.all(np.isfinite(ws)) and np.all(np.isfinite(pdf)) and np.all(pdf >= 0.0)
+
+
+def test_empty_batches_are_no_ops():
+    import torch
+    from paper_2305_02678_b200 import neural, render
+    from paper_2305_02678_b200.latent import LatentPyramid
+    from oracle import nm_oracle as O
+
+    rng = np.random.default_rng(6)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 16, 16).levels)
+    e2, e3, e1 = np.zeros((0, 2), np.float32), np.zeros((0, 3), np.float32), np.zeros(0, np.float32)
+    f, _, ch = neural.eval_material(mat, e2, e1, e3, e3, e1, fp16=True)
+    assert f.shape == (0, 3) and ch.shape == (0,)
+    ws, pdf = neural.sample_pdf(mat, e2, e1, e1, e3, e3)
+    assert ws.shape == (0, 3) and pdf.shape == (0,)
+    assert render.cone_level(e1, e1, e1, e1, 1.0, 5).shape == (0,)
+    z, lv = mat.latent.fetch(e2, e1, e1)
+    assert z.shape == (0, 8)
+    torch.cuda.synchronize()
