@@ -170,6 +170,25 @@ struct NoOp {
   __device__ void operator()() const {}
 };
 
+// Query: the frame layer (N = 16 into F) and the sampler's first layer (N =
+// SW into E) both read input chunk 0 — one barrier, one commit.
+template <int SW, int LW>
+__device__ __forceinline__ void mma_issue_first2(const GG& g, uint32_t f_tmem, uint32_t e_tmem,
+                                                 uint32_t a_tmem, uint32_t frame_off, uint32_t s1_off,
+                                                 uint64_t* bar) {
+  tc::tmem_st_wait();
+  tc::tc_fence_before();
+  tc::named_bar(g.bar_id, 128);
+  if (g.r == 32 * LW) {
+    tc::tc_fence_after();
+    tc::mma_ts(f_tmem, a_tmem, g.desc0 + ((uint64_t)((16 * 16) >> 4) << 16) + (frame_off >> 4),
+               tc::idesc_f16(128, 16), 0);
+    tc::mma_ts(e_tmem, a_tmem, g.desc0 + ((uint64_t)((SW * 16) >> 4) << 16) + (s1_off >> 4),
+               tc::idesc_f16(128, SW), 0);
+    tc::mma_commit(bar);
+  }
+}
+
 // D[0, W) -> scaled leaky -> (hi, lo) into A
 template <int W>
 __device__ __forceinline__ void hidden_epi(uint32_t dl, uint32_t al) {
@@ -345,6 +364,7 @@ __device__ __forceinline__ void blend_pack(const TexPrefetch& p, uint32_t (&zp)[
 struct SlotSt {
   uint32_t d0, a0;  // lane-0 TMEM addresses: accumulator D, input A (frame D at a0 + 16)
   uint32_t dl, al;  // the same with this warp's lane field
+  uint32_t e0, el;  // query: sampler layer-1 accumulator (lane 0 / this warp's lanes)
   uint64_t* bar;    // MMA completion barrier
   uint32_t ph;      // its parity
   int t;            // current tile (>= ntiles: idle)
@@ -368,13 +388,17 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   __shared__ uint32_t tbase_sh;
   constexpr bool kBrdf = Need<MODE>::brdf, kSamp = Need<MODE>::samp;
   // stage layout of one tile (see the file comment)
-  constexpr int kOutB = kBrdf ? BNH : -1;             // BRDF output stage
-  constexpr int kS0 = kBrdf ? BNH + 1 : 0;            // first sampler stage
-  constexpr int kFinal = kSamp ? kS0 + SNH : kOutB;   // last stage
+  // query: the sampler's first layer reads the same input chunk 0 as the
+  // frame layer, so both are issued together (its D in a third region E) and
+  // the sampler chain starts at the BRDF output stage: one round trip less
+  constexpr bool kQM = kBrdf && kSamp;
+  constexpr int kOutB = kBrdf ? BNH : -1;                   // BRDF output stage
+  constexpr int kS0 = kBrdf ? (kQM ? BNH : BNH + 1) : 0;    // stage issuing sampler layer 2
+  constexpr int kFinal = kSamp ? kS0 + SNH : kOutB;         // last stage
   constexpr int kStages = kFinal + 1;
   constexpr int DW = BW > SW ? BW : SW;
   static_assert(DW >= 32, "frame-layer D aliases A columns [16, 32)");
-  constexpr uint32_t kSlotCols = 2 * DW;
+  constexpr uint32_t kSlotCols = 2 * DW + (kQM ? SW : 0);
   constexpr uint32_t kBiasCol = G * NS * kSlotCols;
   static_assert(kBiasCol + 32 <= 512, "TMEM budget");
   // power-of-two allocation covering all slots + bias chunks, so CTAs that
@@ -458,6 +482,8 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     sl[s].a0 = sl[s].d0 + DW;
     sl[s].dl = sl[s].d0 + lane;
     sl[s].al = sl[s].a0 + lane;
+    sl[s].e0 = sl[s].a0 + DW;
+    sl[s].el = sl[s].e0 + lane;
     sl[s].bar = &mma_bar[gi][s];
     sl[s].ph = 0u;
     sl[s].t = blockIdx.x * G + gi + s * stride;
@@ -480,7 +506,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     const uint32_t x[8] = {S.zp[0], S.zp[1], S.zp[2], S.zp[3],
                            pack2(ib.wi[3 * r], ib.wi[3 * r + 1]), pack2(ib.wi[3 * r + 2], 1.f), 0u, 0u};
     tc::tmem_st8(S.al, x);
-    if constexpr (kBrdf)
+    if constexpr (kQM)
+      mma_issue_first2<SW, LW>(g, S.a0 + 16, S.e0, S.a0, mp.fast_frame_off, mp.layers[mp.samp_first].b_off,
+                               S.bar);
+    else if constexpr (kBrdf)
       mma_issue<16, 1, false, LW>(g, S.a0 + 16, S.a0, mp.fast_frame_off, 0, S.bar, NoOp{});
     else
       mma_issue<SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar, NoOp{});
@@ -595,13 +624,15 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
               stg3(a.albedo, q, al);
             }
           }
-          if constexpr (kSamp) {
-            // query: sampler input chunk 0 = [z, wi, 1] -> sampler layer 1
-            const uint32_t x[8] = {S.zp[0], S.zp[1], S.zp[2], S.zp[3],
-                                   pack2(S.wi.x, S.wi.y), pack2(S.wi.z, 1.f), 0u, 0u};
-            tc::tmem_st8(S.al, x);
-            mma_issue<SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar,
-                                        NoOp{});
+          if constexpr (kQM) {
+            // query: sampler layer 1 (issued with the frame layer, in E) -> layer 2
+            hidden_epi<SW>(S.el, S.al);
+            if constexpr (SNH == 1)
+              mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
+                                                   1, S.bar, NoOp{});
+            else
+              mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
+                                                   1, S.bar, NoOp{});
           }
         } else if constexpr (kSamp && k > kS0 && k < kFinal) {
           // sampler layer j+1 (j = k - kS0 >= 1; stage kS0 is k == 0 or handled below)
@@ -614,16 +645,6 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           else
             mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
                                                  j + 1, S.bar, NoOp{});
-        } else if constexpr (kSamp && kBrdf && k == kS0) {
-          // query: sampler layer 1 D -> layer 2
-          wait_mma();
-          hidden_epi<SW>(S.dl, S.al);
-          if constexpr (SNH == 1)
-            mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                 1, S.bar, NoOp{});
-          else
-            mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                 1, S.bar, NoOp{});
         }
         if constexpr (kSamp && k == kFinal) {
           // proxy parameters, sample, pdf
