@@ -455,9 +455,15 @@ def test_texel_grad_scatter_vs_reference():
     grads = pyr.zero_grads()
     grads[0] += 1.0  # accumulate, not overwrite
     pyr.accumulate_texel_grads(grads, g["tg_uv"], g["tg_level"], g["tg_zgrad"])
+    # fp32 sums in a different order (atomics vs np.add.at): the error bound
+    # scales with the per-texel sum of |contributions|, which the same kernel
+    # gives for |zgrad| (bilinear weights are non-negative)
+    mag = pyr.zero_grads()
+    pyr.accumulate_texel_grads(mag, g["tg_uv"], g["tg_level"], np.abs(g["tg_zgrad"]))
     for i, gl in enumerate(grads):
         want = g[f"tg_grad{i}"] + (1.0 if i == 0 else 0.0)
-        np.testing.assert_allclose(gl, want, rtol=1e-5, atol=1e-5)
+        tol = 1e-5 + 64 * np.finfo(np.float32).eps * mag[i]
+        assert np.all(np.abs(gl - want) <= tol), (i, np.abs(gl - want).max())
 
 
 # --- boundary inputs ------------------------------------------------------------
