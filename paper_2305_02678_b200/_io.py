@@ -79,8 +79,8 @@ def out(t, numpy_mode, np_dtype=np.float64):
 
 # ---------------------------------------------------------------------------
 # Large host (numpy) batches stream through the GPU inside the native library
-# (nm_eval_host: chunks on two internal streams, H2D / kernel / D2H
-# overlapped).  Host buffers should be pinned for full overlap.
+# (nm_eval_host: chunks over staging slots, H2D / kernel / D2H on three
+# internal streams, overlapped).  Host buffers should be pinned for full overlap.
 
 STREAM_CHUNK = int(os.environ.get("NMQ_STREAM_CHUNK", 1 << 19))  # queries per chunk
 

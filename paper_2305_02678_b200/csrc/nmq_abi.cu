@@ -584,20 +584,24 @@ int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
   return finish(m, launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream), "nm_eval");
 }
 
-// Host-buffer eval: the batch streams through the GPU in chunks on
-// NMQ_HOST_STREAMS internal streams — H2D of chunk c+1, the fused kernel of chunk c and the
-// D2H of chunk c-1 overlap (copy engines + SMs).  Blocking: returns when
-// rgb_out (host) is complete.  Device staging is per device, grow-only.
+// Host-buffer eval: the batch streams through the GPU in chunks over a ring
+// of NMQ_HOST_SLOTS device staging slots and three internal streams — one
+// for all H2D copies (chunks in order: concurrent H2D copies on several copy
+// engines would only share PCIe and finish together, delaying the first
+// kernel), one for the fused kernels, one for the D2H copies (the opposite
+// PCIe direction, overlapped with the later chunks' H2D).  Blocking: returns
+// when rgb_out (host) is complete.  Device staging is per device, grow-only.
 namespace {
-#ifndef NMQ_HOST_STREAMS
-#define NMQ_HOST_STREAMS 4  // chunks in flight: H2D can run ahead of the D2H of older chunks
+#ifndef NMQ_HOST_SLOTS
+#define NMQ_HOST_SLOTS 4  // chunks in flight: H2D can run ahead of the D2H of older chunks
 #endif
 struct HostStage {
   std::mutex mu;
   char* buf = nullptr;
   size_t bytes = 0;
-  cudaStream_t st[NMQ_HOST_STREAMS] = {};
+  cudaStream_t h2d = nullptr, run = nullptr, d2h = nullptr;
   cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_in[NMQ_HOST_SLOTS] = {}, ev_k[NMQ_HOST_SLOTS] = {}, ev_out[NMQ_HOST_SLOTS] = {};
 };
 HostStage g_stage[16];
 }  // namespace
@@ -617,7 +621,7 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
   std::lock_guard<std::mutex> lock(H.mu);
   cudaError_t e;
   const size_t per_row = 8 + 4 + 4 + 12 + 12 + 12;  // uv lod u_rr wi wo | rgb
-  const size_t need = NMQ_HOST_STREAMS * (size_t)chunk * per_row + 1024;
+  const size_t need = NMQ_HOST_SLOTS * (size_t)chunk * per_row + 1024;
   if (H.bytes < need) {
     if (H.buf) cudaFree(H.buf);
     H.buf = nullptr;
@@ -625,35 +629,48 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
     if ((e = cudaMalloc(&H.buf, need)) != cudaSuccess) return cuda_fail(e, "host-eval staging");
     H.bytes = need;
   }
-  if (!H.st[0]) {
-    for (auto& st : H.st) cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+  if (!H.h2d) {
+    for (cudaStream_t* st : {&H.h2d, &H.run, &H.d2h}) cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&H.ev_start, cudaEventDisableTiming);
+    for (int i = 0; i < NMQ_HOST_SLOTS; ++i) {
+      cudaEventCreateWithFlags(&H.ev_in[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&H.ev_k[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&H.ev_out[i], cudaEventDisableTiming);
+    }
   }
   cudaEventRecord(H.ev_start, (cudaStream_t)stream);  // after prior work on the caller's stream
-  for (auto& st : H.st) cudaStreamWaitEvent(st, H.ev_start, 0);
+  for (cudaStream_t st : {H.h2d, H.run, H.d2h}) cudaStreamWaitEvent(st, H.ev_start, 0);
   for (int64_t c0 = 0, ci = 0; c0 < n; c0 += chunk, ++ci) {
     const int64_t c = n - c0 < chunk ? n - c0 : chunk;
-    cudaStream_t st = H.st[ci % NMQ_HOST_STREAMS];
-    char* base = H.buf + (size_t)(ci % NMQ_HOST_STREAMS) * chunk * per_row;
+    const int s = (int)(ci % NMQ_HOST_SLOTS);
+    const bool reuse = ci >= NMQ_HOST_SLOTS;  // slot held an older chunk
+    char* base = H.buf + (size_t)s * chunk * per_row;
     float* d_uv = (float*)base;
     float* d_lod = d_uv + 2 * chunk;
     float* d_urr = d_lod + chunk;
     float* d_wi = d_urr + chunk;
     float* d_wo = d_wi + 3 * chunk;
     float* d_rgb = d_wo + 3 * chunk;
-    cudaMemcpyAsync(d_uv, uv + 2 * c0, c * 8, cudaMemcpyHostToDevice, st);
-    if (lod_stride) cudaMemcpyAsync(d_lod, lod + c0, c * 4, cudaMemcpyHostToDevice, st);
-    else cudaMemcpyAsync(d_lod, lod, 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_urr, u_rr + c0, c * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_wi, wi + 3 * c0, c * 12, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_wo, wo + 3 * c0, c * 12, cudaMemcpyHostToDevice, st);
+    if (reuse) cudaStreamWaitEvent(H.h2d, H.ev_k[s], 0);  // older chunk's kernel has read the inputs
+    cudaMemcpyAsync(d_uv, uv + 2 * c0, c * 8, cudaMemcpyHostToDevice, H.h2d);
+    if (lod_stride) cudaMemcpyAsync(d_lod, lod + c0, c * 4, cudaMemcpyHostToDevice, H.h2d);
+    else cudaMemcpyAsync(d_lod, lod, 4, cudaMemcpyHostToDevice, H.h2d);
+    cudaMemcpyAsync(d_urr, u_rr + c0, c * 4, cudaMemcpyHostToDevice, H.h2d);
+    cudaMemcpyAsync(d_wi, wi + 3 * c0, c * 12, cudaMemcpyHostToDevice, H.h2d);
+    cudaMemcpyAsync(d_wo, wo + 3 * c0, c * 12, cudaMemcpyHostToDevice, H.h2d);
+    cudaEventRecord(H.ev_in[s], H.h2d);
+    cudaStreamWaitEvent(H.run, H.ev_in[s], 0);
+    if (reuse) cudaStreamWaitEvent(H.run, H.ev_out[s], 0);  // older chunk's rgb has left
     QueryArgs a{};
     a.n = c; a.uv = d_uv; a.lod = d_lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = d_urr;
     a.wi = d_wi; a.wo = d_wo; a.rgb = d_rgb;
-    if ((e = launch_fused(m->mp, kModeEval, a, st)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
-    cudaMemcpyAsync(rgb_out + 3 * c0, d_rgb, c * 12, cudaMemcpyDeviceToHost, st);
+    if ((e = launch_fused(m->mp, kModeEval, a, H.run)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
+    cudaEventRecord(H.ev_k[s], H.run);
+    cudaStreamWaitEvent(H.d2h, H.ev_k[s], 0);
+    cudaMemcpyAsync(rgb_out + 3 * c0, d_rgb, c * 12, cudaMemcpyDeviceToHost, H.d2h);
+    cudaEventRecord(H.ev_out[s], H.d2h);
   }
-  for (auto& st : H.st)
+  for (cudaStream_t st : {H.h2d, H.run, H.d2h})
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
   return NM_OK;
 }

@@ -55,6 +55,9 @@ using namespace dev;
 #ifndef NMQ_G_QUERY
 #define NMQ_G_QUERY 5
 #endif
+#ifndef NMQ_EVAL2
+#define NMQ_EVAL2 0  // eval in two stages per tile (see kE2)
+#endif
 #ifndef NMQ_FAST_NS
 #define NMQ_FAST_NS 1  // tiles in flight per group (2 = ping-pong; slower: fewer warps)
 #endif
@@ -169,6 +172,32 @@ __device__ __forceinline__ void mma_issue(const GG& g, uint32_t d_tmem, uint32_t
 struct NoOp {
   __device__ void operator()() const {}
 };
+
+// Eval (two-stage tiles): the last hidden BRDF layer of tile t (A -> D, KA
+// k-steps + bias chunk) and the frame layer of tile t+1 (X -> Y) issued
+// together — one barrier, one commit.
+template <int N, int KA, int LW>
+__device__ __forceinline__ void mma_issue_hid_frame(const GG& g, uint32_t d_tmem, uint32_t a_tmem,
+                                                    uint32_t b_off, int bias_chunk, bool frame,
+                                                    uint32_t y_tmem, uint32_t x_tmem, uint32_t frame_off,
+                                                    uint64_t* bar) {
+  tc::tmem_st_wait();
+  tc::tc_fence_before();
+  tc::named_bar(g.bar_id, 128);
+  if (g.r == 32 * LW) {
+    tc::tc_fence_after();
+    constexpr uint32_t idesc = tc::idesc_f16(128, N);
+    constexpr uint32_t lbo = N * 16;
+    const uint64_t d = g.desc0 + ((uint64_t)(lbo >> 4) << 16) + (b_off >> 4);
+#pragma unroll
+    for (int s = 0; s < KA; ++s) tc::mma_ts(d_tmem, a_tmem + 8 * s, d + ((s * 2 * lbo) >> 4), idesc, s > 0);
+    tc::mma_ts(d_tmem, g.bias0 + 8 * bias_chunk, d + ((KA * 2 * lbo) >> 4), idesc, 1);
+    if (frame)
+      tc::mma_ts(y_tmem, x_tmem, g.desc0 + ((uint64_t)((16 * 16) >> 4) << 16) + (frame_off >> 4),
+                 tc::idesc_f16(128, 16), 0);
+    tc::mma_commit(bar);
+  }
+}
 
 // Query: the frame layer (N = 16 into F) and the sampler's first layer (N =
 // SW into E) both read input chunk 0 — one barrier, one commit.
@@ -392,13 +421,19 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   // frame layer, so both are issued together (its D in a third region E) and
   // the sampler chain starts at the BRDF output stage: one round trip less
   constexpr bool kQM = kBrdf && kSamp;
+  // eval, two stages per tile (NMQ_EVAL2): tile t's output layer runs in
+  // tile t+1's first stage, and tile t+1's frame layer is issued with tile
+  // t's last hidden layer — 2 MMA round trips per tile instead of 3, for
+  // 32 more TMEM columns per group (X: next tile's input chunks, Y: its
+  // frame-layer D)
+  constexpr bool kE2 = NMQ_EVAL2 && MODE == kModeEval && NS == 1 && BNH == 2 && !TS;
   constexpr int kOutB = kBrdf ? BNH : -1;                   // BRDF output stage
   constexpr int kS0 = kBrdf ? (kQM ? BNH : BNH + 1) : 0;    // stage issuing sampler layer 2
   constexpr int kFinal = kSamp ? kS0 + SNH : kOutB;         // last stage
   constexpr int kStages = kFinal + 1;
   constexpr int DW = BW > SW ? BW : SW;
   static_assert(DW >= 32, "frame-layer D aliases A columns [16, 32)");
-  constexpr uint32_t kSlotCols = 2 * DW + (kQM ? SW : 0);
+  constexpr uint32_t kSlotCols = 2 * DW + (kQM ? SW : 0) + (kE2 ? 32 : 0);
   constexpr uint32_t kBiasCol = G * NS * kSlotCols;
   static_assert(kBiasCol + 32 <= 512, "TMEM budget");
   // power-of-two allocation covering all slots + bias chunks, so CTAs that
@@ -515,6 +550,104 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       mma_issue<SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar, NoOp{});
   };
 
+  if constexpr (kE2) {
+    // ===== eval, two stages per tile ============================================
+    SlotSt& S = sl[0];
+    const uint32_t X = S.a0 + DW, XL = X + lane, Y = X + 16, YL = Y + lane;
+    auto chunk0 = [&](const InBuf<MODE>& ib) {
+      const uint32_t x[8] = {S.zp[0], S.zp[1], S.zp[2], S.zp[3],
+                             pack2(ib.wi[3 * r], ib.wi[3 * r + 1]), pack2(ib.wi[3 * r + 2], 1.f), 0u, 0u};
+      tc::tmem_st8(XL, x);
+    };
+    if (S.t < ntiles) {
+      stage_inputs<MODE>(a, seg_base, n_rows, S.t, buf(0, 0), &in_bar[gi][0][0], r, r == 64);
+      if (S.t + sstride < ntiles)
+        stage_inputs<MODE>(a, seg_base, n_rows, S.t + sstride, buf(0, 1), &in_bar[gi][0][1], r, r == 64);
+      wait_in(S, 0, 0, S.t);
+      TexPrefetch p0;
+      prefetch_texels<MODE>(mp, a, buf(0, 0), r, lod0, p0);
+      blend_pack(p0, S.zp);
+      S.level = p0.level;
+      tc::mbar_wait(&w_bar, 0);
+      chunk0(buf(0, 0));
+      mma_issue<16, 1, false, 0>(g, Y, X, mp.fast_frame_off, 0, S.bar, NoOp{});
+    }
+    bool has_prev = false, pvalid = false, pup = false;
+    int64_t pq = 0;
+    auto out_prev = [&]() {  // output layer of the previous tile (its L2 D is in D)
+      float y[6];
+      out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
+      if (pvalid) {
+        const V3 f = pup ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
+        stg3(a.rgb, pq, f);
+        if (want_albedo) {
+          const V3 al = pup ? v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f)) : v3(0.f, 0.f, 0.f);
+          stg3(a.albedo, pq, al);
+        }
+      }
+    };
+    while (S.t < ntiles) {
+      const int b = S.it & 1;
+      const int64_t q_in = (int64_t)S.t * kTile + r;
+      const bool valid = q_in < n_rows;
+      const int t2 = S.t + 2 * sstride;
+      // --- stage 0: previous tile's output, this tile's frames -> BRDF layer 1
+      const InBuf<MODE>& ib = buf(0, b);
+      const V3 wi = v3(ib.wi[3 * r], ib.wi[3 * r + 1], ib.wi[3 * r + 2]);
+      const V3 wo = v3(ib.wo[3 * r], ib.wo[3 * r + 1], ib.wo[3 * r + 2]);
+      if (want_level) {
+        if (valid) a.level[SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
+      }
+      if (S.t + sstride < ntiles) {
+        wait_in(S, 0, b ^ 1, S.t + sstride);
+        prefetch_texels<MODE>(mp, a, buf(0, b ^ 1), r, lod0, S.nx);
+      }
+      auto refill = [&]() {
+        if (t2 < last_full) {
+          if (r == 96) stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(0, b), &in_bar[gi][0][b], r, true);
+        } else if (t2 < ntiles) {
+          stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(0, b), &in_bar[gi][0][b], r, false);
+        }
+      };
+      mma_wait<0>(g, S.bar, S.ph);
+      if (has_prev) out_prev();
+      {
+        uint32_t fr[16];
+        tc::tmem_ld16(YL, fr);
+        tc::tmem_ld_wait();
+        float raw[12];
+#pragma unroll
+        for (int j = 0; j < 12; ++j) raw[j] = __uint_as_float(fr[j]);
+        float ti[6], to[6];
+        frames2_transform(raw, wi, wo, ti, to);
+        const uint32_t x[8] = {pack2(ti[0], ti[1]), pack2(ti[2], ti[3]), pack2(ti[4], ti[5]),
+                               pack2(to[0], to[1]), pack2(to[2], to[3]), pack2(to[4], to[5]), 0u, 0u};
+        tc::tmem_st8(XL + 8, x);
+      }
+      mma_issue<BW, 2, false, 1>(g, S.d0, X, mp.fast_l1_off, 0, S.bar, refill);
+      // --- stage 1: hidden epilogue -> BRDF layer 2 (+ next tile's frame layer)
+      mma_wait<1>(g, S.bar, S.ph);
+      hidden_epi<BW>(S.dl, S.al);
+      pq = SEG && a.out_idx && valid ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
+      pvalid = valid;
+      pup = (wi.z > 0.f) && (wo.z > 0.f);
+      has_prev = true;
+      const int tn = S.t + sstride;
+      if (tn < ntiles) {
+        blend_pack(S.nx, S.zp);
+        S.level = S.nx.level;
+        chunk0(buf(0, b ^ 1));
+      }
+      mma_issue_hid_frame<BW, 2 * BW / 16, 2>(g, S.d0, S.a0, mp.layers[mp.brdf_first + 1].b_off, 1,
+                                              tn < ntiles, Y, X, mp.fast_frame_off, S.bar);
+      S.t = tn;
+      S.it += 1;
+    }
+    if (has_prev) {
+      mma_wait<3>(g, S.bar, S.ph);
+      out_prev();
+    }
+  } else {
   // --- prologue: per slot stage tiles 0 and 1, fetch + blend tile 0, issue its first MMA
   sfor<NS>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
@@ -679,6 +812,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       });
     });
   }
+  }  // !kE2
 
   tc::tc_fence_before();
   __syncthreads();

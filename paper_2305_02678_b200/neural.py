@@ -243,7 +243,7 @@ class _QueryInputs:
 
 def _stream_eval(mat, uv, level, wi, wo, u_rr, out):
     """eval_material for a large host batch through nm_eval_host: chunked
-    H2D / fused kernel / D2H overlapped on two internal streams, all in native
+    H2D / fused kernel / D2H overlapped on three internal streams, all in native
     code.  None if not applicable (albedo head, non-contiguous shapes...)."""
     if mat.cfg.albedo_head:
         return None
