@@ -213,6 +213,58 @@ def make_train_case(name="train", seed=41):
     print(name)
 
 
+def make_vertex_case(name="vertex", n=3000, seed=51):
+    """The renderer's per-vertex shading context (render.py:340-420,
+    SURVEY §8 f2) on a two-material scene: material "alpha" (2x32) bound
+    fp16, "beta" (2x16) bound fp32, objects [beta, alpha, beta]; records
+    eval(wi), sample(rng) -> (wi, pdf) and pdf(wi) of the reference's own
+    _VertexShading, plus the inputs and both materials."""
+    geom, latent, neural, proxy = _ref()
+    from types import SimpleNamespace
+    from neuralmat import render
+    d = {}
+    mats = {}
+    for k, (tag, arch) in enumerate((("alpha", "2x32"), ("beta", "2x16"))):
+        cfg = neural.NeuralMaterialConfig(brdf_hidden=arch)
+        mat = neural.NeuralMaterial.create(cfg, np.random.default_rng(seed + 10 * k))
+        lrng = np.random.default_rng(seed + 10 * k + 1)
+        pyr = latent.LatentPyramid.zeros(32, 32)
+        for lvl in pyr.levels:
+            lvl[:] = lrng.standard_normal(lvl.shape).astype(np.float32)
+        mat.latent = pyr
+        mats[tag] = mat
+        d[f"{tag}_config"] = np.array(json.dumps(cfg.to_json()))
+        for i, l in enumerate(pyr.levels):
+            d[f"{tag}_lat{i}"] = l
+        _nets(f"{tag}_frame", mat.frame_layer, d)
+        _nets(f"{tag}_brdf", mat.brdf_decoder, d)
+        _nets(f"{tag}_sampler", mat.sampler_decoder, d)
+    objects = [SimpleNamespace(material=m) for m in ("beta", "alpha", "beta")]
+    materials = {"alpha": render.NeuralBinding(mats["alpha"], fp16=True),
+                 "beta": render.NeuralBinding(mats["beta"], fp16=False)}
+    scene = SimpleNamespace(objects=objects, materials=materials)
+    q = np.random.default_rng(seed + 2)
+    obj = q.integers(0, 3, n)
+    uv = _f32(q.uniform(-0.5, 1.5, (n, 2)))
+    level = _f32(q.random(n) * 5.0).astype(np.float64)
+    wi, wo = geom.sample_half_diff(q, n)
+    wi, wo = _f32(wi).astype(np.float64), _f32(wo).astype(np.float64)
+    hits = SimpleNamespace(obj=obj, uv=uv.astype(np.float64))
+    out = {}
+    for tag, cfg in (("lod", render.RenderConfig(lod=True)),
+                     ("nolod", render.RenderConfig(lod=False)),
+                     ("forced", render.RenderConfig(force_level=2, fp16=True))):
+        rng = np.random.default_rng(seed + 3)
+        ctx = render._VertexShading(scene, cfg, hits, wo, level, rng)
+        f = ctx.eval(wi)
+        ws, pdf_s = ctx.sample(rng)
+        pb = ctx.pdf(wi)
+        out.update({f"{tag}_f": f, f"{tag}_ws": ws, f"{tag}_pdf_ws": pdf_s, f"{tag}_pdf_wi": pb})
+    d.update(obj=obj.astype(np.int64), uv=uv, level=level, wi=wi, wo=wo, rng_seed=np.int64(seed + 3), **out)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     make_case("c1_2x32", {}, n=4096, taps=True, fp32_path=True)
@@ -227,6 +279,7 @@ def main():
     make_archive()
     make_lod_case()
     make_train_case()
+    make_vertex_case()
 
 
 if __name__ == "__main__":
