@@ -200,6 +200,33 @@ int nm_mlp_forward_cached(const nm_mlp* mlp, int64_t batch, const float* x, floa
 int nm_mlp_backward(const nm_mlp* mlp, int64_t batch, void* cache, const float* out_grad,
                     double* dparams, double* dx, void* stream);
 
+/* KL sampler loss (replaces the heads of training.sampler_loss_and_grads,
+ * training.py:219-273, and its default target _brdf_target_and_grad,
+ * training.py:187-216; the three network passes run on nm_mlp_*).  Row
+ * layouts, all device pointers, b = batch:
+ *   nm_kl_sample: raw_s (b, 9 | 2 isotropic) sampler outputs, raw_f (b, 6 nf)
+ *     frame-layer outputs (ignored without frames), z (b, 8), wi (b, 3) f64,
+ *     u_d / u_s (b, 2) f64 -> x2 (2b, in) fp32 BRDF decoder inputs at the
+ *     diffuse (rows [0, b)) and specular (rows [b, 2b)) samples, in = 8 + 6 nf
+ *     (14 without frames); scratch (b, NM_KL_SCRATCH) f64 (samples + aux).
+ *   nm_kl_target: y (2b, out_w) decoder outputs -> target (2b) = lum(f) cos + 1e-4,
+ *     lum (2b), out_grad (2b, out_w) fp32 = d target / d y (columns >= 3 zero).
+ *   nm_kl_target_dir: dx (2b, in) f64 decoder-input gradients -> dtarget (2b, 3).
+ *   nm_kl_grad: target / dtarget (2b ...) -> draw (b, 9 | 2) fp32 = d loss / d raw
+ *     (the batch mean's 1/b included), loss_rows (b) f64 (loss = their mean). */
+#define NM_KL_SCRATCH 17
+int nm_kl_sample(int64_t b, int32_t use_frames, int32_t n_frames, int32_t isotropic, const float* raw_s,
+                 const float* raw_f, const float* z, const double* wi, const double* u_d,
+                 const double* u_s, float* x2_out, double* scratch, void* stream);
+int nm_kl_target(int64_t b, int32_t out_w, const float* y, const double* scratch, double* target_out,
+                 double* lum_out, float* out_grad, void* stream);
+int nm_kl_target_dir(int64_t b, int32_t use_frames, int32_t n_frames, const float* raw_f,
+                     const double* dx, const double* scratch, const double* lum, double* dtarget_out,
+                     void* stream);
+int nm_kl_grad(int64_t b, int32_t isotropic, const float* raw_s, const double* wi,
+               const double* scratch, const double* target, const double* dtarget, float* draw_out,
+               double* loss_rows, void* stream);
+
 /* Level of detail from ray cones (replaces render.footprint_to_level,
  * render.py:334-337, and the footprint in render._surface_frames_and_level,
  * render.py:436-443).  float64 like the reference.

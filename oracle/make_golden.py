@@ -265,6 +265,37 @@ def make_vertex_case(name="vertex", n=3000, seed=51):
     print(name)
 
 
+def make_kl_case(name="kl", b=2048, seed=61):
+    """KL sampler loss (training.py:219-273) from the reference:
+    loss and sampler-decoder gradients with fixed uniforms, for the default
+    material (2 frames), one frame, no frames (vanilla), isotropic sampler
+    and the albedo head (6 decoder outputs)."""
+    geom, latent, neural, proxy = _ref()
+    from neuralmat import training
+    d = {}
+    variants = (("std", {}), ("oneframe", {"n_frames": 1}), ("vanilla", {"use_frames": False}),
+                ("iso", {"sampler_isotropic": True}), ("albedo", {"albedo_head": True}))
+    for k, (tag, kw) in enumerate(variants):
+        cfg = neural.NeuralMaterialConfig(**kw)
+        mat = neural.NeuralMaterial.create(cfg, np.random.default_rng(seed + k))
+        rng = np.random.default_rng(seed + 100 + k)
+        z = _f32(rng.normal(0, 1, (b, 8)))
+        wi, _ = geom.sample_half_diff(rng, b)
+        us = (rng.random((b, 2)), rng.random((b, 2)))
+        loss, grads = training.sampler_loss_and_grads(mat, z, wi, None, us=us)
+        d[f"{tag}_config"] = np.array(json.dumps(cfg.to_json()))
+        _nets(f"{tag}_frame", mat.frame_layer, d)
+        _nets(f"{tag}_brdf", mat.brdf_decoder, d)
+        _nets(f"{tag}_sampler", mat.sampler_decoder, d)
+        d.update({f"{tag}_z": z, f"{tag}_wi": wi, f"{tag}_ud": us[0], f"{tag}_us": us[1],
+                  f"{tag}_loss": np.float64(loss)})
+        for i, (dw, db) in enumerate(grads):
+            d[f"{tag}_dw{i}"] = dw
+            d[f"{tag}_db{i}"] = db
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     make_case("c1_2x32", {}, n=4096, taps=True, fp32_path=True)
@@ -280,6 +311,7 @@ def main():
     make_lod_case()
     make_train_case()
     make_vertex_case()
+    make_kl_case()
 
 
 if __name__ == "__main__":

@@ -19,6 +19,7 @@ NM_ERR_UNSUPPORTED = -3
 NM_MULTI_DIVERGENT = 0
 NM_MULTI_BINNED = 1
 NM_MULTI_BINNED_ASYNC = 2
+NM_KL_SCRATCH = 17  # doubles per row of the KL-loss scratch (include/nmq.h)
 
 c_float_p = ctypes.c_void_p  # device pointers are passed as raw addresses
 c_i64 = ctypes.c_int64
@@ -108,6 +109,10 @@ SIGNATURES = {
                                       ctypes.c_void_p]),
     "nm_mlp_backward": (c_i32, [ctypes.c_void_p, c_i64, ctypes.c_void_p, c_float_p, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_void_p]),
+    "nm_kl_sample": (c_i32, [c_i64, c_i32, c_i32, c_i32] + [ctypes.c_void_p] * 9),
+    "nm_kl_target": (c_i32, [c_i64, c_i32] + [ctypes.c_void_p] * 6),
+    "nm_kl_target_dir": (c_i32, [c_i64, c_i32, c_i32] + [ctypes.c_void_p] * 6),
+    "nm_kl_grad": (c_i32, [c_i64, c_i32] + [ctypes.c_void_p] * 8),
     "nm_footprint_level": (c_i32, [c_i64, ctypes.c_void_p, c_i32, ctypes.c_void_p, ctypes.c_void_p]),
     "nm_cone_level": (c_i32, [c_i64, c_float_p, c_float_p, c_float_p, c_float_p, c_float_p, c_i32,
                               c_i32, c_float_p, ctypes.c_void_p]),

@@ -7,7 +7,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libnmq.so")
-SOURCES = ["nmq_kernels.cu", "nmq_fast.cu", "nmq_warp.cu", "nmq_lod.cu", "nmq_train.cu", "nmq_abi.cu", "nmq_multi.cu"]
+SOURCES = ["nmq_kernels.cu", "nmq_fast.cu", "nmq_warp.cu", "nmq_lod.cu", "nmq_train.cu", "nmq_kl.cu", "nmq_abi.cu", "nmq_multi.cu"]
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-lineinfo",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 

@@ -878,6 +878,55 @@ int nm_mlp_backward(const nm_mlp* m, int64_t batch, void* cache, const float* ou
                 "nm_mlp_backward");
 }
 
+int nm_kl_sample(int64_t b, int32_t use_frames, int32_t n_frames, int32_t isotropic, const float* raw_s,
+                 const float* raw_f, const float* z, const double* wi, const double* u_d,
+                 const double* u_s, float* x2_out, double* scratch, void* stream) {
+  NM_CHECK_N(b);
+  if (b == 0) return NM_OK;
+  if (!raw_s || !z || !wi || !u_d || !u_s || !x2_out || !scratch || (use_frames && !raw_f))
+    return fail(NM_ERR_INVALID, "null input");
+  if (use_frames && (n_frames < 1 || n_frames > 4)) return fail(NM_ERR_UNSUPPORTED, "1..4 frames");
+  return finish(nullptr, launch_kl_sample(b, use_frames != 0, n_frames, isotropic != 0, raw_s, raw_f, z,
+                                          wi, u_d, u_s, x2_out, scratch, (cudaStream_t)stream),
+                "nm_kl_sample");
+}
+
+int nm_kl_target(int64_t b, int32_t out_w, const float* y, const double* scratch, double* target_out,
+                 double* lum_out, float* out_grad, void* stream) {
+  NM_CHECK_N(b);
+  if (b == 0) return NM_OK;
+  if (!y || !scratch || !target_out || !lum_out || !out_grad) return fail(NM_ERR_INVALID, "null input");
+  if (out_w < 3) return fail(NM_ERR_INVALID, "decoder output narrower than 3");
+  return finish(nullptr, launch_kl_target(b, out_w, y, scratch, target_out, lum_out, out_grad,
+                                          (cudaStream_t)stream),
+                "nm_kl_target");
+}
+
+int nm_kl_target_dir(int64_t b, int32_t use_frames, int32_t n_frames, const float* raw_f,
+                     const double* dx, const double* scratch, const double* lum, double* dtarget_out,
+                     void* stream) {
+  NM_CHECK_N(b);
+  if (b == 0) return NM_OK;
+  if (!dx || !scratch || !lum || !dtarget_out || (use_frames && !raw_f))
+    return fail(NM_ERR_INVALID, "null input");
+  if (use_frames && (n_frames < 1 || n_frames > 4)) return fail(NM_ERR_UNSUPPORTED, "1..4 frames");
+  return finish(nullptr, launch_kl_target_dir(b, use_frames != 0, n_frames, raw_f, dx, scratch, lum,
+                                              dtarget_out, (cudaStream_t)stream),
+                "nm_kl_target_dir");
+}
+
+int nm_kl_grad(int64_t b, int32_t isotropic, const float* raw_s, const double* wi,
+               const double* scratch, const double* target, const double* dtarget, float* draw_out,
+               double* loss_rows, void* stream) {
+  NM_CHECK_N(b);
+  if (b == 0) return NM_OK;
+  if (!raw_s || !wi || !scratch || !target || !dtarget || !draw_out || !loss_rows)
+    return fail(NM_ERR_INVALID, "null input");
+  return finish(nullptr, launch_kl_grad(b, isotropic != 0, raw_s, wi, scratch, target, dtarget, draw_out,
+                                        loss_rows, (cudaStream_t)stream),
+                "nm_kl_grad");
+}
+
 int nm_footprint_level(int64_t n, const double* area_texels, int32_t n_levels, double* level_out,
                        void* stream) {
   NM_CHECK_N(n);

@@ -152,6 +152,17 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
                                 const float* wts, int32_t w_floats, int64_t B, const float* x_cache,
                                 const float* pre_cache, const float* out_grad, double* g_cache,
                                 double* dparams, double* dx, cudaStream_t s);
+// KL sampler-loss heads (nmq_kl.cu)
+cudaError_t launch_kl_sample(int64_t b, int frames, int nf, int iso, const float* raw_s,
+                             const float* raw_f, const float* z, const double* wi, const double* u_d,
+                             const double* u_s, float* x2, double* scr, cudaStream_t st);
+cudaError_t launch_kl_target(int64_t b, int out_w, const float* y, const double* scr, double* tgt,
+                             double* lum, float* og, cudaStream_t st);
+cudaError_t launch_kl_target_dir(int64_t b, int frames, int nf, const float* raw_f, const double* dx,
+                                 const double* scr, const double* lum, double* dtgt, cudaStream_t st);
+cudaError_t launch_kl_grad(int64_t b, int iso, const float* raw_s, const double* wi, const double* scr,
+                           const double* tgt, const double* dtgt, float* draw, double* loss_rows,
+                           cudaStream_t st);
 // level of detail from ray cones (nmq_lod.cu)
 cudaError_t launch_footprint_level(int64_t n, const double* area, int32_t n_levels, double* out,
                                    cudaStream_t s);

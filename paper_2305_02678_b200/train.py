@@ -7,6 +7,9 @@ network engine and latent-gradient scatter used by its offline baking loop
   float32 forward, float64 reverse chain (the reference promotes to float64
   at its first leaky layer), dW = g^T x and db = sum g reduced over the
   batch on the GPU (csrc/nmq_train.cu).
+* ``sampler_loss_and_grads(mat, z, wi, rng, target_and_grad=None, us=None)``
+  — the KL sampler loss (training.py:219-273): network passes on the fp32
+  engine, float64 per-row heads in csrc/nmq_kl.cu.
 * ``accumulate_texel_grads(pyramid, grad_levels, uv, chosen, z_grad)`` —
   ``LatentPyramid.accumulate_texel_grads`` (latent.py:109-119): the exact
   adjoint of the fetch, scattered with atomics; adds into ``grad_levels``
@@ -178,6 +181,86 @@ def accumulate_texel_grads(pyramid, grad_levels, uv, chosen, z_grad):
             g[...] = host[o:o + k].reshape(g.shape)
             o += k
     return grad_levels
+
+
+def sampler_loss_and_grads(mat, z, wi, rng, target_and_grad=None, us=None):
+    """KL-style sampler loss and its gradients for the sampler decoder —
+    reference training.sampler_loss_and_grads (training.py:219-273) with the
+    default target _brdf_target_and_grad (training.py:187-216).
+
+    Returns (loss, grads), grads in Mlp.backward's layout.  The three network
+    passes (sampler forward, BRDF decoder forward + input backward at the 2B
+    samples, sampler backward) run on the fp32 network engine; the per-row
+    heads (proxy, the two lobe samples, the luminance target and its
+    direction derivative through the frames, grad log pdf, the sample and raw
+    Jacobians) are float64 CUDA kernels (csrc/nmq_kl.cu).  `us` fixes the
+    two (b, 2) uniform draws, else they come from `rng` in the reference's
+    order; `target_and_grad(wo) -> (f (b,), df (b, 3))` replaces the default
+    target (called on host arrays, like the reference's gradient oracles).
+    numpy in -> numpy out (float64 loss, the reference's gradient dtypes)."""
+    cfg = mat.cfg
+    if cfg.channels != LATENT_CHANNELS:
+        raise NotImplementedError("the GPU sampler loss handles 8-channel latents")
+    np_mode = _io.is_numpy_like(z)
+    dev = _io.cuda_device(None if np_mode else z.device)
+    if np_mode:
+        z64 = np.atleast_2d(np.asarray(z, np.float64))
+        wi64 = np.atleast_2d(np.asarray(wi, np.float64))
+        zt = torch.from_numpy(np.ascontiguousarray(z64, np.float32)).to(dev)
+        wit = torch.from_numpy(np.ascontiguousarray(wi64)).to(dev)
+    else:
+        zt = z.to(dev, torch.float32).reshape(-1, LATENT_CHANNELS).contiguous()
+        wit = (wi if isinstance(wi, torch.Tensor) else torch.as_tensor(np.asarray(wi, np.float64))) \
+            .to(dev, torch.float64).reshape(-1, 3).contiguous()
+    b = zt.shape[0]
+    if wit.shape[0] != b or zt.shape[1] != LATENT_CHANNELS:
+        raise ValueError("z must be (b, 8) and wi (b, 3)")
+    iso = bool(cfg.sampler_isotropic)
+    lib = _lib.load()
+    st = _io.stream_ptr(dev)
+    inp = torch.cat([zt.double(), wit], 1).float().contiguous()
+    raw, cache = forward_cached(mat.sampler_decoder, inp)
+    u_d, u_s = us if us is not None else (rng.random((b, 2)), rng.random((b, 2)))
+    ud = torch.as_tensor(np.ascontiguousarray(u_d, np.float64)).to(dev)
+    us_t = torch.as_tensor(np.ascontiguousarray(u_s, np.float64)).to(dev)
+    frames = bool(cfg.use_frames)
+    nf = int(cfg.n_frames) if frames else 0
+    raw_f = forward_cached(mat.frame_layer, zt)[0] if frames else None
+    in_w = LATENT_CHANNELS + (6 * nf if frames else 6)
+    x2 = torch.empty((2 * b, in_w), device=dev, dtype=torch.float32)
+    scr = torch.empty((b, _lib.NM_KL_SCRATCH), device=dev, dtype=torch.float64)
+    _lib.check(lib.nm_kl_sample(b, int(frames), nf, int(iso), raw.data_ptr(), _io.ptr(raw_f), zt.data_ptr(),
+                                wit.data_ptr(), ud.data_ptr(), us_t.data_ptr(), x2.data_ptr(), scr.data_ptr(),
+                                st), "nm_kl_sample")
+    if target_and_grad is None:
+        y, cache_b = forward_cached(mat.brdf_decoder, x2)
+        out_w = y.shape[1]
+        tgt = torch.empty(2 * b, device=dev, dtype=torch.float64)
+        lum = torch.empty(2 * b, device=dev, dtype=torch.float64)
+        og = torch.empty((2 * b, out_w), device=dev, dtype=torch.float32)
+        _lib.check(lib.nm_kl_target(b, out_w, y.data_ptr(), scr.data_ptr(), tgt.data_ptr(), lum.data_ptr(),
+                                    og.data_ptr(), st), "nm_kl_target")
+        _, dx = backward(mat.brdf_decoder, cache_b, og)
+        dtgt = torch.empty((2 * b, 3), device=dev, dtype=torch.float64)
+        _lib.check(lib.nm_kl_target_dir(b, int(frames), nf, _io.ptr(raw_f), dx.data_ptr(), scr.data_ptr(),
+                                        lum.data_ptr(), dtgt.data_ptr(), st), "nm_kl_target_dir")
+    else:
+        host = scr.cpu().numpy()
+        f_d, df_d = target_and_grad(host[:, 0:3])
+        f_s, df_s = target_and_grad(host[:, 3:6])
+        tgt = torch.from_numpy(np.concatenate([np.asarray(f_d, np.float64).reshape(-1),
+                                               np.asarray(f_s, np.float64).reshape(-1)])).to(dev)
+        dtgt = torch.from_numpy(np.ascontiguousarray(np.concatenate(
+            [np.asarray(df_d, np.float64).reshape(-1, 3), np.asarray(df_s, np.float64).reshape(-1, 3)]))).to(dev)
+    draw = torch.empty((b, 2 if iso else 9), device=dev, dtype=torch.float32)
+    rows = torch.empty(b, device=dev, dtype=torch.float64)
+    _lib.check(lib.nm_kl_grad(b, int(iso), raw.data_ptr(), wit.data_ptr(), scr.data_ptr(), tgt.data_ptr(),
+                              dtgt.data_ptr(), draw.data_ptr(), rows.data_ptr(), st), "nm_kl_grad")
+    loss = float(np.mean(rows.cpu().numpy()))
+    grads, _ = backward(mat.sampler_decoder, cache, draw)
+    if np_mode:
+        grads = [(dw.cpu().numpy(), db.cpu().numpy()) for dw, db in grads]
+    return loss, grads
 
 
 # drop-in methods, as on the reference's classes

@@ -33,7 +33,7 @@ def pytest_collection_modifyitems(config, items):
             it.add_marker(skip)
 
 
-def golden_cases(pattern="*.npz", exclude=("proxy_kat", "lod", "train", "vertex")):
+def golden_cases(pattern="*.npz", exclude=("proxy_kat", "lod", "train", "vertex", "kl")):
     names = sorted(os.path.splitext(os.path.basename(p))[0]
                    for p in glob.glob(os.path.join(GOLDEN, pattern)))
     return [n for n in names if n not in exclude]
