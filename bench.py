@@ -533,11 +533,61 @@ def run_train(args):
         }))
 
 
+def run_kl(args):
+    """SURVEY §8 f4, not the headline: the KL sampler loss + sampler-decoder
+    gradients (training.py:219-273) on 65,536 rows of the default 2x32
+    material (sampler forward, BRDF forward + input backward at both lobe
+    samples, the float64 heads, sampler backward) — rows/s, the loss read
+    back every step; the numpy oracle (the reference's algorithm) beside it."""
+    rank, world, local = dist_init(args.gpus)
+    device = torch.device("cuda", local)
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import synth, train
+    B = 65536
+    mat = synth.material("2x32", 64, 64, seed=0, device=device)
+    g = torch.Generator(device=device)
+    g.manual_seed(7 + rank)
+    z = torch.randn((B, 8), device=device, generator=g)
+    q = synth.queries(B, 1, seed=2 + rank, device=device)
+    wi = q["wi"].double()
+    us = (torch.rand((B, 2), device=device, generator=g, dtype=torch.float64),
+          torch.rand((B, 2), device=device, generator=g, dtype=torch.float64))
+    stream = torch.cuda.current_stream(device)
+
+    def step(i):
+        train.sampler_loss_and_grads(mat, z, wi, None, us=us)
+
+    steps = max(5, args.steps // 100)
+    ms = _time_loop(step, steps, args.warmup, stream, world)
+    n_cpu = 8192
+    om = O.Material(O.Config(), O.Net([(l.w, l.b, l.act) for l in mat.frame_layer.layers]),
+                    O.Net([(l.w, l.b, l.act) for l in mat.brdf_decoder.layers]),
+                    O.Net([(l.w, l.b, l.act) for l in mat.sampler_decoder.layers]))
+    zh, wih = z[:n_cpu].cpu().numpy(), wi[:n_cpu].cpu().numpy()
+    ush = tuple(u[:n_cpu].cpu().numpy() for u in us)
+    t0 = time.perf_counter()
+    O.sampler_loss_and_grads(om, zh, wih, ush)
+    t_cpu = time.perf_counter() - t0
+    if rank == 0:
+        print(json.dumps({
+            "metric": "KL sampler-loss rows/s (loss + sampler-decoder gradients)",
+            "value": B * world / (ms / 1e3), "unit": "rows/s", "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "fp32 networks, f64 heads / backward chains",
+            "data": "synthetic: random-init 2x32 material, N(0,1) codes, half-diff directions",
+            "config": {"workload": "kl (SURVEY §8 f4, training.py:219-273)", "rows": B},
+            "cpu_baseline": {"value": n_cpu / t_cpu, "unit": "rows/s", "cores": 1, "kind": "port",
+                             "sample": f"{n_cpu} rows, oracle.sampler_loss_and_grads (numpy, 1 core)"},
+        }))
+
+
 def run_ours(args):
     if args.workload == "c4":
         return run_c4(args)
     if args.workload == "train":
         return run_train(args)
+    if args.workload == "kl":
+        return run_kl(args)
     if args.workload == "c5":
         return run_c5(args)
     rank, world, local = dist_init(args.gpus)
@@ -713,7 +763,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["c2", "c3", "full", "c4", "c5", "train"], default="c2")
+    ap.add_argument("--workload", choices=["c2", "c3", "full", "c4", "c5", "train", "kl"], default="c2")
     ap.add_argument("--sets", type=int, default=3)
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-sample", type=int, default=C2_N)

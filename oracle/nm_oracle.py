@@ -672,3 +672,155 @@ def cone_level(cone_w, cone_s, t, cos_hit, density, n_levels):
     diam = width / np.maximum(np.abs(np.asarray(cos_hit, np.float64)), 0.05)
     area = (diam * np.asarray(density, np.float64)) ** 2
     return footprint_to_level(area, n_levels)
+
+
+# ---------------------------------------------------------------------------
+# KL sampler loss (training.py:187-273) — SURVEY §8 f4
+
+EPS_KL = 1e-4                                  # training.py:45
+LUM_WEIGHTS = np.array([0.2126, 0.7152, 0.0722])  # training.py:46
+_TINY = 1e-30                                  # training.py:47
+
+
+def _quad_tanh_grad(x):
+    """neural.py:53-56"""
+    ax = np.abs(x)
+    den = 1.0 + ax + 0.5 * x * x
+    return (1.0 + ax) / (den * den)
+
+
+def _kl_target(mat, z, wi, wo):
+    """training.py:187-216: lum(f) cos(theta_o) + eps and its wo-derivative
+    (frames and decoder supply values and direction derivatives only)."""
+    up = wo[:, 2] > 0.0
+    woz = np.maximum(wo[:, 2], 0.0)
+    if mat.cfg.use_frames:
+        fr = frames_from_raw(mat.frame.forward(z.astype(np.float32)))
+        inp = np.concatenate([z, frame_transform(fr, wi), frame_transform(fr, wo)], -1)
+    else:
+        fr = None
+        inp = np.concatenate([z, wi, wo], -1)
+    y, cache = forward_cached(mat.brdf, inp.astype(np.float32))
+    y = np.asarray(y, np.float64)
+    lum = brdf_output(y[:, 0:3]) @ LUM_WEIGHTS
+    target = np.where(up, lum * woz, 0.0) + EPS_KL
+    og = np.zeros_like(y, dtype=np.float32)
+    og[:, 0:3] = (LUM_WEIGHTS * np.where(y[:, 0:3] > 0.0, np.exp(np.minimum(y[:, 0:3], 60.0)), 0.0)
+                  * woz[:, None]).astype(np.float32)
+    _, din = backward(mat.brdf, cache, og)
+    din = np.asarray(din, np.float64)
+    c = z.shape[1]
+    if fr is not None:  # neural.py:198-205 transform adjoint on the wo block
+        nf = mat.cfg.n_frames
+        g = din[:, c + 3 * nf:].reshape(-1, nf, 3)
+        t, b, n = fr
+        dt = np.sum(g[..., 0:1] * t + g[..., 1:2] * b + g[..., 2:3] * n, axis=1)
+    else:
+        dt = din[:, c + 3:]
+    dt = dt + lum[:, None] * np.array([0.0, 0.0, 1.0])
+    return target, np.where(up[:, None], dt, 0.0)
+
+
+def _grad_log_pdf(p, wi, wo):
+    """proxy.py:203-250: (p, d log p / d wo), subgradient 0 at the kinks."""
+    nd = p.diffuse_axis()
+    dn = np.sum(wo * nd, -1)
+    pd = np.maximum(dn, 0.0) / np.pi
+    dpd = np.where((dn > 0.0)[:, None], nd / np.pi, 0.0)
+    hs = wi + wo
+    hl = np.linalg.norm(hs, axis=-1)
+    ok = hl > 1e-9
+    h = hs / np.maximum(hl, 1e-12)[:, None]
+    flip = np.where(h[:, 2] < 0.0, -1.0, 1.0)
+    h = h * flip[:, None]
+    hz = ok & (h[:, 2] > 0.0)
+    q = _inverse_warp(p, h)
+    qn2 = np.maximum(np.sum(q * q, -1), _TINY)
+    coh = np.sum(wo * h, -1)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        ps = np.where(hz, h[:, 2] / (p.det() * 4.0 * np.pi * qn2 * qn2 * np.maximum(np.abs(coh), 1e-12)), 0.0)
+    ax, ay, s, rho = p.alpha[:, 0], p.alpha[:, 1], p.s, p.rho
+    mtq = np.stack([q[:, 0] / ax - q[:, 1] * rho / (ax * s), q[:, 1] / (ay * s),
+                    q[:, 0] * p.mu_s[:, 0] / ax
+                    + q[:, 1] * (p.mu_s[:, 1] / (ay * s) - p.mu_s[:, 0] * rho / (ax * s)) + q[:, 2]], -1)
+    inv_coh = np.where(np.abs(coh) < 1e-12, 0.0, 1.0 / np.where(coh == 0.0, 1.0, coh))
+    dlog_dh = (np.stack([0 * ps, 0 * ps, 1.0 / np.maximum(h[:, 2], 1e-12)], -1)
+               - 4.0 * mtq / qn2[:, None] - wo * inv_coh[:, None])
+    proj = dlog_dh - h * np.sum(h * dlog_dh, -1)[:, None]
+    dlog_ps = flip[:, None] * proj / np.maximum(hl, 1e-12)[:, None] - h * inv_coh[:, None]
+    dps = np.where(hz[:, None], ps[:, None] * dlog_ps, 0.0)
+    pm = p.wd * pd + p.ws * ps
+    dp = p.wd[:, None] * dpd + p.ws[:, None] * dps
+    return pm, dp / np.maximum(pm, _TINY)[:, None]
+
+
+def sampler_loss_and_grads(mat, z, wi, us):
+    """training.py:219-273 with the default target and fixed uniforms
+    us = (u_d, u_s): the reparameterized KL estimate over both lobes and
+    the sampler decoder's gradients -> (loss, [(dW, db), ...])."""
+    z = np.atleast_2d(np.asarray(z, np.float64))
+    wi = np.atleast_2d(np.asarray(wi, np.float64))
+    b = z.shape[0]
+    iso = mat.cfg.sampler_isotropic
+    raw, cache = forward_cached(mat.sampler, np.concatenate([z, wi], -1).astype(np.float32))
+    raw = np.asarray(raw, np.float64)
+    p = proxy_from_raw(raw, isotropic=iso)
+    u_d, u_s = (np.asarray(u, np.float64) for u in us)
+    # samples + aux (proxy.py:149-165)
+    v = uniform_sphere(u_d)
+    nd = p.diffuse_axis()
+    g = nd + v
+    gl = np.maximum(np.linalg.norm(g, axis=-1), 1e-9)
+    wo_d = g / gl[:, None]
+    m = ndf_sample(u_s)
+    gs = np.einsum("bij,bj->bi", p.warp(), m)
+    gls = np.linalg.norm(gs, axis=-1)
+    h = gs / np.maximum(gls, 1e-12)[:, None]
+    wo_s = _mirror(wi, h)
+    f_d, df_d = _kl_target(mat, z, wi, wo_d)
+    f_s, df_s = _kl_target(mat, z, wi, wo_s)
+    p_d, dl_d = _grad_log_pdf(p, wi, wo_d)
+    p_s, dl_s = _grad_log_pdf(p, wi, wo_s)
+    ell_d = np.log(np.maximum(p_d, _TINY)) - np.log(f_d)
+    ell_s = np.log(np.maximum(p_s, _TINY)) - np.log(f_s)
+    loss = float(np.mean(p.wd * ell_d + p.ws * ell_s))
+    brk_d = dl_d - df_d / f_d[:, None]
+    brk_s = dl_s - df_s / f_s[:, None]
+    # d wo / d mu_d (proxy.py:253-266)
+    vlen = np.sqrt(1.0 + np.sum(p.mu_d ** 2, -1))
+    g_mu_d = np.empty((b, 2))
+    for k in range(2):
+        e = np.zeros_like(nd)
+        e[:, k] = -1.0
+        dnd = (e - nd * np.sum(nd * e, -1)[:, None]) / vlen[:, None]
+        dwo = (dnd - wo_d * np.sum(wo_d * dnd, -1)[:, None]) / gl[:, None]
+        g_mu_d[:, k] = p.wd * np.sum(brk_d * dwo, -1)
+    # d wo / d (ax, ay, rho, msx, msy) (proxy.py:269-282)
+    ay, s, rho = p.alpha[:, 1], p.s, p.rho
+    dg = np.zeros((b, 3, 5))
+    dg[:, 0, 0] = m[:, 0]
+    dg[:, 1, 1] = rho * m[:, 0] + s * m[:, 1]
+    dg[:, 1, 2] = ay * (m[:, 0] - rho * m[:, 1] / s)
+    dg[:, 0, 3] = -m[:, 2]
+    dg[:, 1, 4] = -m[:, 2]
+    dh = (dg - h[..., None] * np.sum(h[..., None] * dg, 1)[:, None, :]) / gls[:, None, None]
+    js = 2.0 * h[..., None] * np.sum(wi[..., None] * dh, 1)[:, None, :] \
+        + 2.0 * np.sum(wi * h, -1)[:, None, None] * dh
+    g_spec = p.ws[:, None] * np.einsum("bi,bik->bk", brk_s, js)
+    # raw-output Jacobian (neural.py:334-350)
+    draw = np.zeros_like(raw)
+    if iso:
+        draw[:, 0] = (ell_d - ell_s) * 0.5 * _quad_tanh_grad(raw[:, 0])
+        draw[:, 1] = (g_spec[:, 0] + g_spec[:, 1]) * 0.5 * _quad_tanh_grad(raw[:, 1])
+    else:
+        wd, ws = softmax_pair(raw[:, RAW_WD], raw[:, RAW_WS])
+        sj = wd * ws
+        draw[:, 0] = (ell_d - ell_s) * sj
+        draw[:, 3] = (ell_s - ell_d) * sj
+        draw[:, 1:3] = g_mu_d * (1.0 + 0.5 * raw[:, 1:3] ** 2)
+        draw[:, 4:6] = g_spec[:, 0:2] * 0.5 * _quad_tanh_grad(raw[:, 4:6])
+        draw[:, 6] = g_spec[:, 2] * _quad_tanh_grad(raw[:, 6])
+        draw[:, 7:9] = g_spec[:, 3:5] * (1.0 + 0.5 * raw[:, 7:9] ** 2)
+    draw /= b
+    grads, _ = backward(mat.sampler, cache, draw.astype(np.float32))
+    return loss, grads

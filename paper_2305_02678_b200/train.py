@@ -221,8 +221,8 @@ def sampler_loss_and_grads(mat, z, wi, rng, target_and_grad=None, us=None):
     inp = torch.cat([zt.double(), wit], 1).float().contiguous()
     raw, cache = forward_cached(mat.sampler_decoder, inp)
     u_d, u_s = us if us is not None else (rng.random((b, 2)), rng.random((b, 2)))
-    ud = torch.as_tensor(np.ascontiguousarray(u_d, np.float64)).to(dev)
-    us_t = torch.as_tensor(np.ascontiguousarray(u_s, np.float64)).to(dev)
+    ud, us_t = ((u.to(dev, torch.float64).contiguous() if isinstance(u, torch.Tensor)
+                 else torch.from_numpy(np.ascontiguousarray(u, np.float64)).to(dev)) for u in (u_d, u_s))
     frames = bool(cfg.use_frames)
     nf = int(cfg.n_frames) if frames else 0
     raw_f = forward_cached(mat.frame_layer, zt)[0] if frames else None

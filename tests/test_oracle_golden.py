@@ -128,3 +128,25 @@ def test_training_side_oracle_matches_reference():
     pyr.accumulate_texel_grads(levels, g["tg_uv"].astype(np.float64), g["tg_level"], g["tg_zgrad"])
     for i, l in enumerate(levels):
         assert np.array_equal(l, g[f"tg_grad{i}"])
+
+
+@pytest.mark.parametrize("tag", ["std", "oneframe", "vanilla", "iso", "albedo"])
+def test_kl_sampler_loss_oracle_matches_reference(tag):
+    """oracle.sampler_loss_and_grads against the reference's own
+    training.sampler_loss_and_grads (tests/golden/kl.npz)."""
+    import json
+    g = load_golden("kl")
+    cfg = O.Config(**json.loads(str(g[f"{tag}_config"])))
+
+    def net(prefix):
+        n = int(g[f"{tag}_{prefix}_n"])
+        return O.Net([(g[f"{tag}_{prefix}_w{i}"], g[f"{tag}_{prefix}_b{i}"],
+                       O.ACT_LINEAR if int(g[f"{tag}_{prefix}_a{i}"]) == 0 else O.ACT_LEAKY)
+                      for i in range(n)]) if n else None
+
+    mat = O.Material(cfg, net("frame"), net("brdf"), net("sampler"))
+    loss, grads = O.sampler_loss_and_grads(mat, g[f"{tag}_z"], g[f"{tag}_wi"], (g[f"{tag}_ud"], g[f"{tag}_us"]))
+    assert abs(loss - float(g[f"{tag}_loss"])) <= 1e-12 * abs(float(g[f"{tag}_loss"]))
+    for i, (dw, db) in enumerate(grads):
+        for a, want in ((dw, g[f"{tag}_dw{i}"]), (db, g[f"{tag}_db{i}"])):
+            assert np.abs(a - want).max() <= 1e-6 * np.abs(want).max() + 1e-12
