@@ -168,11 +168,14 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   void* stream);
 
 /* --- misc -------------------------------------------------------------- */
-/* nm_eval with HOST buffers (pinned for full PCIe overlap; pageable works):
- * the batch streams through the GPU in `chunk`-query pieces (0 = 512k) on two
- * internal streams, H2D / fused kernel / D2H overlapped; blocking (rgb_out is
- * complete on return); ordered after prior work on `stream`.  The reference
- * call it replaces is eval_material on numpy arrays (neural.py:303). */
+/* nm_eval with HOST buffers; blocking (rgb_out is complete on return),
+ * ordered after prior work on `stream`.  All buffers pinned (page-locked):
+ * zero-copy, one fused launch reading the inputs and writing rgb over PCIe
+ * (`chunk` unused; env NMQ_HOST_ZEROCOPY=0 disables).  Otherwise the batch
+ * streams through device staging in `chunk`-query pieces (0 = 512k): one
+ * stream for the H2D copies, one for the kernels, one for the D2H copies.
+ * The reference call it replaces is eval_material on numpy arrays
+ * (neural.py:303). */
 int nm_eval_host(const nm_material* mat, int64_t n, const float* uv, const float* lod,
                  int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
                  float* rgb_out, int64_t chunk, void* stream);
