@@ -36,5 +36,30 @@ net = mlp.Mlp.create((20, 32, 32, 3), rng)
 out, cache = train.forward_cached(net, rng.normal(size=(n, 20)).astype(np.float32))
 train.backward(net, cache, rng.normal(size=(n, 3)).astype(np.float32))
 mat.latent.accumulate_texel_grads(mat.latent.zero_grads(), uv, np.zeros(n, np.int64), rng.normal(size=(n, 8)).astype(np.float32))
+# KL sampler loss (std + isotropic)
+for cfg in (neural.NeuralMaterialConfig(), neural.NeuralMaterialConfig(sampler_isotropic=True)):
+    km = neural.NeuralMaterial.create(cfg, rng)
+    train.sampler_loss_and_grads(km, rng.normal(size=(n, 8)).astype(np.float32), wi.astype(np.float64), rng)
+# per-vertex shading context (two materials)
+from types import SimpleNamespace
+scene = SimpleNamespace(objects=[SimpleNamespace(material="a"), SimpleNamespace(material="b")],
+                        materials={"a": render.NeuralBinding(mats[0], fp16=True),
+                                   "b": render.NeuralBinding(mats[1], fp16=False)})
+ctx = render.VertexShading(scene, SimpleNamespace(lod=True, force_level=None, fp16=False),
+                           SimpleNamespace(obj=ids, uv=uv), wo, lod, rng)
+ctx.eval(wi); ctx.sample(rng); ctx.pdf(wi)
+# host-buffer eval: zero-copy (pinned) and staged (pageable) paths
+import ctypes
+from paper_2305_02678_b200 import _lib, _io
+lib = _lib.load()
+h = mat.device_material(None)
+pin = {k: torch.from_numpy(v).pin_memory() for k, v in (("uv", uv), ("lod", lod), ("urr", urr), ("wi", wi), ("wo", wo))}
+rgb_pin = torch.empty((n, 3)).pin_memory()
+rgb_pg = np.empty((n, 3), np.float32)
+for src, dst in ((pin, rgb_pin.data_ptr()), ({"uv": uv, "lod": lod, "urr": urr, "wi": wi, "wo": wo}, rgb_pg.ctypes.data)):
+    ptr = {k: (v.data_ptr() if isinstance(v, torch.Tensor) else v.ctypes.data) for k, v in src.items()}
+    _lib.check(lib.nm_eval_host(h.ptr, n, ptr["uv"], ptr["lod"], 1, ptr["urr"], ptr["wi"], ptr["wo"], dst,
+                                256, _io.stream_ptr(h.device)))
+assert np.array_equal(rgb_pin.numpy(), rgb_pg)
 torch.cuda.synchronize()
 print("sanitize_run ok")
