@@ -55,6 +55,9 @@ using namespace dev;
 #ifndef NMQ_G_QUERY
 #define NMQ_G_QUERY 5
 #endif
+#ifndef NMQ_EVAL_OUT_MMA
+#define NMQ_EVAL_OUT_MMA 0  // eval: BRDF output layer on the tensor core (see kOM)
+#endif
 #ifndef NMQ_EVAL2
 #define NMQ_EVAL2 0  // eval in two stages per tile (see kE2)
 #endif
@@ -427,9 +430,13 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   // 32 more TMEM columns per group (X: next tile's input chunks, Y: its
   // frame-layer D)
   constexpr bool kE2 = NMQ_EVAL2 && MODE == kModeEval && NS == 1 && BNH == 2 && !TS;
+  // eval (NMQ_EVAL_OUT_MMA): the BRDF output layer on the tensor core too
+  // (hi/lo split of the last hidden layer, N = 16 MMA, read back one stage later)
+  constexpr bool kOM = NMQ_EVAL_OUT_MMA && MODE == kModeEval && !kE2;
   constexpr int kOutB = kBrdf ? BNH : -1;                   // BRDF output stage
+  constexpr int kOutR = kOM ? BNH + 1 : kOutB;              // BRDF output read back
   constexpr int kS0 = kBrdf ? (kQM ? BNH : BNH + 1) : 0;    // stage issuing sampler layer 2
-  constexpr int kFinal = kSamp ? kS0 + SNH : kOutB;         // last stage
+  constexpr int kFinal = kSamp ? kS0 + SNH : kOutR;         // last stage
   constexpr int kStages = kFinal + 1;
   constexpr int DW = BW > SW ? BW : SW;
   static_assert(DW >= 32, "frame-layer D aliases A columns [16, 32)");
@@ -741,6 +748,31 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           hidden_epi<BW>(S.dl, S.al);
           mma_issue<BW, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + k].b_off, k,
                                                S.bar, NoOp{});
+        } else if constexpr (kOM && k == kOutB) {
+          // BRDF output layer on the tensor core: last hidden layer -> A, N = 16 MMA
+          wait_mma();
+          hidden_epi<BW>(S.dl, S.al);
+          mma_issue<16, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + BNH].b_off, BNH,
+                                               S.bar, NoOp{});
+        } else if constexpr (kOM && k == kOutR) {
+          wait_mma();
+          uint32_t yr[8];
+          tc::tmem_ld8(S.dl, yr);
+          tc::tmem_ld_wait();
+          float y[6];
+#pragma unroll
+          for (int j = 0; j < 6; ++j) y[j] = __uint_as_float(yr[j]) * fc.inv_brdf;
+          if (valid) {
+            const int64_t q = SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
+            const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
+                              : v3(0.f, 0.f, 0.f);
+            stg3(a.rgb, q, f);
+            if (want_albedo) {
+              const V3 al = S.up ? v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f))
+                                 : v3(0.f, 0.f, 0.f);
+              stg3(a.albedo, q, al);
+            }
+          }
         } else if constexpr (k == kOutB) {
           // BRDF output layer on the CUDA cores
           wait_mma();

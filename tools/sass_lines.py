@@ -35,7 +35,7 @@ for l in dis.splitlines():
 tot = sum(v[0] for v in out.values())
 print(f"total lane-instr/query {tot*32/nq:.1f}")
 src = {}
-for (f, ln), (e, w) in sorted(out.items(), key=lambda kv: -kv[1][0])[:45]:
+for (f, ln), (e, w) in sorted(out.items(), key=lambda kv: -kv[1][0])[:int(sys.argv[5]) if len(sys.argv) > 5 else 45]:
     if f not in src:
         try:
             src[f] = open(subprocess.run(["bash", "-c", f"ls paper_2305_02678_b200/csrc/{f}"], capture_output=True, text=True).stdout.strip()).read().splitlines()
