@@ -69,6 +69,13 @@ using namespace dev;
 #define NMQ_BIAS_SMEM 0
 #endif
 constexpr bool kBiasSmem = NMQ_BIAS_SMEM != 0;
+// MMA issue: each warp arrives on an issue mbarrier (bar + 1, count 4) after
+// its TMEM stores; only the issuing thread (and the TMA-refill thread)
+// waits, instead of a 128-thread named barrier.
+#ifndef NMQ_ISS_MBAR
+#define NMQ_ISS_MBAR 0
+#endif
+constexpr bool kIssMbar = NMQ_ISS_MBAR != 0;
 constexpr uint32_t kBiasTile = 4096;  // bytes per bias depth (128 rows x K 16 fp16)
 #ifndef NMQ_EVAL_OUT_MMA
 #define NMQ_EVAL_OUT_MMA 0  // eval: BRDF output layer on the tensor core (see kOM)
@@ -179,12 +186,26 @@ __device__ __forceinline__ void bias_mma(const GG& g, uint32_t d_tmem, int j, ui
 // at the group barrier; lane 0 of warp LW issues KA k-steps of A (TMEM) x B
 // (SMEM weights at b_off), + the bias chunk when HID, and commits to `bar`.
 // `hook` then runs on every thread (TMA refills after the barrier).
-template <int N, int KA, bool HID, int LW, class F>
-__device__ __forceinline__ void mma_issue(const GG& g, uint32_t d_tmem, uint32_t a_tmem,
-                                          uint32_t b_off, int bias_chunk, uint64_t* bar, F&& hook) {
+// Issue sync: the group's TMEM stores done before lane 0 of warp LW issues.
+// Returns after the named barrier (all threads) or after this warp's arrive.
+template <bool IM, int LW>
+__device__ __forceinline__ void issue_sync(const GG& g, uint64_t* bar, uint32_t ph) {
   tc::tmem_st_wait();
   tc::tc_fence_before();
-  tc::named_bar(g.bar_id, 128);
+  if constexpr (IM) {
+    __syncwarp();
+    if ((g.r & 31) == 0) tc::mbar_arrive(bar + 1);
+    if (g.r == 32 * LW) tc::mbar_wait(bar + 1, ph);
+  } else {
+    tc::named_bar(g.bar_id, 128);
+  }
+}
+
+template <bool IM, int N, int KA, bool HID, int LW, class F>
+__device__ __forceinline__ void mma_issue(const GG& g, uint32_t d_tmem, uint32_t a_tmem,
+                                          uint32_t b_off, int bias_chunk, uint64_t* bar, uint32_t ph,
+                                          F&& hook) {
+  issue_sync<IM, LW>(g, bar, ph);
   if (g.r == 32 * LW) {
     tc::tc_fence_after();
     constexpr uint32_t idesc = tc::idesc_f16(128, N);
@@ -230,13 +251,11 @@ __device__ __forceinline__ void mma_issue_hid_frame(const GG& g, uint32_t d_tmem
 
 // Query: the frame layer (N = 16 into F) and the sampler's first layer (N =
 // SW into E) both read input chunk 0 — one barrier, one commit.
-template <int SW, int LW>
+template <bool IM, int SW, int LW>
 __device__ __forceinline__ void mma_issue_first2(const GG& g, uint32_t f_tmem, uint32_t e_tmem,
                                                  uint32_t a_tmem, uint32_t frame_off, uint32_t s1_off,
-                                                 uint64_t* bar) {
-  tc::tmem_st_wait();
-  tc::tc_fence_before();
-  tc::named_bar(g.bar_id, 128);
+                                                 uint64_t* bar, uint32_t ph) {
+  issue_sync<IM, LW>(g, bar, ph);
   if (g.r == 32 * LW) {
     tc::tc_fence_after();
     tc::mma_ts(f_tmem, a_tmem, g.desc0 + ((uint64_t)((16 * 16) >> 4) << 16) + (frame_off >> 4),
@@ -440,7 +459,7 @@ __global__ void __launch_bounds__(G * 128, 1)
 fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
             const __grid_constant__ FastConsts fc) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t mma_bar[G][NS];
+  __shared__ uint64_t mma_bar[G][NS][2];  // [0] MMA completion, [1] issue (kIssMbar)
   __shared__ uint64_t in_bar[G][NS][2];
   __shared__ uint64_t w_bar;  // weights staged by TMA
   __shared__ uint32_t tbase_sh;
@@ -474,6 +493,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   // happen to share an SM never block each other in tcgen05.alloc
   constexpr uint32_t kTmemCols = kUsedCols <= 128 ? 128 : (kUsedCols <= 256 ? 256 : 512);
   constexpr bool kWaitAll = ((NMQ_WAIT_ALL_MODES) >> MODE) & 1;
+  // the issue mbarrier needs the all-warps completion wait: with the
+  // polling warp's release barrier a warp could run a phase ahead
+  constexpr bool kIm = kIssMbar && kWaitAll;
+  static_assert(!(kE2 && kIm), "the two-stage eval path uses the named-barrier issue sync");
 
   const int tid = threadIdx.x;
   // warp-uniform by construction (shfl from lane 0): lets ptxas keep the
@@ -489,7 +512,8 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
 
   // --- CTA setup --------------------------------------------------------------
   if (tid < G * NS) {
-    tc::mbar_init(&mma_bar[tid / NS][tid % NS], 1);
+    tc::mbar_init(&mma_bar[tid / NS][tid % NS][0], 1);
+    tc::mbar_init(&mma_bar[tid / NS][tid % NS][1], 4);
     tc::mbar_init(&in_bar[tid / NS][tid % NS][0], 1);
     tc::mbar_init(&in_bar[tid / NS][tid % NS][1], 1);
   }
@@ -566,7 +590,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     sl[s].al = sl[s].a0 + lane;
     sl[s].e0 = sl[s].a0 + DW;
     sl[s].el = sl[s].e0 + lane;
-    sl[s].bar = &mma_bar[gi][s];
+    sl[s].bar = &mma_bar[gi][s][0];
     sl[s].ph = 0u;
     sl[s].t = blockIdx.x * G + gi + s * stride;
     sl[s].it = 0;
@@ -589,12 +613,12 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
                            pack2(ib.wi[3 * r], ib.wi[3 * r + 1]), pack2(ib.wi[3 * r + 2], 1.f), 0u, 0u};
     tc::tmem_st8(S.al, x);
     if constexpr (kQM)
-      mma_issue_first2<SW, LW>(g, S.a0 + 16, S.e0, S.a0, mp.fast_frame_off, mp.layers[mp.samp_first].b_off,
-                               S.bar);
+      mma_issue_first2<kIm, SW, LW>(g, S.a0 + 16, S.e0, S.a0, mp.fast_frame_off, mp.layers[mp.samp_first].b_off,
+                               S.bar, S.ph);
     else if constexpr (kBrdf)
-      mma_issue<16, 1, false, LW>(g, S.a0 + 16, S.a0, mp.fast_frame_off, 0, S.bar, NoOp{});
+      mma_issue<kIm, 16, 1, false, LW>(g, S.a0 + 16, S.a0, mp.fast_frame_off, 0, S.bar, S.ph, NoOp{});
     else
-      mma_issue<SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar, NoOp{});
+      mma_issue<kIm, SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar, S.ph, NoOp{});
   };
 
   if constexpr (kE2) {
@@ -617,7 +641,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       S.level = p0.level;
       tc::mbar_wait(&w_bar, 0);
       chunk0(buf(0, 0));
-      mma_issue<16, 1, false, 0>(g, Y, X, mp.fast_frame_off, 0, S.bar, NoOp{});
+      mma_issue<kIm, 16, 1, false, 0>(g, Y, X, mp.fast_frame_off, 0, S.bar, S.ph, NoOp{});
     }
     bool has_prev = false, pvalid = false, pup = false;
     int64_t pq = 0;
@@ -671,7 +695,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
                                pack2(to[0], to[1]), pack2(to[2], to[3]), pack2(to[4], to[5]), 0u, 0u};
         tc::tmem_st8(XL + 8, x);
       }
-      mma_issue<BW, 2, false, 1>(g, S.d0, X, mp.fast_l1_off, 0, S.bar, refill);
+      mma_issue<kIm, BW, 2, false, 1>(g, S.d0, X, mp.fast_l1_off, 0, S.bar, S.ph, refill);
       // --- stage 1: hidden epilogue -> BRDF layer 2 (+ next tile's frame layer)
       mma_wait<1, kWaitAll>(g, S.bar, S.ph);
       hidden_epi<BW>(S.dl, S.al);
@@ -751,7 +775,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           }
           auto refill = [&]() {  // after the barrier: every row of buffer b was read
             if (t2 < last_full) {
-              if (r == 32 * ((LW + 2) % 4)) stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
+              if (r == 32 * ((LW + 2) % 4)) {
+              if constexpr (kIm) tc::mbar_wait(S.bar + 1, S.ph);  // every row has read buffer b
+              stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
+            }
             } else if (t2 < ntiles) {
               stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, false);  // own row
             }
@@ -771,29 +798,29 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
                                    pack2(to[0], to[1]), pack2(to[2], to[3]), pack2(to[4], to[5]),
                                    0u, 0u};
             tc::tmem_st8(S.al + 8, x);
-            mma_issue<BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, refill);
+            mma_issue<kIm, BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, S.ph, refill);
           } else {
             // sample+pdf: sampler layer 1 D -> layer 2
             hidden_epi<SW>(S.dl, S.al);
             if constexpr (SNH == 1)
-              mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, refill);
+              mma_issue<kIm, 16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
+                                                   1, S.bar, S.ph, refill);
             else
-              mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, refill);
+              mma_issue<kIm, SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
+                                                   1, S.bar, S.ph, refill);
           }
         } else if constexpr (kBrdf && k < kOutB) {
           // BRDF hidden layer k+1
           wait_mma();
           hidden_epi<BW>(S.dl, S.al);
-          mma_issue<BW, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + k].b_off, k,
-                                               S.bar, NoOp{});
+          mma_issue<kIm, BW, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + k].b_off, k,
+                                               S.bar, S.ph, NoOp{});
         } else if constexpr (kOM && k == kOutB) {
           // BRDF output layer on the tensor core: last hidden layer -> A, N = 16 MMA
           wait_mma();
           hidden_epi<BW>(S.dl, S.al);
-          mma_issue<16, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + BNH].b_off, BNH,
-                                               S.bar, NoOp{});
+          mma_issue<kIm, 16, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + BNH].b_off, BNH,
+                                               S.bar, S.ph, NoOp{});
         } else if constexpr (kOM && k == kOutR) {
           wait_mma();
           uint32_t yr[8];
@@ -833,11 +860,11 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             // query: sampler layer 1 (issued with the frame layer, in E) -> layer 2
             hidden_epi<SW>(S.el, S.al);
             if constexpr (SNH == 1)
-              mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, NoOp{});
+              mma_issue<kIm, 16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
+                                                   1, S.bar, S.ph, NoOp{});
             else
-              mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, NoOp{});
+              mma_issue<kIm, SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
+                                                   1, S.bar, S.ph, NoOp{});
           }
         } else if constexpr (kSamp && k > kS0 && k < kFinal) {
           // sampler layer j+1 (j = k - kS0 >= 1; stage kS0 is k == 0 or handled below)
@@ -845,11 +872,11 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           wait_mma();
           hidden_epi<SW>(S.dl, S.al);
           if constexpr (j + 1 == SNH)
-            mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
-                                                 j + 1, S.bar, NoOp{});
+            mma_issue<kIm, 16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
+                                                 j + 1, S.bar, S.ph, NoOp{});
           else
-            mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
-                                                 j + 1, S.bar, NoOp{});
+            mma_issue<kIm, SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
+                                                 j + 1, S.bar, S.ph, NoOp{});
         }
         if constexpr (kSamp && k == kFinal) {
           // proxy parameters, sample, pdf
