@@ -50,7 +50,7 @@ using namespace dev;
 #define NMQ_G_EVAL 7
 #endif
 #ifndef NMQ_G_SAMPLE
-#define NMQ_G_SAMPLE 6  // with SMEM texel staging (NMQ_TEX_SMEM); 5 with register prefetch
+#define NMQ_G_SAMPLE 7  // with SMEM texel staging (NMQ_TEX_SMEM) + all-warps MMA wait; 5 with register prefetch
 #endif
 #ifndef NMQ_G_QUERY
 #define NMQ_G_QUERY 5
@@ -58,9 +58,10 @@ using namespace dev;
 // MMA completion, per mode (bit 1 << MODE): every warp sleeps on the
 // mbarrier itself (try_wait with a suspend hint) instead of one polling warp
 // releasing the other three through a named barrier.  Measured on B200:
-// eval +3 %, query +4 %, sample+pdf -2 %.
+// eval +3 %, query +4 %; sample+pdf -1 % at G = 6, +1 % at G = 7 (which the
+// freed named barriers allow).
 #ifndef NMQ_WAIT_ALL_MODES
-#define NMQ_WAIT_ALL_MODES ((1 << kModeEval) | (1 << kModeQuery))
+#define NMQ_WAIT_ALL_MODES ((1 << kModeEval) | (1 << kModeQuery) | (1 << kModeSamplePdf))
 #endif
 // Hidden-layer biases: A operand of the bias k-step from SMEM (4 KB tile per
 // depth, every row (beta_hi, beta_lo, 0...)) instead of a 32-column TMEM
