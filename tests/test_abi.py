@@ -99,3 +99,20 @@ def test_product_package_never_imports_the_oracle():
             if f.endswith(".py"):
                 for line in open(os.path.join(dirpath, f)):
                     assert not re.match(r"\s*(from|import)\s+oracle", line), (f, line)
+
+
+def test_training_and_host_entry_points_validate_before_launch(lib):
+    """The KL-loss heads, the host-buffer eval and the multi-material limits
+    reject bad arguments with a status (no device work), like the query entry
+    points; empty batches are no-ops."""
+    from paper_2305_02678_b200 import _lib
+    inv, ok = _lib.NM_ERR_INVALID, _lib.NM_OK
+    assert lib.nm_kl_sample(-1, 1, 2, 0, *([None] * 9)) == inv
+    assert lib.nm_kl_sample(0, 1, 2, 0, *([None] * 9)) == ok
+    assert lib.nm_kl_sample(4, 1, 2, 0, *([None] * 9)) == inv
+    assert lib.nm_kl_target(4, 3, *([None] * 6)) == inv
+    assert lib.nm_kl_target_dir(4, 1, 2, *([None] * 6)) == inv
+    assert lib.nm_kl_grad(4, 0, *([None] * 8)) == inv
+    assert lib.nm_kl_grad(0, 0, *([None] * 8)) == ok
+    assert lib.nm_eval_host(None, 10, None, None, 1, None, None, None, None, 0, None) == inv
+    assert lib.nm_mlp_backward(None, 4, None, None, None, None, None) == inv
