@@ -146,6 +146,11 @@ class Clocks:
 # algorithmic bytes: fp32 I/O + 16 B per unique texel touched
 
 def unique_texels(mat_handle, q):
+    return int(torch.unique(texel_ids(mat_handle, q)).numel())
+
+
+def texel_ids(mat_handle, q):
+    """Global texel index of every tap of every query (the exact fetch taps)."""
     from paper_2305_02678_b200 import _lib
     lib = _lib.load()
     n = q["uv"].shape[0]
@@ -161,7 +166,17 @@ def unique_texels(mat_handle, q):
     t = taps.view(n, 4, 2).long()
     lvl = lv.long()
     gid = off_t[lvl][:, None] + t[..., 1] * w_t[lvl][:, None] + t[..., 0]
-    return int(torch.unique(gid.reshape(-1)).numel())
+    return gid.reshape(-1)
+
+
+def hbm_roofline(bytes_per_q, n, ms, note):
+    """Roofline object for workloads timed end to end on the device (several
+    launches per step): achieved = algorithmic bytes / step time."""
+    hbm, _, kind = peaks()
+    ach = bytes_per_q * n / (ms / 1e3) / 1e9
+    return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+            "traffic": None, "peak_source": kind, "algorithmic_bytes_per_query": bytes_per_q,
+            "note": note}
 
 
 # ---------------------------------------------------------------------------
@@ -404,6 +419,16 @@ def run_c4(args):
     ms_b = _time_loop(step(_lib.NM_MULTI_BINNED), steps, args.warmup, stream, world)
     ms_a = _time_loop(step(_lib.NM_MULTI_BINNED_ASYNC), steps, args.warmup, stream, world)
     ms_d = _time_loop(step(_lib.NM_MULTI_DIVERGENT), max(3, steps // 4), 2, stream, world)
+    # algorithmic bytes: 52 B of fp32 I/O + 16 B per unique texel touched, counted
+    # exactly per material on each input set (binning traffic is overhead, not algorithm)
+    tex_b = []
+    for q, mid in zip(sets, ids):
+        u = 0
+        for k, hk in enumerate(handles):
+            sel = mid == k
+            u += unique_texels(hk, {key: v[sel].contiguous() for key, v in q.items()})
+        tex_b.append(16.0 * u / n)
+    bpq = io_bytes("c2") + float(np.mean(tex_b))
     if rank == 0:
         texels = sum(int(h.info.latent_texels) for h in handles)
         print(json.dumps({
@@ -419,6 +444,9 @@ def run_c4(args):
                              "note": "no host round trip (segment sizes stay on the device)"},
             "divergent": {"value": n * world / (ms_d / 1e3), "ms_per_step": ms_d},
             "binned_over_divergent": ms_d / ms_b,
+            "roofline": hbm_roofline(bpq, n * world, ms_b, "binned step (histogram + scan + scatter + "
+                                     "per-material launches) timed as a whole; texel bytes exact per material"),
+            "roofline_binned_async": hbm_roofline(bpq, n * world, ms_a, "binned_async step"),
         }))
 
 
@@ -458,6 +486,12 @@ def run_c5(args):
         if world > 1:
             shard.gather_bands(band, H, W)
 
+    seen = torch.zeros(int(h.info.latent_texels), dtype=torch.bool, device=device)
+    for c0 in range(0, n, chunk):
+        c1 = min(n, c0 + chunk)
+        seen[texel_ids(h, {k: v[c0:c1] for k, v in q.items()})] = True
+    bpq = io_bytes("c2") + 16.0 * int(seen.sum()) / n
+    del seen
     steps = max(2, args.steps // 50)
     ms_c = _time_loop(compute, steps, 2, stream, world)
     ms_f = _time_loop(frame, steps, 1, stream, world)
@@ -472,6 +506,8 @@ def run_c5(args):
             "config": {"workload": "C5 eval 3840x2160x64spp sharded by pixel-row band",
                        "queries_per_frame": total, "parallelism": f"pixel-tile x{world}"},
             "with_spp_reduce_and_gather": {"value": total / (ms_f / 1e3), "ms_per_frame": ms_f},
+            "roofline": hbm_roofline(bpq, n, ms_c, "one fused eval launch over the rank's band; texel "
+                                     "bytes = 16 B x unique texels of the band (exact)"),
         }))
 
 
