@@ -72,21 +72,32 @@ __global__ void bin_scan_kernel(int32_t n_mats, const int32_t* __restrict__ coun
 }
 
 // Each CTA bins a chunk of kScatterRows queries: ranks within the chunk per
-// material from warp-aggregated SHARED atomics, then ONE global atomic per
-// material per CTA reserves the chunk's contiguous range of each segment,
-// and every query copies its inputs there.  (One global atomic per distinct
-// id per warp — 5 x 65k atomics on 5 counters for C4 — serialised at L2:
-// 115 us per 2.07M queries; this way ~5k atomics.)  Ids outside
-// [0, n_mats) are skipped (bin_count_kernel flags them).
-constexpr int kScatterItems = 8;
+// material from warp-aggregated SHARED atomics, ONE global atomic per
+// material per CTA reserves the chunk's contiguous range of each segment
+// (one global atomic per distinct id per warp — 5 x 65k atomics on 5
+// counters for C4 — serialised at L2: 115 us per 2.07M queries), and the
+// chunk is permuted through SMEM so every segment range is written with
+// coalesced stores.  Ids outside [0, n_mats) are skipped (bin_count_kernel
+// flags them).
+constexpr int kScatterItems = 4;
 constexpr int kScatterRows = 256 * kScatterItems;
+struct ScatterSmem {
+  float uv[2 * kScatterRows];
+  float lod[kScatterRows];
+  float urr[kScatterRows];
+  float wi[3 * kScatterRows];
+  float wo[3 * kScatterRows];
+  int32_t row[kScatterRows];
+};
 __global__ void __launch_bounds__(256) bin_scatter_kernel(
     int64_t n, int32_t n_mats, const int32_t* __restrict__ mat_id, int32_t* __restrict__ cursor,
     int32_t* __restrict__ order, const float* __restrict__ uv, const float* __restrict__ lod,
     int32_t lod_stride, const float* __restrict__ urr, const float* __restrict__ wi,
     const float* __restrict__ wo, float* __restrict__ p_uv, float* __restrict__ p_lod,
     float* __restrict__ p_urr, float* __restrict__ p_wi, float* __restrict__ p_wo) {
-  __shared__ int32_t cnt[kMaxMats], base[kMaxMats];
+  extern __shared__ __align__(16) uint8_t sm_raw[];
+  ScatterSmem& S = *reinterpret_cast<ScatterSmem*>(sm_raw);
+  __shared__ int32_t cnt[kMaxMats], loc[kMaxMats + 1], base[kMaxMats];
   for (int i = threadIdx.x; i < n_mats; i += blockDim.x) cnt[i] = 0;
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kScatterRows;
@@ -110,22 +121,54 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) {  // chunk-local segment offsets
+    int32_t acc = 0;
+    for (int m = 0; m < n_mats; ++m) {
+      loc[m] = acc;
+      acc += cnt[m];
+    }
+    loc[n_mats] = acc;
+  }
   for (int i = threadIdx.x; i < n_mats; i += blockDim.x) base[i] = cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0;
   __syncthreads();
+  // gather (coalesced reads) into chunk-local sorted order in SMEM
 #pragma unroll
   for (int k = 0; k < kScatterItems; ++k) {
     if (mi[k] < 0) continue;
     const int64_t i = c0 + k * 256 + threadIdx.x;
-    const int64_t s = base[mi[k]] + rk[k];
-    order[s] = (int32_t)i;
-    reinterpret_cast<float2*>(p_uv)[s] = __ldg(reinterpret_cast<const float2*>(uv) + i);
-    p_lod[s] = __ldg(lod + (lod_stride ? i : 0));
-    p_urr[s] = __ldg(urr + i);
+    const int p = loc[mi[k]] + rk[k];
+    const float2 u = __ldg(reinterpret_cast<const float2*>(uv) + i);
+    S.uv[2 * p] = u.x;
+    S.uv[2 * p + 1] = u.y;
+    S.lod[p] = __ldg(lod + (lod_stride ? i : 0));
+    S.urr[p] = __ldg(urr + i);
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-      p_wi[3 * s + j] = __ldg(wi + 3 * i + j);
-      p_wo[3 * s + j] = __ldg(wo + 3 * i + j);
+      S.wi[3 * p + j] = __ldg(wi + 3 * i + j);
+      S.wo[3 * p + j] = __ldg(wo + 3 * i + j);
     }
+    S.row[p] = (int32_t)i;
+  }
+  __syncthreads();
+  // write each segment range contiguously: position p -> slot base[m] + p - loc[m]
+  const int tot = loc[n_mats];
+  auto slot_of = [&](int p) {
+    int m = 0;
+    while (p >= loc[m + 1]) ++m;  // n_mats <= 64, typically a handful
+    return (int64_t)base[m] + (p - loc[m]);
+  };
+  for (int p = threadIdx.x; p < tot; p += blockDim.x) {
+    const int64_t sl = slot_of(p);
+    order[sl] = S.row[p];
+    p_lod[sl] = S.lod[p];
+    p_urr[sl] = S.urr[p];
+    reinterpret_cast<float2*>(p_uv)[sl] = make_float2(S.uv[2 * p], S.uv[2 * p + 1]);
+  }
+  for (int f = threadIdx.x; f < 3 * tot; f += blockDim.x) {
+    const int p = f / 3, j = f - 3 * p;
+    const int64_t sl = slot_of(p);
+    p_wi[3 * sl + j] = S.wi[f];
+    p_wo[3 * sl + j] = S.wo[f];
   }
 }
 
@@ -230,7 +273,13 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
   if ((e = cudaMemsetAsync(w.counts, 0, (3 * n_mats + 2) * 4, s)) != cudaSuccess) return e;
   bin_count_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
   bin_scan_kernel<<<1, 32, 0, s>>>(n_mats, w.counts, w.offsets, w.cursor, w.seg);
-  bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, 0, s>>>(
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(ScatterSmem));
+    attr = true;
+  }
+  bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sizeof(ScatterSmem), s>>>(
       a.n, n_mats, mat_id, w.cursor, w.order, a.uv, a.lod,
                                                   a.lod_stride, a.u_rr, a.wi, a.wo, w.uv, w.lod,
                                                   w.urr, w.wi, w.wo);
