@@ -26,6 +26,11 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// Per-material counts.  Up to 8 materials: per-thread register counters
+// over a grid-stride loop, warp sums (__reduce_add_sync), one shared atomic
+// per material per warp and one global atomic per material per CTA (few
+// CTAs: global atomics on a handful of counters serialise at L2).  More
+// materials: warp-aggregated shared atomics (__match_any_sync).
 __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mats,
                                                         const int32_t* __restrict__ mat_id,
                                                         int32_t* __restrict__ counts,
@@ -33,19 +38,46 @@ __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mat
   __shared__ int32_t sc[kMaxMats];
   for (int i = threadIdx.x; i < n_mats; i += blockDim.x) sc[i] = 0;
   __syncthreads();
-  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
-       base += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = base + threadIdx.x;
-    const bool in = i < n;
-    int m = in ? __ldg(mat_id + i) : -1;
-    if (in && (m < 0 || m >= n_mats)) {
-      atomicExch(bad, 1);
-      m = -1;
+  if (n_mats <= 8) {
+    int32_t c[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool b = false;
+    auto add = [&](int m) {
+      b |= m < 0 || m >= n_mats;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) c[k] += m == k;
+    };
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n4 = ((uintptr_t)mat_id & 15u) == 0 ? n / 4 : 0;  // 16-byte loads
+    for (int64_t j = gt; j < n4; j += gs) {
+      const int4 v = __ldg(reinterpret_cast<const int4*>(mat_id) + j);
+      add(v.x);
+      add(v.y);
+      add(v.z);
+      add(v.w);
     }
-    const uint32_t active = __ballot_sync(0xffffffffu, m >= 0);
-    if (m >= 0) {
-      const uint32_t peers = __match_any_sync(active, m);
-      if ((peers & lanemask_lt()) == 0) atomicAdd(&sc[m], __popc(peers));
+    for (int64_t i = 4 * n4 + gt; i < n; i += gs) add(__ldg(mat_id + i));
+    if (b) atomicExch(bad, 1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int32_t w = __reduce_add_sync(0xffffffffu, c[k]);
+      if ((threadIdx.x & 31) == 0 && k < n_mats && w) atomicAdd(&sc[k], w);
+    }
+  } else {
+    for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < n;
+         base += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t i = base + threadIdx.x;
+      const bool in = i < n;
+      int m = in ? __ldg(mat_id + i) : -1;
+      if (in && (m < 0 || m >= n_mats)) {
+        atomicExch(bad, 1);
+        m = -1;
+      }
+      const uint32_t active = __ballot_sync(0xffffffffu, m >= 0);
+      if (m >= 0) {
+        const uint32_t peers = __match_any_sync(active, m);
+        if ((peers & lanemask_lt()) == 0) atomicAdd(&sc[m], __popc(peers));
+      }
     }
   }
   __syncthreads();
@@ -271,7 +303,10 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
   MultiWs w = carve(ws, a.n, n_mats);
   cudaError_t e;
   if ((e = cudaMemsetAsync(w.counts, 0, (3 * n_mats + 2) * 4, s)) != cudaSuccess) return e;
-  bin_count_kernel<<<grid256(a.n), 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
+  {
+    const int nb = grid256(a.n), cap = 4 * num_sms_multi();
+    bin_count_kernel<<<nb < cap ? nb : cap, 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
+  }
   bin_scan_kernel<<<1, 32, 0, s>>>(n_mats, w.counts, w.offsets, w.cursor, w.seg);
   static bool attr = false;
   if (!attr) {
