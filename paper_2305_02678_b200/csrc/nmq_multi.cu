@@ -85,24 +85,6 @@ __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mat
     if (sc[i]) atomicAdd(counts + i, sc[i]);
 }
 
-// Segment offsets padded to multiples of 4 rows, so every segment's staged
-// inputs are 16-byte aligned (TMA / the specialized kernels).
-__global__ void bin_scan_kernel(int32_t n_mats, const int32_t* __restrict__ counts,
-                                int32_t* __restrict__ offsets, int32_t* __restrict__ cursor,
-                                int32_t* __restrict__ seg) {
-  if (threadIdx.x == 0) {
-    int32_t acc = 0;
-    for (int m = 0; m < n_mats; ++m) {
-      offsets[m] = acc;
-      cursor[m] = acc;
-      seg[2 * m] = acc;  // {base, count} of segment m, read by the segment launch
-      seg[2 * m + 1] = counts[m];
-      acc += (counts[m] + 3) & ~3;
-    }
-    offsets[n_mats] = acc;
-  }
-}
-
 // Each CTA bins a chunk of kScatterRows queries: ranks within the chunk per
 // material from warp-aggregated SHARED atomics, ONE global atomic per
 // material per CTA reserves the chunk's contiguous range of each segment
@@ -122,15 +104,31 @@ struct ScatterSmem {
   int32_t row[kScatterRows];
 };
 __global__ void __launch_bounds__(256) bin_scatter_kernel(
-    int64_t n, int32_t n_mats, const int32_t* __restrict__ mat_id, int32_t* __restrict__ cursor,
+    int64_t n, int32_t n_mats, const int32_t* __restrict__ mat_id, const int32_t* __restrict__ counts,
+    int32_t* __restrict__ seg, int32_t* __restrict__ cursor,
     int32_t* __restrict__ order, const float* __restrict__ uv, const float* __restrict__ lod,
     int32_t lod_stride, const float* __restrict__ urr, const float* __restrict__ wi,
     const float* __restrict__ wo, float* __restrict__ p_uv, float* __restrict__ p_lod,
     float* __restrict__ p_urr, float* __restrict__ p_wi, float* __restrict__ p_wo) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
   ScatterSmem& S = *reinterpret_cast<ScatterSmem*>(sm_raw);
-  __shared__ int32_t cnt[kMaxMats], loc[kMaxMats + 1], base[kMaxMats];
+  __shared__ int32_t cnt[kMaxMats], loc[kMaxMats + 1], base[kMaxMats], off[kMaxMats];
   for (int i = threadIdx.x; i < n_mats; i += blockDim.x) cnt[i] = 0;
+  if (threadIdx.x == 0) {
+    // segment bases: exclusive scan of the counts, padded to multiples of 4
+    // rows so every segment's staged inputs are 16-byte aligned (TMA); CTA 0
+    // publishes {base, count} per segment for the segment launches
+    int32_t acc = 0;
+    for (int m = 0; m < n_mats; ++m) {
+      const int32_t c = counts[m];
+      off[m] = acc;
+      if (blockIdx.x == 0) {
+        seg[2 * m] = acc;
+        seg[2 * m + 1] = c;
+      }
+      acc += (c + 3) & ~3;
+    }
+  }
   __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kScatterRows;
   int mi[kScatterItems];
@@ -161,7 +159,8 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     }
     loc[n_mats] = acc;
   }
-  for (int i = threadIdx.x; i < n_mats; i += blockDim.x) base[i] = cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0;
+  for (int i = threadIdx.x; i < n_mats; i += blockDim.x)
+    base[i] = off[i] + (cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0);
   __syncthreads();
   // gather (coalesced reads) into chunk-local sorted order in SMEM
 #pragma unroll
@@ -307,7 +306,6 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
     const int nb = grid256(a.n), cap = 4 * num_sms_multi();
     bin_count_kernel<<<nb < cap ? nb : cap, 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
   }
-  bin_scan_kernel<<<1, 32, 0, s>>>(n_mats, w.counts, w.offsets, w.cursor, w.seg);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -315,10 +313,10 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
     attr = true;
   }
   bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sizeof(ScatterSmem), s>>>(
-      a.n, n_mats, mat_id, w.cursor, w.order, a.uv, a.lod,
+      a.n, n_mats, mat_id, w.counts, w.seg, w.cursor, w.order, a.uv, a.lod,
                                                   a.lod_stride, a.u_rr, a.wi, a.wo, w.uv, w.lod,
                                                   w.urr, w.wi, w.wo);
-  g_launches += 3;
+  g_launches += 2;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (!checked) {
     // one launch per material on its own stream, each on ~1/n_mats of the
