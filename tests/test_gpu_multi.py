@@ -88,3 +88,24 @@ def test_multi_modes_agree_and_reject_bad_ids():
     bad[17] = len(mats)
     with pytest.raises(ValueError):
         neural.eval_material_multi(mats, bad, uv, lod, wi, wo, urr, mode="binned")
+    # BINNED_ASYNC never syncs: out-of-range ids (either side) are skipped by
+    # the binning, every valid row is still exact
+    bad[100] = -3
+    c = neural.eval_material_multi(mats, bad, uv, lod, wi, wo, urr, mode="binned_async")
+    ok = (bad >= 0) & (bad < len(mats))
+    np.testing.assert_array_equal(c[ok], a[ok])
+
+
+def test_binning_large_batch_all_rows_land():
+    """Batches spanning many 1024-row scatter chunks and uneven segments:
+    every query's result lands in its own row (binned == divergent)."""
+    from paper_2305_02678_b200 import neural
+
+    rng = np.random.default_rng(11)
+    mats, _ = _materials(rng)
+    n = 70001
+    uv, lod, urr, wi, wo = _queries(rng, n)
+    ids = np.minimum(rng.geometric(0.45, n) - 1, len(mats) - 1).astype(np.int32)  # skewed
+    a = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode="binned_async")
+    b = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode="divergent")
+    np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
