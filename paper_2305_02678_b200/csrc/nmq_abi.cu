@@ -347,8 +347,8 @@ extern "C" {
 
 const char* nm_last_error(void) { return t_err.c_str(); }
 int nm_version(void) { return NMQ_VERSION; }
-int64_t nm_launch_count(void) { return g_launches; }
-int nm_last_kernel_path(void) { return g_last_path; }
+int64_t nm_launch_count(void) { return g_launches.load(); }
+int nm_last_kernel_path(void) { return g_last_path.load(); }
 int nm_set_kernel_path(int path) {
   if (path < 0 || path > 3) return fail(NM_ERR_INVALID, "kernel path must be 0..3");
   g_kernel_path = path;

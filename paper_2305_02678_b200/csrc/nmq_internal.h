@@ -1,6 +1,7 @@
 // nmq_internal.h — material layout shared by the host (nmq_abi.cu) and the
 // kernels (nmq_kernels.cu).  Not part of the public ABI.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -169,10 +170,10 @@ cudaError_t launch_footprint_level(int64_t n, const double* area, int32_t n_leve
 cudaError_t launch_cone_level(int64_t n, const float* cone_w, const float* cone_s, const float* t,
                               const float* cos_hit, const float* density, int32_t density_stride,
                               int32_t n_levels, float* lod, cudaStream_t s);
-extern int64_t g_launches;
+extern std::atomic<int64_t> g_launches;  // host threads may launch concurrently
 // kernel path: 0 = auto (tcgen05 pipelined, then warp-tile, then generic),
 // 1 = generic only, 2 = tcgen05 pipelined, 3 = warp-tile (each falls back to generic)
 extern int g_kernel_path;
-extern int g_last_path;  // family of the last launch_fused (1/2/3 as above)
+extern std::atomic<int> g_last_path;  // family of the last launch_fused (1/2/3 as above)
 
 }  // namespace nmq

@@ -22,9 +22,9 @@
 
 namespace nmq {
 
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
 int g_kernel_path = 0;
-int g_last_path = 0;
+std::atomic<int> g_last_path{0};
 
 namespace {
 
@@ -610,12 +610,12 @@ cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cuda
   if (a.n <= 0) return cudaSuccess;
   if (groups == 0 && (g_kernel_path == 0 || g_kernel_path == 2)) {
     const cudaError_t e = launch_fast(mp, mode, a, s);
-    if (e != cudaErrorNotSupported) return g_last_path = 2, e;
+    if (e != cudaErrorNotSupported) return g_last_path.store(2), e;
     (void)cudaGetLastError();
   }
   if (groups == 0 && (g_kernel_path == 0 || g_kernel_path == 3)) {
     const cudaError_t e = launch_warp(mp, mode, a, s);
-    if (e != cudaErrorNotSupported) return g_last_path = 3, e;
+    if (e != cudaErrorNotSupported) return g_last_path.store(3), e;
     (void)cudaGetLastError();
   }
   g_last_path = 1;

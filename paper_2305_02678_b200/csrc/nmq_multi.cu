@@ -13,6 +13,7 @@
 //    materials present in it and decodes the whole tile with each of them,
 //    keeping each row's own material (nmq_kernels.cu, kModeEvalMulti).
 #include <cstdint>
+#include <mutex>
 #include "nmq_internal.h"
 
 namespace nmq {
@@ -216,6 +217,7 @@ int num_sms_multi() {
 // Side streams for concurrent segment launches (per device, created once).
 constexpr int kMaxSide = 32;
 struct SideStreams {
+  std::mutex mu;  // one fork..join enqueue at a time (the events are shared)
   cudaStream_t st[kMaxSide] = {};
   cudaEvent_t ev[kMaxSide + 1] = {};
   bool ready = false;
@@ -226,6 +228,8 @@ SideStreams& sides() {
   int dev = 0;
   cudaGetDevice(&dev);
   SideStreams& S = g_side[dev & 15];
+  static std::mutex init_mu;
+  std::lock_guard<std::mutex> g(init_mu);
   if (!S.ready) {
     for (int i = 0; i < kMaxSide; ++i) {
       cudaStreamCreateWithFlags(&S.st[i], cudaStreamNonBlocking);
@@ -330,6 +334,7 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
     // dispatch of the next.)
     const int nsm = num_sms_multi();
     const int per = nsm / n_mats > 0 ? nsm / n_mats : 1;
+    std::lock_guard<std::mutex> lock(sides().mu);
     fork_streams(s, n_mats);
     for (int m = 0; m < n_mats; ++m) {
       QueryArgs sa{};
@@ -360,6 +365,7 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
   int64_t total = 0;
   for (int m = 0; m < n_mats; ++m) total += host_counts[m];
   const int nsm = num_sms_multi();
+  std::lock_guard<std::mutex> lock(sides().mu);
   fork_streams(s, n_mats);
   int64_t off = 0;
   for (int m = 0; m < n_mats; ++m) {

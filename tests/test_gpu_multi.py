@@ -109,3 +109,38 @@ def test_binning_large_batch_all_rows_land():
     a = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode="binned_async")
     b = neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode="divergent")
     np.testing.assert_allclose(a, b, rtol=1e-5, atol=1e-6)
+
+
+def test_binned_async_from_concurrent_host_threads():
+    """Two host threads issuing BINNED_ASYNC calls on their own streams at the
+    same time (shared side streams / events): each result is complete and
+    exact when its call's stream is synchronized."""
+    import threading
+    import torch
+    from paper_2305_02678_b200 import neural
+
+    rng = np.random.default_rng(5)
+    mats, _ = _materials(rng)
+    n = 30000
+    qs = [_queries(rng, n) for _ in range(2)]
+    ids = [rng.integers(0, len(mats), n).astype(np.int32) for _ in range(2)]
+    want = [neural.eval_material_multi(mats, ids[k], *qs[k][:2], qs[k][3], qs[k][4], qs[k][2],
+                                       mode="binned_async") for k in range(2)]  # one thread
+    dev = torch.device("cuda", 0)
+    got = [None, None]
+
+    def run(k):
+        st = torch.cuda.Stream(dev)
+        with torch.cuda.stream(st):
+            t = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in qs[k]]
+            idt = torch.from_numpy(ids[k]).to(dev)
+            for _ in range(5):
+                f = neural.eval_material_multi(mats, idt, t[0], t[1], t[3], t[4], t[2], mode="binned_async")
+            st.synchronize()
+            got[k] = f.cpu().numpy()
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    [x.start() for x in th]
+    [x.join() for x in th]
+    for k in range(2):
+        np.testing.assert_array_equal(got[k], want[k])
