@@ -84,6 +84,9 @@ constexpr uint32_t kBiasTile = 4096;  // bytes per bias depth (128 rows x K 16 f
 #ifndef NMQ_EVAL2
 #define NMQ_EVAL2 0  // eval in two stages per tile (see kE2)
 #endif
+#ifndef NMQ_PDL
+#define NMQ_PDL 1  // programmatic dependent launch (prologue overlaps the previous kernel's tail): C2 +4 %
+#endif
 #ifndef NMQ_FAST_NS
 #define NMQ_FAST_NS 1  // tiles in flight per group (2 = ping-pong; slower: fewer warps)
 #endif
@@ -570,6 +573,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   static_assert(1 + (kWaitAll ? 1 : 2) * G <= 16, "named barriers");
   const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
 
+  // programmatic dependent launch: everything above (barriers, TMEM, the
+  // material's weights) is independent of earlier work on the stream; wait
+  // for it here, before the first read of the inputs or write of the outputs
+  if constexpr (NMQ_PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
   const float lod0 = a.lod_stride ? 0.f : __ldg(a.lod);
   // SEG: a binned segment (device row range + output-row indirection); the
   // plain instantiation carries none of it
@@ -913,6 +920,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     });
   }
   }  // !kE2
+  if constexpr (NMQ_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   tc::tc_fence_before();
   __syncthreads();
@@ -971,7 +979,22 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   if (grid > (ntiles + G - 1) / G) grid = (ntiles + G - 1) / G;
   if (grid < 1) grid = 1;
   const FastConsts fc = make_consts(BNH, SNH);
-  kern<<<(int)grid, G * 128, smem, s>>>(mp, a, fc);
+  if constexpr (NMQ_PDL) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(G * 128);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, mp, a, fc);
+    if (e != cudaSuccess) return e;
+  } else {
+    kern<<<(int)grid, G * 128, smem, s>>>(mp, a, fc);
+  }
   ++g_launches;
   return cudaGetLastError();
 }
