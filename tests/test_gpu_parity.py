@@ -299,8 +299,9 @@ def test_scalar_lod_broadcast(kernel_path):
 
 
 def test_streamed_host_eval_matches_device_path():
-    """Large host batches take the chunked two-stream H2D / kernel / D2H
-    pipeline; its results equal the one-shot device path bit for bit."""
+    """Large host batches take the staged H2D / kernel / D2H pipeline
+    (pageable) or the zero-copy launch (pinned); both equal the one-shot
+    device path bit for bit."""
     import torch
     from paper_2305_02678_b200 import _io, neural, synth
 
@@ -318,6 +319,20 @@ def test_streamed_host_eval_matches_device_path():
     f64, _, _ = neural.eval_material(mat, host["uv"], host["lod"], host["wi"], host["wo"],
                                      host["u_rr"], fp16=True, return_level=False)
     assert f64.dtype == np.float64 and np.array_equal(f64, f_dev.cpu().numpy().astype(np.float64))
+    # pinned inputs too: the zero-copy path (one kernel reading / writing over
+    # PCIe, partial last tile included) is bit-identical as well
+    pinned = {k: torch.from_numpy(v).pin_memory().numpy() for k, v in host.items()}
+    out2 = torch.zeros((n, 3), dtype=torch.float32, pin_memory=True).numpy()
+    launches = _lib_launches()
+    neural.eval_material(mat, pinned["uv"], pinned["lod"], pinned["wi"], pinned["wo"], pinned["u_rr"],
+                         fp16=True, return_level=False, out=out2)
+    assert _lib_launches() - launches == 1  # one fused launch, no chunking
+    assert np.array_equal(out2, f_dev.cpu().numpy())
+
+
+def _lib_launches():
+    from paper_2305_02678_b200 import _lib
+    return int(_lib.load().nm_launch_count())
 
 
 def test_lod_from_ray_cones_vs_reference_goldens():
