@@ -44,7 +44,8 @@ __device__ __forceinline__ void axis_f64(double c, int32_t n, int32_t& i0, int32
 
 __global__ void texel_grads_kernel(const __grid_constant__ MatParams mp, int64_t n,
                                    const float* __restrict__ uv, const int32_t* __restrict__ level,
-                                   const float* __restrict__ z_grad, float* __restrict__ grad) {
+                                   const float* __restrict__ z_grad, float* __restrict__ grad,
+                                   bool vec) {
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     int l = __ldg(level + q);
@@ -62,8 +63,19 @@ __global__ void texel_grads_kernel(const __grid_constant__ MatParams mp, int64_t
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const int64_t t = L.off + (int64_t)ys[k] * L.w + xs[k];
+      float v[8];
 #pragma unroll
-      for (int c = 0; c < 8; ++c) atomicAdd(grad + 8 * t + c, (float)(w[k] * (double)g[c]));
+      for (int c = 0; c < 8; ++c) v[c] = (float)(w[k] * (double)g[c]);
+      if (vec) {  // two 16-byte vector reductions per texel (same fp32 atomic adds)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(grad + 8 * t + 4 * h),
+                       "f"(v[4 * h]), "f"(v[4 * h + 1]), "f"(v[4 * h + 2]), "f"(v[4 * h + 3])
+                       : "memory");
+      } else {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) atomicAdd(grad + 8 * t + c, v[c]);
+      }
     }
   }
 }
@@ -143,7 +155,10 @@ __global__ void mlp_backward_kernel(const __grid_constant__ MlpView v, int64_t B
   }
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < B;
        r += (int64_t)gridDim.x * blockDim.x) {
-    double g[kMW], h[kMW];
+    // one register array: the layer's output gradient goes to g_cache (which
+    // the dW/db reduction needs anyway) and is read back from there (L1) for
+    // g @ W, so g and g @ W are never live at once (half the registers)
+    double g[kMW];
     const int fl = v.fo[v.n_layers - 1];
 #pragma unroll
     for (int j = 0; j < kMW; ++j)
@@ -151,27 +166,24 @@ __global__ void mlp_backward_kernel(const __grid_constant__ MlpView v, int64_t B
     for (int l = v.n_layers - 1; l >= 0; --l) {
       const int fi = v.fi[l], fo = v.fo[l];
       const bool leaky = v.act[l] != 0;
+      double* gc = g_cache + pre_off[l] + r;
 #pragma unroll
       for (int j = 0; j < kMW; ++j) {
         if (j < fo) {
           if (leaky && __ldg(pre_cache + pre_off[l] + (int64_t)j * B + r) < 0.f) g[j] *= (double)kLeaky;
-          g_cache[pre_off[l] + (int64_t)j * B + r] = g[j];  // same column-major layout as pre
+          gc[(int64_t)j * B] = g[j];  // same column-major layout as pre
         }
       }
       const float* W = sw + v.w_off[l];
 #pragma unroll
-      for (int k = 0; k < kMW; ++k) {
-        if (k < fi) {
-          double acc = 0.0;
+      for (int k = 0; k < kMW; ++k) g[k] = 0.0;
+      for (int j = 0; j < fo; ++j) {  // g @ W (mlp.py:115), same j order per element
+        const double gj = gc[(int64_t)j * B];
+        const float* Wj = W + j * (fi + 1);
 #pragma unroll
-          for (int j = 0; j < kMW; ++j)
-            if (j < fo) acc = fma(g[j], (double)W[j * (fi + 1) + k], acc);
-          h[k] = acc;  // g @ W (mlp.py:115)
-        }
+        for (int k = 0; k < kMW; ++k)
+          if (k < fi) g[k] = fma(gj, (double)Wj[k], g[k]);
       }
-#pragma unroll
-      for (int k = 0; k < kMW; ++k)
-        if (k < fi) g[k] = h[k];
     }
     const int fi0 = v.fi[0];
 #pragma unroll
@@ -267,7 +279,8 @@ cudaError_t launch_texel_grads(const MatParams& mp, int64_t n, const float* uv, 
   if (n <= 0) return cudaSuccess;
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
-  texel_grads_kernel<<<(int)blocks, 256, 0, s>>>(mp, n, uv, level, z_grad, grad);
+  const bool vec = ((uintptr_t)grad & 15u) == 0;
+  texel_grads_kernel<<<(int)blocks, 256, 0, s>>>(mp, n, uv, level, z_grad, grad, vec);
   ++g_launches;
   return cudaGetLastError();
 }
