@@ -200,8 +200,10 @@ __global__ void __launch_bounds__(256) mlp_dparam_kernel(int64_t B, int fi, int 
                                                          const float* __restrict__ in_src,
                                                          const double* __restrict__ g,
                                                          double* __restrict__ dp) {
-  __shared__ double sg[kMaxW][kTileRows];
-  __shared__ float sx[kMaxW + 1][kTileRows];
+  // rows padded by one element: the lanes of a warp read consecutive k (and
+  // mostly one j) at the same rr — unpadded, every lane hit the same bank
+  __shared__ double sg[kMaxW][kTileRows + 1];
+  __shared__ float sx[kMaxW + 1][kTileRows + 1];
   const int pairs = fo * (fi + 1);
   constexpr int kPer = (kMaxW * (kMaxW + 1) + 255) / 256;
   double acc[kPer];
