@@ -565,7 +565,7 @@ def run_train(args):
     if rank == 0:
         print(json.dumps({
             "metric": "training-side rows/s (forward_cached + backward of both decoders + texel-grad scatter)",
-            "value": B / (ms / 1e3), "unit": "rows/s", "n_gpus": world, "steps": steps,
+            "value": B * world / (ms / 1e3), "unit": "rows/s", "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "fp32 forward, fp64 backward chain / reductions",
             "data": "synthetic: random-init networks, N(0,1) inputs and gradients",
