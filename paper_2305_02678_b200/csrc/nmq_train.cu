@@ -15,8 +15,9 @@
 //    output gradients cached column-major.
 //  * mlp_dparam_kernel: dW = g^T x and db = sum g over the batch — a
 //    split-K reduction: each CTA stages 32-row tiles of g and the layer
-//    input in SMEM, accumulates its (out x in+1) partials in float64
-//    registers and adds them to the result with float64 atomics.
+//    input (as float64) in SMEM, accumulates 4x4 register blocks of its
+//    (out x in+1) partials in float64 and adds them to the result with
+//    float64 atomics.
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "nmq_device.cuh"
@@ -194,35 +195,68 @@ __global__ void mlp_backward_kernel(const __grid_constant__ MlpView v, int64_t B
 
 // dW[j][k] = sum_r g[j][r] * in[k][r], db[j] = sum_r g[j][r]   (mlp.py:114)
 // `in` = the cached input x (layer 0) or act(pre of the previous layer).
-constexpr int kRowsPerCta = 256, kTileRows = 32;  // ~B/256 CTAs of split-K partials
+constexpr int kRowsPerCta = 256, kTileRows = 32;  // B/256 CTAs of split-K partials per layer
 
-__global__ void __launch_bounds__(256) mlp_dparam_kernel(int64_t B, int fi, int fo, int in_act,
-                                                         const float* __restrict__ in_src,
-                                                         const double* __restrict__ g,
-                                                         double* __restrict__ dp) {
-  // rows padded by one element: the lanes of a warp read consecutive k (and
-  // mostly one j) at the same rr — unpadded, every lane hit the same bank
-  __shared__ double sg[kMaxW][kTileRows + 1];
-  __shared__ float sx[kMaxW + 1][kTileRows + 1];
-  const int pairs = fo * (fi + 1);
-  constexpr int kPer = (kMaxW * (kMaxW + 1) + 255) / 256;
-  double acc[kPer];
+// Register-blocked: a thread owns a 4(j) x 4(k) block of (dW | db) and reads
+// its 4 g and 4 inputs per row as two 16-byte SMEM loads each (inputs are
+// converted to float64 once, at staging), 16 DFMA per 4 loads.  Narrow layers
+// (< 128 blocks) split the tile rows over R thread slices whose partials meet
+// in a float64 SMEM reduction before the one global atomic per parameter.
+constexpr int kBlk = 4;
+constexpr int kMaxNbJ = (kMaxW + kBlk - 1) / kBlk, kMaxNbK = (kMaxW + 1 + kBlk - 1) / kBlk;
+constexpr int kBlkPer = (kMaxNbJ * kMaxNbK + 255) / 256;
+constexpr int kGPer = (kBlk * kMaxNbJ * kTileRows + 255) / 256, kXPer = (kBlk * kMaxNbK * kTileRows + 255) / 256;
+constexpr int kDpSmem = kTileRows * (kBlk * kMaxNbJ + 2) + kTileRows * (kBlk * kMaxNbK + 2);
+static_assert(kDpSmem >= kMaxW * (kMaxW + 1), "reduction buffer reuses the staging tiles");
+
+struct DparamArgs {  // every layer of one network: blockIdx.y = layer
+  int32_t fi[kMaxLayers], fo[kMaxLayers], in_act[kMaxLayers];
+  const float* in_src[kMaxLayers];
+  const double* g[kMaxLayers];
+  double* dp[kMaxLayers];
+};
+
+__global__ void __launch_bounds__(256) mlp_dparam_kernel(const __grid_constant__ DparamArgs args, int64_t B) {
+  const int l = blockIdx.y;
+  const int fi = args.fi[l], fo = args.fo[l], in_act = args.in_act[l];
+  const float* __restrict__ in_src = args.in_src[l];
+  const double* __restrict__ g = args.g[l];
+  double* __restrict__ dp = args.dp[l];
+  __shared__ __align__(16) double smem[kDpSmem];
+  const int njb = (fo + kBlk - 1) / kBlk, nkb = (fi + 1 + kBlk - 1) / kBlk, nb = njb * nkb;
+  // row strides padded by 2 doubles (16-byte aligned rows, fewer store conflicts)
+  const int SJ = kBlk * njb + 2, SK = kBlk * nkb + 2;
+  double* sg = smem;                  // [kTileRows][SJ]
+  double* sx = smem + kTileRows * SJ;  // [kTileRows][SK]
+  const int R = nb >= 128 ? 1 : (256 / nb < kTileRows ? 256 / nb : kTileRows);
+  const int t = threadIdx.x;
+  double acc[kBlkPer][kBlk * kBlk];
 #pragma unroll
-  for (int e = 0; e < kPer; ++e) acc[e] = 0.0;
+  for (int e = 0; e < kBlkPer; ++e)
+#pragma unroll
+    for (int i = 0; i < kBlk * kBlk; ++i) acc[e][i] = 0.0;
   const int64_t r0 = (int64_t)blockIdx.x * kRowsPerCta;
   const int64_t r1 = r0 + kRowsPerCta < B ? r0 + kRowsPerCta : B;
-  for (int64_t t0 = r0; t0 < r1; t0 += kTileRows) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < fo * kTileRows; i += blockDim.x) {
-      const int j = i / kTileRows, rr = i % kTileRows;
-      const int64_t r = t0 + rr;
-      sg[j][rr] = r < r1 ? g[(int64_t)j * B + r] : 0.0;
+  // the next tile's g and inputs are loaded into registers while the current
+  // one is reduced (17 loads in flight per thread instead of one)
+  const int ng = kBlk * njb * kTileRows, nx = kBlk * nkb * kTileRows;
+  double gr[kGPer];
+  float xr[kXPer];
+  auto load = [&](int64_t t0) {
+#pragma unroll
+    for (int u = 0; u < kGPer; ++u) {
+      const int i = t + u * 256, j = i / kTileRows;
+      if (i >= ng) break;  // warp-uniform (ng is a multiple of 128): narrow layers skip the rest
+      const int64_t r = t0 + i % kTileRows;
+      gr[u] = (j < fo && r < r1) ? g[(int64_t)j * B + r] : 0.0;
     }
-    for (int i = threadIdx.x; i < (fi + 1) * kTileRows; i += blockDim.x) {
-      const int k = i / kTileRows, rr = i % kTileRows;
-      const int64_t r = t0 + rr;
+#pragma unroll
+    for (int u = 0; u < kXPer; ++u) {
+      const int i = t + u * 256, k = i / kTileRows;
+      if (i >= nx) break;
+      const int64_t r = t0 + i % kTileRows;
       float xv = 0.f;
-      if (r < r1) {
+      if (r < r1 && k <= fi) {
         if (k == fi) {
           xv = 1.f;  // bias column
         } else {
@@ -230,25 +264,72 @@ __global__ void __launch_bounds__(256) mlp_dparam_kernel(int64_t B, int fi, int 
           if (in_act && xv < 0.f) xv *= kLeaky;
         }
       }
-      sx[k][rr] = xv;
+      xr[u] = xv;
     }
+  };
+  load(r0);
+  for (int64_t t0 = r0; t0 < r1; t0 += kTileRows) {
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < kPer; ++e) {
-      const int pidx = threadIdx.x + e * 256;
-      if (pidx < pairs) {
-        const int j = pidx / (fi + 1), k = pidx % (fi + 1);
-        double s = acc[e];
+    for (int u = 0; u < kGPer; ++u) {
+      const int i = t + u * 256;
+      if (i >= ng) break;
+      sg[(i % kTileRows) * SJ + i / kTileRows] = gr[u];
+    }
 #pragma unroll
-        for (int rr = 0; rr < kTileRows; ++rr) s = fma(sg[j][rr], (double)sx[k][rr], s);
-        acc[e] = s;
+    for (int u = 0; u < kXPer; ++u) {
+      const int i = t + u * 256;
+      if (i >= nx) break;
+      sx[(i % kTileRows) * SK + i / kTileRows] = (double)xr[u];
+    }
+    __syncthreads();
+    if (t0 + kTileRows < r1) load(t0 + kTileRows);
+#pragma unroll
+    for (int e = 0; e < kBlkPer; ++e) {
+      const int blk = R > 1 ? t % nb : t + e * 256;
+      const int slice = R > 1 ? t / nb : 0;
+      if ((R > 1 && (e > 0 || slice >= R)) || blk >= nb) continue;
+      const double* gp = sg + kBlk * (blk / nkb);
+      const double* xp = sx + kBlk * (blk % nkb);
+      for (int rr = slice; rr < kTileRows; rr += R) {
+        const double2 g01 = *reinterpret_cast<const double2*>(gp + rr * SJ);
+        const double2 g23 = *reinterpret_cast<const double2*>(gp + rr * SJ + 2);
+        const double2 x01 = *reinterpret_cast<const double2*>(xp + rr * SK);
+        const double2 x23 = *reinterpret_cast<const double2*>(xp + rr * SK + 2);
+        const double gv[4] = {g01.x, g01.y, g23.x, g23.y}, xv[4] = {x01.x, x01.y, x23.x, x23.y};
+#pragma unroll
+        for (int a = 0; a < kBlk; ++a)
+#pragma unroll
+          for (int c = 0; c < kBlk; ++c) acc[e][a * kBlk + c] = fma(gv[a], xv[c], acc[e][a * kBlk + c]);
       }
     }
   }
+  const int pairs = fo * (fi + 1);
+  if (R > 1) {  // slices meet in SMEM, then one global atomic per parameter
+    __syncthreads();
+    for (int i = t; i < pairs; i += blockDim.x) smem[i] = 0.0;
+    __syncthreads();
+  }
 #pragma unroll
-  for (int e = 0; e < kPer; ++e) {
-    const int pidx = threadIdx.x + e * 256;
-    if (pidx < pairs) atomicAdd(dp + pidx, acc[e]);
+  for (int e = 0; e < kBlkPer; ++e) {
+    const int blk = R > 1 ? t % nb : t + e * 256;
+    const int slice = R > 1 ? t / nb : 0;
+    if ((R > 1 && (e > 0 || slice >= R)) || blk >= nb) continue;
+    const int j0 = kBlk * (blk / nkb), k0 = kBlk * (blk % nkb);
+#pragma unroll
+    for (int a = 0; a < kBlk; ++a)
+#pragma unroll
+      for (int c = 0; c < kBlk; ++c) {
+        const int j = j0 + a, k = k0 + c;
+        if (j < fo && k <= fi) {
+          if (R > 1) atomicAdd(smem + j * (fi + 1) + k, acc[e][a * kBlk + c]);
+          else atomicAdd(dp + j * (fi + 1) + k, acc[e][a * kBlk + c]);
+        }
+      }
+  }
+  if (R > 1) {
+    __syncthreads();
+    for (int i = t; i < pairs; i += blockDim.x) atomicAdd(dp + i, smem[i]);
   }
 }
 
@@ -339,16 +420,22 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
   ++g_launches;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if ((e = cudaMemsetAsync(dparams, 0, (size_t)w_floats * 8, s)) != cudaSuccess) return e;
+  // all layers' dW/db in one launch: the layers are independent once the
+  // backward chain has cached every g, and n_layers x the CTAs hide load latency
+  DparamArgs da;
   int64_t pre_off = 0;
-  const int grid = (int)((B + kRowsPerCta - 1) / kRowsPerCta);
   for (int l = 0; l < n_layers; ++l) {
-    const float* in_src = l == 0 ? x_cache : pre_cache + (pre_off - (int64_t)fo[l - 1] * B);
-    const int in_act = l == 0 ? 0 : act[l - 1];
-    mlp_dparam_kernel<<<grid, 256, 0, s>>>(B, fi[l], fo[l], in_act, in_src, g_cache + pre_off,
-                                           dparams + v.w_off[l]);
-    ++g_launches;
+    da.fi[l] = fi[l];
+    da.fo[l] = fo[l];
+    da.in_act[l] = l == 0 ? 0 : act[l - 1];
+    da.in_src[l] = l == 0 ? x_cache : pre_cache + (pre_off - (int64_t)fo[l - 1] * B);
+    da.g[l] = g_cache + pre_off;
+    da.dp[l] = dparams + v.w_off[l];
     pre_off += (int64_t)fo[l] * B;
   }
+  const dim3 grid((unsigned)((B + kRowsPerCta - 1) / kRowsPerCta), (unsigned)n_layers);
+  mlp_dparam_kernel<<<grid, 256, 0, s>>>(da, B);
+  ++g_launches;
   return cudaGetLastError();
 }
 
