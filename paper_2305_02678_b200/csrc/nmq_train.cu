@@ -43,10 +43,20 @@ __device__ __forceinline__ void axis_f64(double c, int32_t n, int32_t& i0, int32
   i1 = (i0 + 1 == n) ? 0 : i0 + 1;
 }
 
+// The coarse tail of the pyramid (levels of <= 16x16 texels, a few hundred
+// texels) receives a large share of all taps — with a uniform lod every level
+// takes 1/L of the queries, the 1x1 level all 4 taps of each — so its
+// contributions are pre-summed per CTA in SMEM and flushed once (global
+// atomics on those addresses serialised at L2 dominated the scatter).
+constexpr int kTailTexels = 512;
+
 __global__ void texel_grads_kernel(const __grid_constant__ MatParams mp, int64_t n,
                                    const float* __restrict__ uv, const int32_t* __restrict__ level,
                                    const float* __restrict__ z_grad, float* __restrict__ grad,
-                                   bool vec) {
+                                   bool vec, int64_t tail_start, int tail_n) {
+  __shared__ __align__(16) float tail[kTailTexels * 8];
+  for (int i = threadIdx.x; i < tail_n * 8; i += blockDim.x) tail[i] = 0.f;
+  __syncthreads();
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n;
        q += (int64_t)gridDim.x * blockDim.x) {
     int l = __ldg(level + q);
@@ -67,7 +77,10 @@ __global__ void texel_grads_kernel(const __grid_constant__ MatParams mp, int64_t
       float v[8];
 #pragma unroll
       for (int c = 0; c < 8; ++c) v[c] = (float)(w[k] * (double)g[c]);
-      if (vec) {  // two 16-byte vector reductions per texel (same fp32 atomic adds)
+      if (t >= tail_start) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) atomicAdd(tail + 8 * (t - tail_start) + c, v[c]);
+      } else if (vec) {  // two 16-byte vector reductions per texel (same fp32 atomic adds)
 #pragma unroll
         for (int h = 0; h < 2; ++h)
           asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(grad + 8 * t + 4 * h),
@@ -77,6 +90,25 @@ __global__ void texel_grads_kernel(const __grid_constant__ MatParams mp, int64_t
 #pragma unroll
         for (int c = 0; c < 8; ++c) atomicAdd(grad + 8 * t + c, v[c]);
       }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < tail_n; i += blockDim.x) {
+    const float4 lo = reinterpret_cast<const float4*>(tail)[2 * i];
+    const float4 hi = reinterpret_cast<const float4*>(tail)[2 * i + 1];
+    const bool touched = lo.x != 0.f || lo.y != 0.f || lo.z != 0.f || lo.w != 0.f || hi.x != 0.f ||
+                         hi.y != 0.f || hi.z != 0.f || hi.w != 0.f;
+    if (!touched) continue;
+    float* dst = grad + 8 * (tail_start + i);
+    if (vec) {
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(lo.x), "f"(lo.y),
+                   "f"(lo.z), "f"(lo.w) : "memory");
+      asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst + 4), "f"(hi.x), "f"(hi.y),
+                   "f"(hi.z), "f"(hi.w) : "memory");
+    } else {
+      const float v[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+      for (int c = 0; c < 8; ++c) atomicAdd(dst + c, v[c]);
     }
   }
 }
@@ -363,7 +395,13 @@ cudaError_t launch_texel_grads(const MatParams& mp, int64_t n, const float* uv, 
   int64_t blocks = (n + 255) / 256;
   if (blocks > (int64_t)sm_count() * 16) blocks = (int64_t)sm_count() * 16;
   const bool vec = ((uintptr_t)grad & 15u) == 0;
-  texel_grads_kernel<<<(int)blocks, 256, 0, s>>>(mp, n, uv, level, z_grad, grad, vec);
+  // coarse tail: the last levels whose texels together fit kTailTexels
+  const LevelDesc& last = mp.lv[mp.n_levels - 1];
+  const int64_t total = last.off + (int64_t)last.w * last.h;
+  int64_t tail_start = total;
+  for (int l = mp.n_levels - 1; l >= 0 && total - mp.lv[l].off <= kTailTexels; --l) tail_start = mp.lv[l].off;
+  texel_grads_kernel<<<(int)blocks, 256, 0, s>>>(mp, n, uv, level, z_grad, grad, vec, tail_start,
+                                                 (int)(total - tail_start));
   ++g_launches;
   return cudaGetLastError();
 }
