@@ -170,13 +170,17 @@ __global__ void mlp_forward_kernel(const __grid_constant__ MlpView v, int64_t B,
   }
 }
 
-template <int kMW>
+template <int kMW, typename WT>
 __global__ void mlp_backward_kernel(const __grid_constant__ MlpView v, int64_t B,
                                     const float* __restrict__ wts, const float* __restrict__ pre_cache,
                                     const float* __restrict__ out_grad, double* __restrict__ g_cache,
                                     double* __restrict__ dx) {
-  extern __shared__ float sw[];
-  for (int i = threadIdx.x; i < v.w_floats; i += blockDim.x) sw[i] = wts[i];
+  // WT = double: weights widened to float64 once at staging (exact), so the
+  // chain's DFMAs take them straight from SMEM without a per-use F2F
+  // conversion; WT = float for networks whose float64 copy exceeds SMEM
+  extern __shared__ __align__(8) unsigned char sraw[];
+  WT* swd = reinterpret_cast<WT*>(sraw);
+  for (int i = threadIdx.x; i < v.w_floats; i += blockDim.x) swd[i] = (WT)wts[i];
   __syncthreads();
   int64_t pre_off[kMaxLayers];
   {
@@ -207,12 +211,12 @@ __global__ void mlp_backward_kernel(const __grid_constant__ MlpView v, int64_t B
           gc[(int64_t)j * B] = g[j];  // same column-major layout as pre
         }
       }
-      const float* W = sw + v.w_off[l];
+      const WT* W = swd + v.w_off[l];
 #pragma unroll
       for (int k = 0; k < kMW; ++k) g[k] = 0.0;
       for (int j = 0; j < fo; ++j) {  // g @ W (mlp.py:115), same j order per element
         const double gj = gc[(int64_t)j * B];
-        const float* Wj = W + j * (fi + 1);
+        const WT* Wj = W + j * (fi + 1);
 #pragma unroll
         for (int k = 0; k < kMW; ++k)
           if (k < fi) g[k] = fma(gj, (double)Wj[k], g[k]);
@@ -447,9 +451,10 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
     o += fo[l] * (fi[l] + 1);
   }
   v.w_floats = w_floats;
-  const size_t smem = (size_t)w_floats * 4;
-  const bool wide = max_width(v) > 32;
-  auto kern = wide ? mlp_backward_kernel<64> : mlp_backward_kernel<32>;
+  const bool wide = max_width(v) > 32, w64 = (size_t)w_floats * 8 <= 200 * 1024;
+  const size_t smem = (size_t)w_floats * (w64 ? 8 : 4);  // float64 copy of the weights when it fits
+  auto kern = wide ? (w64 ? mlp_backward_kernel<64, double> : mlp_backward_kernel<64, float>)
+                   : (w64 ? mlp_backward_kernel<32, double> : mlp_backward_kernel<32, float>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t blocks = (B + 127) / 128;
