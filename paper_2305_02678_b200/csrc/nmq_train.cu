@@ -239,11 +239,6 @@ constexpr int kRowsPerCta = 256, kTileRows = 32;  // B/256 CTAs of split-K parti
 // (< 128 blocks) split the tile rows over R thread slices whose partials meet
 // in a float64 SMEM reduction before the one global atomic per parameter.
 constexpr int kBlk = 4;
-constexpr int kMaxNbJ = (kMaxW + kBlk - 1) / kBlk, kMaxNbK = (kMaxW + 1 + kBlk - 1) / kBlk;
-constexpr int kBlkPer = (kMaxNbJ * kMaxNbK + 255) / 256;
-constexpr int kGPer = (kBlk * kMaxNbJ * kTileRows + 255) / 256, kXPer = (kBlk * kMaxNbK * kTileRows + 255) / 256;
-constexpr int kDpSmem = kTileRows * (kBlk * kMaxNbJ + 2) + kTileRows * (kBlk * kMaxNbK + 2);
-static_assert(kDpSmem >= kMaxW * (kMaxW + 1), "reduction buffer reuses the staging tiles");
 
 struct DparamArgs {  // every layer of one network: blockIdx.y = layer
   int32_t fi[kMaxLayers], fo[kMaxLayers], in_act[kMaxLayers];
@@ -252,7 +247,16 @@ struct DparamArgs {  // every layer of one network: blockIdx.y = layer
   double* dp[kMaxLayers];
 };
 
+// kMW = the network's widest layer (32 or 64): sizes the register blocks,
+// prefetch registers and SMEM (the 32-wide instance fits 3 CTAs per SM)
+template <int kMW>
 __global__ void __launch_bounds__(256) mlp_dparam_kernel(const __grid_constant__ DparamArgs args, int64_t B) {
+  constexpr int kMaxNbJ = (kMW + kBlk - 1) / kBlk, kMaxNbK = (kMW + 1 + kBlk - 1) / kBlk;
+  constexpr int kBlkPer = (kMaxNbJ * kMaxNbK + 255) / 256;
+  constexpr int kGPer = (kBlk * kMaxNbJ * kTileRows + 255) / 256;
+  constexpr int kXPer = (kBlk * kMaxNbK * kTileRows + 255) / 256;
+  constexpr int kDpSmem = kTileRows * (kBlk * kMaxNbJ + 2) + kTileRows * (kBlk * kMaxNbK + 2);
+  static_assert(kDpSmem >= kMW * (kMW + 1), "reduction buffer reuses the staging tiles");
   const int l = blockIdx.y;
   const int fi = args.fi[l], fo = args.fo[l], in_act = args.in_act[l];
   const float* __restrict__ in_src = args.in_src[l];
@@ -477,7 +481,10 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
     pre_off += (int64_t)fo[l] * B;
   }
   const dim3 grid((unsigned)((B + kRowsPerCta - 1) / kRowsPerCta), (unsigned)n_layers);
-  mlp_dparam_kernel<<<grid, 256, 0, s>>>(da, B);
+  if (wide)
+    mlp_dparam_kernel<64><<<grid, 256, 0, s>>>(da, B);
+  else
+    mlp_dparam_kernel<32><<<grid, 256, 0, s>>>(da, B);
   ++g_launches;
   return cudaGetLastError();
 }
