@@ -121,46 +121,91 @@ struct MlpView {
   int32_t fi[kMaxLayers], fo[kMaxLayers], act[kMaxLayers];
   int32_t w_off[kMaxLayers];  // float offset of layer l in the access-order weights
   int32_t w_floats;
+  int32_t p_off[kMaxLayers];  // forward (kPad): layer offsets of the padded SMEM copy
 };
 
-template <int kMW>
+// kPad: every weight row zero-padded to kMW (+ the bias at index kMW, rows
+// 16-byte aligned) and activations zero beyond the layer width, so the inner
+// product runs unpredicated over kMW with LDS.128 weight reads; the appended
+// terms are 0 * 0, so each row's fp32 FMA chain is unchanged (the per-k
+// predicates of the unpadded instance cost as many ISETPs as FFMAs).
+template <int kMW, bool kPad>
 __global__ void mlp_forward_kernel(const __grid_constant__ MlpView v, int64_t B,
                                    const float* __restrict__ wts, const float* __restrict__ x,
                                    float* __restrict__ x_cache, float* __restrict__ pre_cache,
                                    float* __restrict__ out) {
-  extern __shared__ float sw[];
-  for (int i = threadIdx.x; i < v.w_floats; i += blockDim.x) sw[i] = wts[i];
+  extern __shared__ float4 sw4[];
+  float* sw = reinterpret_cast<float*>(sw4);
+  constexpr int rs = kMW + 4;
+  if (kPad) {
+    for (int l = 0; l < v.n_layers; ++l) {
+      const int fi = v.fi[l];
+      const float* wl = wts + v.w_off[l];
+      for (int i = threadIdx.x; i < v.fo[l] * rs; i += blockDim.x) {
+        const int j = i / rs, k = i % rs;
+        sw[v.p_off[l] + i] = k < fi ? wl[j * (fi + 1) + k] : (k == kMW ? wl[j * (fi + 1) + fi] : 0.f);
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < v.w_floats; i += blockDim.x) sw[i] = wts[i];
+  }
   __syncthreads();
   for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < B;
        r += (int64_t)gridDim.x * blockDim.x) {
     float a[kMW], p[kMW];
     const int fi0 = v.fi[0];
 #pragma unroll
-    for (int k = 0; k < kMW; ++k)
+    for (int k = 0; k < kMW; ++k) {
       if (k < fi0) {
         a[k] = __ldg(x + r * fi0 + k);
         x_cache[(int64_t)k * B + r] = a[k];
+      } else {
+        a[k] = 0.f;
       }
+    }
     int64_t pre_base = 0;
     for (int l = 0; l < v.n_layers; ++l) {
       const int fi = v.fi[l], fo = v.fo[l];
-      const float* W = sw + v.w_off[l];
+      if (kPad) {
+        const float* W = sw + v.p_off[l];
 #pragma unroll
-      for (int j = 0; j < kMW; ++j) {
-        if (j < fo) {
-          const float* row = W + j * (fi + 1);
-          float acc = 0.f;
+        for (int j = 0; j < kMW; ++j) {
+          if (j < fo) {
+            const float4* row = reinterpret_cast<const float4*>(W + j * rs);
+            float acc = 0.f;
 #pragma unroll
-          for (int k = 0; k < kMW; ++k)
-            if (k < fi) acc = fmaf(a[k], row[k], acc);
-          p[j] = acc + row[fi];  // x W^T + b (mlp.py:96)
-          pre_cache[pre_base + (int64_t)j * B + r] = p[j];
+            for (int k4 = 0; k4 < kMW / 4; ++k4) {
+              const float4 w = row[k4];
+              acc = fmaf(a[4 * k4 + 0], w.x, acc);
+              acc = fmaf(a[4 * k4 + 1], w.y, acc);
+              acc = fmaf(a[4 * k4 + 2], w.z, acc);
+              acc = fmaf(a[4 * k4 + 3], w.w, acc);
+            }
+            p[j] = acc + W[j * rs + kMW];  // x W^T + b (mlp.py:96)
+            pre_cache[pre_base + (int64_t)j * B + r] = p[j];
+          } else {
+            p[j] = 0.f;  // keeps the next layer's padded inputs zero
+          }
+        }
+      } else {
+        const float* W = sw + v.w_off[l];
+#pragma unroll
+        for (int j = 0; j < kMW; ++j) {
+          if (j < fo) {
+            const float* row = W + j * (fi + 1);
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < kMW; ++k)
+              if (k < fi) acc = fmaf(a[k], row[k], acc);
+            p[j] = acc + row[fi];  // x W^T + b (mlp.py:96)
+            pre_cache[pre_base + (int64_t)j * B + r] = p[j];
+          }
         }
       }
       const bool leaky = v.act[l] != 0;
 #pragma unroll
       for (int j = 0; j < kMW; ++j)
-        if (j < fo) a[j] = leaky ? (p[j] >= 0.f ? p[j] : kLeaky * p[j]) : p[j];
+        if (kPad || j < fo) a[j] = leaky ? (p[j] >= 0.f ? p[j] : kLeaky * p[j]) : p[j];
       pre_base += (int64_t)fo * B;
     }
     const int fl = v.fo[v.n_layers - 1];
@@ -428,9 +473,17 @@ cudaError_t launch_mlp_forward(const int32_t* fi, const int32_t* fo, const int32
     o += fo[l] * (fi[l] + 1);
   }
   v.w_floats = w_floats;
-  const size_t smem = (size_t)w_floats * 4;
   const bool wide = max_width(v) > 32;  // register arrays sized to the widest layer
-  auto kern = wide ? mlp_forward_kernel<64> : mlp_forward_kernel<32>;
+  const int rs = (wide ? 64 : 32) + 4;
+  int32_t po = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    v.p_off[l] = po;
+    po += fo[l] * rs;
+  }
+  const bool pad = (size_t)po * 4 <= 200 * 1024;
+  const size_t smem = (size_t)(pad ? po : w_floats) * 4;
+  auto kern = wide ? (pad ? mlp_forward_kernel<64, true> : mlp_forward_kernel<64, false>)
+                   : (pad ? mlp_forward_kernel<32, true> : mlp_forward_kernel<32, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t blocks = (B + 127) / 128;
