@@ -247,14 +247,25 @@ const char* nm_last_error(void);
 int nm_version(void);
 /* number of fused-kernel launches issued by this process (for bench claims) */
 int64_t nm_launch_count(void);
-/* test hook: 0 = auto (default: the pipelined tcgen05 kernels, then the
- * warp-tile mma.sync kernels, for materials matching a specialized
- * architecture), 1 = always the runtime-generic kernel, 2 = pipelined tcgen05,
- * 3 = warp-tile (2 and 3 fall back to the generic kernel when inapplicable) */
+/* test hook: 0 = auto (default: the pipelined tcgen05 kernels for materials
+ * matching a specialized architecture), 1 = always the runtime-generic
+ * kernel, 2 = pipelined tcgen05 (falls back to the generic kernel when
+ * inapplicable) */
 int nm_set_kernel_path(int path);
 /* which kernel family ran the last query launch of this process:
- * 1 = generic, 2 = pipelined tcgen05, 3 = warp-tile mma.sync */
+ * 1 = generic, 2 = pipelined tcgen05 */
 int nm_last_kernel_path(void);
+/* test hook of the exact-rounding path: error bound, per unit
+ * frame conditioning, under which the pipelined kernels queue a row's fp16
+ * direction inputs for exact resolution.  <= 0 restores the built-in bound;
+ * a huge value queues every above-horizon row (exercises the resolve path). */
+int nm_set_tw_margin(float delta);
+/* calibration dump of the pipelined eval kernel: like nm_eval (fp16 path),
+ * plus per row its fp32 fast-path [T.wi(6), T.wo(6)] and the two frames'
+ * conditioning factors (14 floats per row) */
+int nm_eval_debug_tw(const nm_material* m, int64_t n, const float* uv, const float* lod,
+                     int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+                     float* rgb_out, float* dbg_out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -200,6 +200,31 @@ class Pyramid:
         return np.sum(tex * wts[..., None], axis=-2, dtype=np.float64).astype(np.float32)
 
 
+class GatherPyramid(Pyramid):
+    """A pyramid whose texels live elsewhere (the 4K..15K pyramids of the
+    BASELINE configs, resident on the GPU): the same fetch as Pyramid.fetch
+    (latent.py:84-98) — float64 taps, weights and weighted sum, narrowed to
+    float32 — with the four taps of each query read through
+    ``gather(level, ys, xs) -> (..., 4, C) float32``."""
+
+    def __init__(self, shapes, gather, channels=LATENT_CHANNELS):
+        # zero-size stand-ins: taps() only reads each level's (H, W)
+        self.levels = [np.empty((h, w, 0), np.float32) for h, w in shapes]
+        self.gather = gather
+        self.channels = channels
+
+    def fetch(self, uv, level, u_rr):
+        uv = np.atleast_2d(np.asarray(uv, dtype=np.float64))
+        chosen = self.choose_level(np.broadcast_to(level, uv.shape[:-1]), u_rr)
+        z = np.empty(uv.shape[:-1] + (self.channels,), dtype=np.float32)
+        for lv in np.unique(chosen):
+            m = chosen == lv
+            xs, ys, wts = self.taps(int(lv), uv[m])
+            tex = np.asarray(self.gather(int(lv), ys, xs), np.float32)
+            z[m] = np.sum(tex * wts[..., None], axis=-2, dtype=np.float64)
+        return z, chosen
+
+
 def random_pyramid(rng, width, height, channels=LATENT_CHANNELS):
     """Synthetic latents, one standard_normal draw per level in order
     (the reference tests' generator, tests/test_latent.py:10-14)."""

@@ -121,6 +121,9 @@ SIGNATURES = {
     "nm_launch_count": (c_i64, []),
     "nm_set_kernel_path": (c_i32, [c_i32]),
     "nm_last_kernel_path": (c_i32, []),
+    "nm_set_tw_margin": (c_i32, [ctypes.c_float]),
+    "nm_eval_debug_tw": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p, c_float_p,
+                                 c_float_p, c_float_p, c_float_p, ctypes.c_void_p]),
 }
 
 _lib = None

@@ -100,6 +100,25 @@ int view_net(const nm_net_desc& d, const char* name, NetView& v) {
 // Pack one chain of layers.  The first layer takes an input vector with its
 // bias slot at index fan_in; later layers take the hi/lo split of the
 // previous padded activation plus the shared bias chunk.
+float h2f(uint16_t bits) {
+  __half_raw r;
+  r.x = bits;
+  return __half2float(__half(r));
+}
+
+// fp32 copy of one network in the reference's packed access order (the
+// fp16 weights widened exactly, or the fp32 master weights for `precise`).
+void append_w32(const NetView& v, bool precise, std::vector<float>& w32, MatParams& mp, int first) {
+  for (int l = 0; l < v.n_layers; ++l) {
+    LayerDesc& L = mp.layers[first + l];
+    L.fan_in = (uint16_t)v.fi[l];
+    L.w32_off = (uint32_t)w32.size();
+    const size_t cnt = (size_t)v.fo[l] * (v.fi[l] + 1);
+    for (size_t i = 0; i < cnt; ++i)
+      w32.push_back(precise ? v.weights[v.ofs[l] + i] : h2f(v.packed[v.ofs[l] + i]));
+  }
+}
+
 int pack_chain(const NetView& v, Packer& pk, MatParams& mp, int& n_layers, const char* name) {
   if (mp.precise) {
     // fp32 path: B = [W_hi | W_hi | W_lo] (+ bias chunk [b_hi, 0, b_lo, 0 ...]
@@ -221,12 +240,6 @@ int detect_fast_arch(const MatParams& mp, const NetView& bv, const NetView& sv,
   return -1;
 }
 
-float h2f(uint16_t bits) {
-  __half_raw r;
-  r.x = bits;
-  return __half2float(__half(r));
-}
-
 // Layers of the specialized kernels (see MatParams::fast_frame_off):
 // re-packed frame layer and BRDF first layer for the shared input chunks,
 // fp32 copy of the BRDF output layer for the FFMA2 path.
@@ -264,65 +277,6 @@ void fill_fast_layers(MatParams& mp, Packer& pk, const NetView& fv, const NetVie
   }
 }
 
-// Warp-tile layout (see MatParams::wk_blob).  Packs every specialized
-// layer into `wk` (fp16 B operands, then fp32 biases scaled by c^depth).
-void fill_warp_layers(MatParams& mp, Packer& wk, const NetView& fv, const NetView& bv,
-                      const NetView& sv) {
-  auto W = [](const NetView& v, int l, int n, int k) {  // fp16 bits of W_l[n][k] (k == fi: bias)
-    return v.packed[v.ofs[l] + (size_t)n * (v.fi[l] + 1) + k];
-  };
-  auto dense = [&](const NetView& v, int l, int n_pad) {  // K = fan_in (padded to 16), N = n_pad
-    const int fi = v.fi[l], fo = v.fo[l];
-    const uint32_t off = wk.append(n_pad, round_up(fi, 16) / 8);
-    for (int n = 0; n < fo; ++n)
-      for (int k = 0; k < fi; ++k) wk.set(off, n_pad, n, k, W(v, l, n, k));
-    return off;
-  };
-  // frame layer: input chunk 0 = [z 0-7, wi 8-10, 1 @ 11]
-  mp.wk_fr = wk.append(16, 2);
-  for (int n = 0; n < 12; ++n) {
-    for (int k = 0; k < 8; ++k) wk.set(mp.wk_fr, 16, n, k, W(fv, 0, n, k));
-    wk.set(mp.wk_fr, 16, n, 11, W(fv, 0, n, 8));
-  }
-  {  // BRDF layer 1 on [z | T.wi(6), T.wo(6), 1 @ 12]
-    const int fi = bv.fi[0], fo = bv.fo[0], n_pad = round_up(fo, 16);
-    mp.wk_b1z = wk.append(n_pad, 1);
-    mp.wk_b1t = wk.append(n_pad, 2);
-    for (int n = 0; n < fo; ++n) {
-      for (int k = 0; k < 8; ++k) wk.set(mp.wk_b1z, n_pad, n, k, W(bv, 0, n, k));
-      for (int k = 8; k < 20; ++k) wk.set(mp.wk_b1t, n_pad, n, k - 8, W(bv, 0, n, k));
-      wk.set(mp.wk_b1t, n_pad, n, 12, W(bv, 0, n, fi));
-    }
-  }
-  for (int l = 1; l < bv.n_layers - 1; ++l) mp.wk_bh[l - 1] = dense(bv, l, round_up(bv.fo[l], 16));
-  mp.wk_bo = dense(bv, bv.n_layers - 1, 8);
-  mp.wk_s1 = wk.append(round_up(sv.fo[0], 16), 2);  // [z 0-7, wi 8-10, 1 @ 11]
-  for (int n = 0; n < sv.fo[0]; ++n)
-    for (int k = 0; k <= 11; ++k) wk.set(mp.wk_s1, round_up(sv.fo[0], 16), n, k, W(sv, 0, n, k));
-  for (int l = 1; l < sv.n_layers - 1; ++l) mp.wk_sh[l - 1] = dense(sv, l, round_up(sv.fo[l], 16));
-  mp.wk_so = dense(sv, sv.n_layers - 1, 16);
-  // fp32 biases of layers >= 1, times c^l (the scaled-leaky activations)
-  auto bias = [&](const NetView& v, int l, int n_pad) {
-    while (wk.blob.size() % 8) wk.blob.push_back(0);
-    const uint32_t off = (uint32_t)(wk.blob.size() * 2);
-    const double sc = std::pow(kLeakyScale, l);
-    for (int n = 0; n < n_pad; ++n) {
-      const float b = n < v.fo[l] ? (float)(sc * (double)h2f(W(v, l, n, v.fi[l]))) : 0.f;
-      uint32_t u;
-      std::memcpy(&u, &b, 4);
-      wk.blob.push_back((uint16_t)(u & 0xFFFFu));
-      wk.blob.push_back((uint16_t)(u >> 16));
-    }
-    return off;
-  };
-  for (int l = 1; l < bv.n_layers - 1; ++l) mp.wk_bias_bh[l - 1] = bias(bv, l, round_up(bv.fo[l], 16));
-  mp.wk_bias_bo = bias(bv, bv.n_layers - 1, 8);
-  for (int l = 1; l < sv.n_layers - 1; ++l) mp.wk_bias_sh[l - 1] = bias(sv, l, round_up(sv.fo[l], 16));
-  mp.wk_bias_so = bias(sv, sv.n_layers - 1, 16);
-  while (wk.blob.size() % 8) wk.blob.push_back(0);
-  mp.wk_bytes = (uint32_t)(wk.blob.size() * 2);
-}
-
 }  // namespace
 
 struct nm_mlp {
@@ -338,7 +292,7 @@ struct nm_material {
   MatParams mp{};
   void* latent = nullptr;
   void* wblob = nullptr;
-  void* wkblob = nullptr;
+  void* w32 = nullptr;
   int64_t texels = 0;
   int brdf_width = 0, sampler_width = 0;
 };
@@ -349,8 +303,12 @@ const char* nm_last_error(void) { return t_err.c_str(); }
 int nm_version(void) { return NMQ_VERSION; }
 int64_t nm_launch_count(void) { return g_launches.load(); }
 int nm_last_kernel_path(void) { return g_last_path.load(); }
+int nm_set_tw_margin(float delta) {
+  g_tw_margin = delta;
+  return NM_OK;
+}
 int nm_set_kernel_path(int path) {
-  if (path < 0 || path > 3) return fail(NM_ERR_INVALID, "kernel path must be 0..3");
+  if (path < 0 || path > 2) return fail(NM_ERR_INVALID, "kernel path must be 0..2");
   g_kernel_path = path;
   return NM_OK;
 }
@@ -395,6 +353,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
 
   // --- networks ---------------------------------------------------------------
   Packer pk;
+  std::vector<float> w32;
   int nl = 0;
   mp.use_frames = d->use_frames ? 1 : 0;
   mp.n_frames = d->use_frames ? d->n_frames : 0;
@@ -416,6 +375,10 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     }
     mp.frame_layer = nl;
     if ((rc = pack_chain(fv, pk, mp, nl, "frame layer")) != NM_OK) { delete m; return rc; }
+    append_w32(fv, mp.precise, w32, mp, mp.frame_layer);
+    // frame layer [W | b] in fp32 for the sequential-FMA evaluation (mlp.py:207)
+    for (int n = 0; n < 6 * d->n_frames; ++n)
+      for (int k = 0; k <= 8; ++k) mp.fw[n][k] = w32[mp.layers[mp.frame_layer].w32_off + n * 9 + k];
   }
   const int brdf_in = d->use_frames ? 8 + 6 * d->n_frames : 14;
   mp.brdf_in = brdf_in;
@@ -439,6 +402,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     mp.brdf_first = nl;
     mp.brdf_count = bv.n_layers;
     if ((rc = pack_chain(bv, pk, mp, nl, "brdf decoder")) != NM_OK) { delete m; return rc; }
+    append_w32(bv, mp.precise, w32, mp, mp.brdf_first);
   }
   if (d->sampler.n_layers > 0) {
     if ((rc = view_net(d->sampler, "sampler decoder", sv)) != NM_OK) { delete m; return rc; }
@@ -450,6 +414,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     mp.samp_first = nl;
     mp.samp_count = sv.n_layers;
     if ((rc = pack_chain(sv, pk, mp, nl, "sampler decoder")) != NM_OK) { delete m; return rc; }
+    append_w32(sv, mp.precise, w32, mp, mp.samp_first);
   }
   for (int l = mp.brdf_first; l < mp.brdf_first + mp.brdf_count; ++l)
     m->brdf_width = m->brdf_width > mp.layers[l].n_pad ? m->brdf_width : mp.layers[l].n_pad;
@@ -458,11 +423,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
   if (mp.dmax < 16) mp.dmax = 16;
   if (mp.dmax == 48) mp.dmax = 64;  // TMEM regions are powers of two
   mp.fast_arch = mp.precise ? -1 : detect_fast_arch(mp, bv, sv, d);
-  Packer wk;
-  if (mp.fast_arch >= 0) {
-    fill_fast_layers(mp, pk, fv, bv);
-    fill_warp_layers(mp, wk, fv, bv, sv);
-  }
+  if (mp.fast_arch >= 0) fill_fast_layers(mp, pk, fv, bv);
   mp.wblob_bytes = (uint32_t)(pk.blob.size() * 2);
   if (mp.wblob_bytes > 200 * 1024) {
     delete m;
@@ -493,20 +454,19 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     delete m;
     return cuda_fail(e, "upload weights");
   }
-  if (mp.wk_bytes) {
-    if ((e = cudaMalloc(&m->wkblob, mp.wk_bytes)) != cudaSuccess ||
-        (e = cudaMemcpy(m->wkblob, wk.blob.data(), mp.wk_bytes, cudaMemcpyHostToDevice)) !=
-            cudaSuccess) {
-      cudaFree(m->latent);
-      cudaFree(m->wblob);
-      if (m->wkblob) cudaFree(m->wkblob);
-      delete m;
-      return cuda_fail(e, "upload warp-tile weights");
-    }
+  if (w32.empty()) w32.push_back(0.f);
+  if ((e = cudaMalloc(&m->w32, w32.size() * sizeof(float))) != cudaSuccess ||
+      (e = cudaMemcpy(m->w32, w32.data(), w32.size() * sizeof(float), cudaMemcpyHostToDevice)) !=
+          cudaSuccess) {
+    cudaFree(m->latent);
+    cudaFree(m->wblob);
+    if (m->w32) cudaFree(m->w32);
+    delete m;
+    return cuda_fail(e, "upload fp32 weights");
   }
   mp.latent = reinterpret_cast<const uint4*>(m->latent);
   mp.wblob = reinterpret_cast<const uint4*>(m->wblob);
-  mp.wk_blob = reinterpret_cast<const uint4*>(m->wkblob);
+  mp.w32 = reinterpret_cast<const float*>(m->w32);
   *out = m;
   return NM_OK;
 }
@@ -516,7 +476,7 @@ int nm_material_destroy(nm_material* m) {
   DeviceGuard guard(m->device);
   if (m->latent) cudaFree(m->latent);
   if (m->wblob) cudaFree(m->wblob);
-  if (m->wkblob) cudaFree(m->wkblob);
+  if (m->w32) cudaFree(m->w32);
   delete m;
   return NM_OK;
 }
@@ -583,6 +543,22 @@ int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
   DeviceGuard guard(m->device);
   if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
   return finish(m, launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream), "nm_eval");
+}
+
+int nm_eval_debug_tw(const nm_material* m, int64_t n, const float* uv, const float* lod,
+                     int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
+                     float* rgb_out, float* dbg_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !wo || !rgb_out || !dbg_out) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.wo = wo; a.rgb = rgb_out; a.dbg = dbg_out;
+  DeviceGuard guard(m->device);
+  const cudaError_t e = launch_fast(m->mp, kModeEval, a, (cudaStream_t)stream);
+  if (e == cudaErrorNotSupported) return fail(NM_ERR_UNSUPPORTED, "material has no pipelined kernel");
+  return finish(m, e, "nm_eval_debug_tw");
 }
 
 // Host-buffer eval.  Pinned (page-locked, UVA-mapped) buffers: zero-copy —

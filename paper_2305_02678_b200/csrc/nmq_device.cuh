@@ -249,16 +249,21 @@ __device__ __forceinline__ Frame frame_from_raw(const float* r) {
 
 // Both learned frames at once (neural.py:207-233) with packed fp32x2 math,
 // and the direction transforms T.wi, T.wo (neural.py:185-196):
-// ti = [t1.wi, b1.wi, n1.wi, t2.wi, b2.wi, n2.wi], same for to.  Per-lane
-// results equal frame_from_raw() + dot() exactly (same ops, same rounding).
-__device__ __forceinline__ void frames2_transform(const float* r, V3 wi, V3 wo, float (&ti)[6],
-                                                  float (&to)[6]) {
+// ti = [t1.wi, b1.wi, n1.wi, t2.wi, b2.wi, n2.wi], same for to.  Returns
+// each frame's conditioning kappa = 1 + |rt|_1 / |n x rt| (the fp32 error
+// of b and t grows as 1/|n x rt|), +inf near the reference's
+// degenerate-tangent branch or a vanishing normal (resolved exactly).
+__device__ __forceinline__ float2 frames2_transform(const float* r, V3 wi, V3 wo, float (&ti)[6],
+                                                    float (&to)[6]) {
   const V3x2 rn = {f2(r[0], r[6]), f2(r[1], r[7]), f2(r[2], r[8])};
   V3x2 rt = {f2(r[3], r[9]), f2(r[4], r[10]), f2(r[5], r[11])};
   const float2 l2 = dot2(rn, rn);
   const V3x2 n = scale2(rn, f2(rsqrtf(fmaxf(l2.x, 1e-24f)), rsqrtf(fmaxf(l2.y, 1e-24f))));
+  const float2 rt1 = __fadd2_rn(__fadd2_rn(f2(fabsf(rt.x.x), fabsf(rt.x.y)), f2(fabsf(rt.y.x), fabsf(rt.y.y))),
+                                f2(fabsf(rt.z.x), fabsf(rt.z.y)));
   V3x2 c = cross2(n, rt);
   float2 c2 = dot2(c, c);
+  const bool ill1 = c2.x < 1e-10f || l2.x < 1e-20f, ill2 = c2.y < 1e-10f || l2.y < 1e-20f;
   if (c2.x < 1e-16f || c2.y < 1e-16f) {  // |c| < 1e-8: degenerate tangent(s)
     if (c2.x < 1e-16f) {
       const V3 f = fallback_tangent(v3(n.x.x, n.y.x, n.z.x));
@@ -271,12 +276,15 @@ __device__ __forceinline__ void frames2_transform(const float* r, V3 wi, V3 wo, 
     c = cross2(n, rt);
     c2 = dot2(c, c);
   }
-  const V3x2 b = scale2(c, f2(rsqrtf(fmaxf(c2.x, 1e-24f)), rsqrtf(fmaxf(c2.y, 1e-24f))));
+  const float2 ic = f2(rsqrtf(fmaxf(c2.x, 1e-24f)), rsqrtf(fmaxf(c2.y, 1e-24f)));
+  const V3x2 b = scale2(c, ic);
   const V3x2 t = cross2(b, n);
   const float2 twi = dot2s(t, wi), bwi = dot2s(b, wi), nwi = dot2s(n, wi);
   const float2 two = dot2s(t, wo), bwo = dot2s(b, wo), nwo = dot2s(n, wo);
   ti[0] = twi.x; ti[1] = bwi.x; ti[2] = nwi.x; ti[3] = twi.y; ti[4] = bwi.y; ti[5] = nwi.y;
   to[0] = two.x; to[1] = bwo.x; to[2] = nwo.x; to[3] = two.y; to[4] = bwo.y; to[5] = nwo.y;
+  const float2 kap = __ffma2_rn(rt1, ic, f2(1.f, 1.f));
+  return f2(ill1 ? __int_as_float(0x7f800000) : kap.x, ill2 ? __int_as_float(0x7f800000) : kap.y);
 }
 
 // ---------------------------------------------------------------------------
@@ -401,6 +409,273 @@ __device__ __forceinline__ V3 proxy_sample(const Proxy& p, V3 wi, float u0, floa
   const V3 h = scale(g, rsqrtf(fmaxf(dot(g, g), 1e-24f)));
   const float d = 2.f * dot(wi, h);
   return v3(fmaf(d, h.x, -wi.x), fmaf(d, h.y, -wi.y), fmaf(d, h.z, -wi.z));
+}
+
+// ---------------------------------------------------------------------------
+// Exact-rounding helpers.  The reference's fp16 path rounds
+// every decoder input to fp16 once (mlp.py:205) after computing it in
+// float64 and narrowing to fp32 (latent.py:93-97, neural.py:282-287):
+// z = fp32(sum_k t_k w_k), T.w = fp32(f64 frames . w).  To reproduce those
+// fp16 values bit for bit the latent blend runs in float64 and the frame
+// transform is resolved in float64 wherever the fast fp32 value lies within
+// its error bound of an fp16 rounding midpoint.
+
+// fractional texel coordinate of one axis, float64 (latent.py:59-64): u*w is
+// exact in float64 for fp32 u, so fma(u, w, -0.5) == fl(u*w - 0.5)
+__device__ __forceinline__ double frac64(float u, int32_t w) {
+  const double x = fma((double)u, (double)w, -0.5);
+  return x - floor(x);
+}
+
+// bilinear weights [(1-fx)(1-fy), fx(1-fy), (1-fx)fy, fx fy] (latent.py:69-71)
+__device__ __forceinline__ void weights64(double fx, double fy, double (&w)[4]) {
+  const double gx = __dsub_rn(1.0, fx), gy = __dsub_rn(1.0, fy);
+  w[0] = __dmul_rn(gx, gy);
+  w[1] = __dmul_rn(fx, gy);
+  w[2] = __dmul_rn(gx, fy);
+  w[3] = __dmul_rn(fx, fy);
+}
+
+__device__ __forceinline__ double h2d_lo(uint32_t v) {
+  double d;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tcvt.f64.f16 %0, l;\n\t}" : "=d"(d) : "r"(v));
+  return d;
+}
+__device__ __forceinline__ double h2d_hi(uint32_t v) {
+  double d;
+  asm("{\n\t.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tcvt.f64.f16 %0, h;\n\t}" : "=d"(d) : "r"(v));
+  return d;
+}
+
+// z = fp32(((t0 w0 + t1 w1) + t2 w2) + t3 w3) with the reference's float64
+// rounding of every product and sum (numpy reduces the tap axis left to
+// right): bit-identical to latent.py:96.  FMA = true contracts each
+// product into its sum (one rounding less; the fp32 result differs only if
+// the float64 sum lies within 2^-53 of an fp32 rounding midpoint).
+template <bool FMA>
+__device__ __forceinline__ void blend64(const uint4 (&tex)[4], const double (&w)[4], float (&z)[8]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t v = (&tex[k].x)[c];
+      const double a = h2d_lo(v), b = h2d_hi(v);
+      if (k == 0) {
+        s0 = __dmul_rn(a, w[0]);
+        s1 = __dmul_rn(b, w[0]);
+      } else if (FMA) {
+        s0 = fma(a, w[k], s0);
+        s1 = fma(b, w[k], s1);
+      } else {
+        s0 = __dadd_rn(s0, __dmul_rn(a, w[k]));
+        s1 = __dadd_rn(s1, __dmul_rn(b, w[k]));
+      }
+    }
+    z[2 * c] = (float)s0;
+    z[2 * c + 1] = (float)s1;
+  }
+}
+
+// fp32 texels (the fp32 master pyramid of the reference's fp32 path)
+__device__ __forceinline__ void blend64_f32(const float4* lat, const int64_t (&idx)[4],
+                                            const double (&w)[4], float (&z)[8]) {
+  double s[8];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float4 a = __ldg(lat + 2 * idx[k]), b = __ldg(lat + 2 * idx[k] + 1);
+    const float t[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const double p = __dmul_rn((double)t[c], w[k]);
+      s[c] = k == 0 ? p : __dadd_rn(s[c], p);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 8; ++c) z[c] = (float)s[c];
+}
+
+// Exact fetch (latent.py:84-98): float64 weights and blend, fp32 result.
+__device__ __forceinline__ void fetch_exact(const MatParams& m, int level, float u, float v, const Taps& t,
+                                            float (&z)[8]) {
+  double w[4];
+  weights64(frac64(u, m.lv[level].w), frac64(v, m.lv[level].h), w);
+  if (m.texel_fp32) {
+    const int64_t idx[4] = {tap_index(t, 0), tap_index(t, 1), tap_index(t, 2), tap_index(t, 3)};
+    blend64_f32(reinterpret_cast<const float4*>(m.latent), idx, w, z);
+    return;
+  }
+  uint4 tex[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tex[k] = __ldg(m.latent + tap_index(t, k));
+  blend64<false>(tex, w, z);
+}
+
+// fp16 rounding of a pair (the decoder input rounding, mlp.py:205)
+__device__ __forceinline__ uint32_t pack_h2(float a, float b) {
+  const __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float2 unpack_h2(uint32_t v) {
+  return __half22float2(*reinterpret_cast<const __half2*>(&v));
+}
+
+// Frame layer on the CUDA cores in the reference's arithmetic: numpy's
+// fp32 `x @ W.T` (OpenBLAS sgemm: one fused multiply-add per k, k = 0..7,
+// in order; pinned by tests/test_oracle_golden.py) then `+ b` (mlp.py:207).
+// x = the fp16 latent code (4 packed pairs).
+__device__ __forceinline__ void frame_raw_seq(const MatParams& m, const uint32_t (&zh)[4], int n_out,
+                                              float (&raw)[12]) {
+  float x[8];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const float2 f = unpack_h2(zh[c]);
+    x[2 * c] = f.x;
+    x[2 * c + 1] = f.y;
+  }
+#pragma unroll
+  for (int j = 0; j < 12; ++j) {
+    if (j < n_out) {
+      float acc = x[0] * m.fw[j][0];
+#pragma unroll
+      for (int k = 1; k < 8; ++k) acc = __fmaf_rn(x[k], m.fw[j][k], acc);
+      raw[j] = __fadd_rn(acc, m.fw[j][8]);
+    } else {
+      raw[j] = 0.f;
+    }
+  }
+}
+
+struct D3 {
+  double x, y, z;
+};
+__device__ __forceinline__ double ddot(D3 a, D3 b) { return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x)); }
+__device__ __forceinline__ D3 dcross(D3 a, D3 b) {
+  return {fma(a.y, b.z, -a.z * b.y), fma(a.z, b.x, -a.x * b.z), fma(a.x, b.y, -a.y * b.x)};
+}
+__device__ __forceinline__ D3 dscale(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+
+// One learned frame in float64 (neural.py:207-233, geom.py:82-89) and the
+// transform of wi / wo (neural.py:185-196), rounded to fp32 as the
+// reference's `inp.astype(np.float32)` does (neural.py:287).  The float64
+// arithmetic differs from numpy's by ~1e-16 relative, far below the fp32
+// rounding that follows.
+__device__ __forceinline__ void frame_tw64(const float* raw, V3 wi, V3 wo, float (&ti)[3], float (&to)[3]) {
+  const D3 rn = {raw[0], raw[1], raw[2]};
+  D3 rt = {raw[3], raw[4], raw[5]};
+  const D3 n = dscale(rn, rsqrt(fmax(ddot(rn, rn), 1e-24)));
+  D3 c = dcross(n, rt);
+  double c2 = ddot(c, c);
+  if (c2 < 1e-16) {  // |c| < 1e-8: fallback tangent n x e_argmin|n| (first index on ties)
+    const double ax = fabs(n.x), ay = fabs(n.y), az = fabs(n.z);
+    const D3 e = (ax <= ay && ax <= az) ? D3{1.0, 0.0, 0.0} : (ay <= az ? D3{0.0, 1.0, 0.0} : D3{0.0, 0.0, 1.0});
+    const D3 f = dcross(n, e);
+    rt = dscale(f, rsqrt(ddot(f, f)));
+    c = dcross(n, rt);
+    c2 = ddot(c, c);
+  }
+  const D3 b = dscale(c, rsqrt(fmax(c2, 1e-24)));
+  const D3 t = dcross(b, n);
+  const D3 di = {wi.x, wi.y, wi.z}, dout = {wo.x, wo.y, wo.z};
+  ti[0] = (float)ddot(t, di); ti[1] = (float)ddot(b, di); ti[2] = (float)ddot(n, di);
+  to[0] = (float)ddot(t, dout); to[1] = (float)ddot(b, dout); to[2] = (float)ddot(n, dout);
+}
+
+// The decoder's direction inputs, exactly as the reference rounds them:
+// x16 = fp16 pairs of [T.wi (3 per frame), T.wo (3 per frame)] for n_frames
+// frames, from the latent code's fp16 pairs.
+__device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
+                                         uint32_t (&x16)[6]) {
+  float raw[12];
+  frame_raw_seq(m, zh, 6 * m.n_frames, raw);
+  float ti[6], to[6];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    if (f < m.n_frames) {
+      float a[3], b[3];
+      frame_tw64(raw + 6 * f, wi, wo, a, b);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        ti[3 * f + k] = a[k];
+        to[3 * f + k] = b[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ti[3 * f + k] = to[3 * f + k] = 0.f;
+    }
+  }
+  if (m.n_frames == 2) {
+    x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], ti[3]); x16[2] = pack_h2(ti[4], ti[5]);
+    x16[3] = pack_h2(to[0], to[1]); x16[4] = pack_h2(to[2], to[3]); x16[5] = pack_h2(to[4], to[5]);
+  } else {  // [T.wi(3), T.wo(3)]
+    x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], to[0]); x16[2] = pack_h2(to[1], to[2]);
+    x16[3] = x16[4] = x16[5] = 0u;
+  }
+}
+
+// Warp-cooperative re-evaluation of one query's BRDF decoder on the CUDA
+// cores (fp32, the reference's fused_forward arithmetic up to summation
+// order: mlp.py:196-208).  All 32 lanes call it with the same `src` lane;
+// that lane holds the query's fp16 decoder input (in16: brdf_in values as
+// packed pairs).  Lane j owns hidden units j and j + 32.  Returns the raw
+// outputs y[0..out) on every lane.
+__device__ __forceinline__ void brdf_simt_warp(const MatParams& m, const uint32_t (&in16)[10], int src,
+                                               float (&y)[6]) {
+  const int lane = threadIdx.x & 31;
+  float h0 = 0.f, h1 = 0.f;  // this lane's activations (units lane, lane + 32)
+  const int nl = m.brdf_count;
+  for (int l = 0; l < nl; ++l) {
+    const LayerDesc& L = m.layers[m.brdf_first + l];
+    const int fi = L.fan_in, fo = L.out;
+    const float* W = m.w32 + L.w32_off;  // [fo][fi + 1]
+    const bool last = l == nl - 1;
+    if (!last) {
+      float a0 = 0.f, a1 = 0.f;
+      const int j0 = lane, j1 = lane + 32;
+      if (l == 0) {  // fan-in <= 20 (host-validated)
+#pragma unroll
+        for (int c = 0; c < 10; ++c) {
+          const float2 f = unpack_h2(__shfl_sync(0xffffffffu, in16[c], src));
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int k = 2 * c + e;
+            const float xk = e ? f.y : f.x;
+            if (k < fi) {
+              if (j0 < fo) a0 = __fmaf_rn(xk, __ldg(W + (size_t)j0 * (fi + 1) + k), a0);
+              if (j1 < fo) a1 = __fmaf_rn(xk, __ldg(W + (size_t)j1 * (fi + 1) + k), a1);
+            }
+          }
+        }
+      } else {
+        for (int k = 0; k < fi; ++k) {
+          const float xk = __shfl_sync(0xffffffffu, k < 32 ? h0 : h1, k & 31);
+          if (j0 < fo) a0 = __fmaf_rn(xk, __ldg(W + (size_t)j0 * (fi + 1) + k), a0);
+          if (j1 < fo) a1 = __fmaf_rn(xk, __ldg(W + (size_t)j1 * (fi + 1) + k), a1);
+        }
+      }
+      if (j0 < fo) a0 += __ldg(W + (size_t)j0 * (fi + 1) + fi);
+      if (j1 < fo) a1 += __ldg(W + (size_t)j1 * (fi + 1) + fi);
+      if (L.act) {
+        a0 = a0 >= 0.f ? a0 : kLeaky * a0;
+        a1 = a1 >= 0.f ? a1 : kLeaky * a1;
+      }
+      h0 = j0 < fo ? a0 : 0.f;
+      h1 = j1 < fo ? a1 : 0.f;
+    } else {
+#pragma unroll
+      for (int o = 0; o < 6; ++o) {
+        float p = 0.f;
+        if (o < fo) {
+          if (lane < fi) p = h0 * __ldg(W + (size_t)o * (fi + 1) + lane);
+          if (lane + 32 < fi) p = __fmaf_rn(h1, __ldg(W + (size_t)o * (fi + 1) + lane + 32), p);
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) p += __shfl_xor_sync(0xffffffffu, p, d);
+          p += __ldg(W + (size_t)o * (fi + 1) + fi);
+        }
+        y[o] = p;
+      }
+    }
+  }
 }
 
 }  // namespace dev

@@ -1,5 +1,5 @@
 // nmq_fast.cu — pipelined, architecture-specialized fused query kernels
-// (the coherent per-material path; see DESIGN.md §3-4).
+// (the coherent per-material path; see DESIGN.md §3-5).
 //
 // One persistent CTA per SM holds G tile groups of 128 threads (thread r of
 // a group owns row r of its tiles = TMEM lane r).  Each group keeps NS tiles
@@ -11,7 +11,9 @@
 // so while slot s's MMA runs on the tensor core the group's warps do the
 // SIMT stage of slot s+1.  A tile's stages (eval, 2x32):
 //
-//     0  frame layer D -> frames, T.wi, T.wo (input chunk 1) -> BRDF layer 1
+//     0  frame layer D -> frames, T.wi, T.wo (input chunk 1) -> BRDF layer 1;
+//        rows whose T.w may round differently from the reference go to the
+//        group's resolve ring, which is drained 128 rows at a time
 //     1  scaled leaky + hi/lo split                           -> BRDF layer 2
 //     2  BRDF output layer (CUDA cores), rgb store; blend the slot's next
 //        tile's prefetched texels -> input chunk 0 -> its frame layer
@@ -23,17 +25,29 @@
 //
 // Inputs (uv, lod, u_rr, wi, wo, u3) reach SMEM by 1-D TMA bulk copies two
 // tiles ahead per slot; each thread's four 16-byte texel loads for the slot's
-// next tile are issued at stage 0 (L1-cached LDG.128) and blended at the
-// last stage.
+// next tile are issued at stage 0 (L1-cached LDG.128) and blended — in
+// float64, exactly as latent.py:96 — at the last stage.
 //
 // Hidden activations use the scaled-leaky trick a~ = y + k|y| (k = 99/101)
 // = c * leaky(y), c = 1 + k: the scale propagates through the (positively
 // homogeneous) network and is undone on the raw outputs; layer biases are
 // multiplied by c^depth inside the MMA via an fp16 (hi, lo) pair in the TMEM
 // bias chunk.  The exact hi/lo split is F2FP + FHFMA (a - f32(hi)) + F2FP.
+//
+// Exact rounding of the decoder's direction inputs.  The
+// reference computes T.wi / T.wo in float64 from the frame layer's fp32
+// outputs, narrows to fp32 and rounds to fp16 (neural.py:282-287).  The
+// tensor-core frame layer and the fp32 frames here are within a small,
+// conditioning-scaled bound of those values; a row whose fast value lies
+// within that bound of an fp16 rounding midpoint is queued (input row, fp16
+// latent code, fast fp16 inputs) and later resolved in the reference's own
+// arithmetic (frame_raw_seq + frame_tw64); if its fp16 inputs differ, the
+// warp re-evaluates the BRDF decoder for it on the CUDA cores (fp32) and
+// overwrites its output.
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <utility>
 #include "tc.cuh"
 #include "nmq_device.cuh"
@@ -50,39 +64,10 @@ using namespace dev;
 #define NMQ_G_EVAL 7
 #endif
 #ifndef NMQ_G_SAMPLE
-#define NMQ_G_SAMPLE 7  // with SMEM texel staging (NMQ_TEX_SMEM) + all-warps MMA wait; 5 with register prefetch
+#define NMQ_G_SAMPLE 7  // with SMEM texel staging (NMQ_TEX_SMEM); 5 with register prefetch
 #endif
 #ifndef NMQ_G_QUERY
 #define NMQ_G_QUERY 5
-#endif
-// MMA completion, per mode (bit 1 << MODE): every warp sleeps on the
-// mbarrier itself (try_wait with a suspend hint) instead of one polling warp
-// releasing the other three through a named barrier.  Measured on B200:
-// eval +3 %, query +4 %; sample+pdf -1 % at G = 6, +1 % at G = 7 (which the
-// freed named barriers allow).
-#ifndef NMQ_WAIT_ALL_MODES
-#define NMQ_WAIT_ALL_MODES ((1 << kModeEval) | (1 << kModeQuery) | (1 << kModeSamplePdf))
-#endif
-// Hidden-layer biases: A operand of the bias k-step from SMEM (4 KB tile per
-// depth, every row (beta_hi, beta_lo, 0...)) instead of a 32-column TMEM
-// chunk, leaving all 512 TMEM columns to the tile groups.
-#ifndef NMQ_BIAS_SMEM
-#define NMQ_BIAS_SMEM 0
-#endif
-constexpr bool kBiasSmem = NMQ_BIAS_SMEM != 0;
-// MMA issue: each warp arrives on an issue mbarrier (bar + 1, count 4) after
-// its TMEM stores; only the issuing thread (and the TMA-refill thread)
-// waits, instead of a 128-thread named barrier.
-#ifndef NMQ_ISS_MBAR
-#define NMQ_ISS_MBAR 0
-#endif
-constexpr bool kIssMbar = NMQ_ISS_MBAR != 0;
-constexpr uint32_t kBiasTile = 4096;  // bytes per bias depth (128 rows x K 16 fp16)
-#ifndef NMQ_EVAL_OUT_MMA
-#define NMQ_EVAL_OUT_MMA 0  // eval: BRDF output layer on the tensor core (see kOM)
-#endif
-#ifndef NMQ_EVAL2
-#define NMQ_EVAL2 0  // eval in two stages per tile (see kE2)
 #endif
 #ifndef NMQ_PDL
 #define NMQ_PDL 1  // programmatic dependent launch (prologue overlaps the previous kernel's tail): C2 +4 %
@@ -92,11 +77,28 @@ constexpr uint32_t kBiasTile = 4096;  // bytes per bias depth (128 rows x K 16 f
 #endif
 
 constexpr float kLk = 0.98019802570343017578f;  // fp32(99/101)
+#ifndef NMQ_X_NORESOLVE
+#define NMQ_X_NORESOLVE 0
+#endif
+#ifndef NMQ_X_NOCHECK
+#define NMQ_X_NOCHECK 0
+#endif
+#ifndef NMQ_EARLY_PREFETCH
+#define NMQ_EARLY_PREFETCH 1
+#endif
+#ifndef NMQ_X_NOAPPEND
+#define NMQ_X_NOAPPEND 0
+#endif
+#ifndef NMQ_X_F32BLEND
+#define NMQ_X_F32BLEND 0
+#endif
+constexpr int kRing = 384;  // resolve ring entries per group (3 batches: see the drain rule)
 
 struct FastConsts {
   uint32_t beta[4];  // fp16 (hi | lo << 16) of c^j
   float inv_brdf;    // 1 / c^(brdf leaky layers)
   float inv_samp;    // 1 / c^(sampler leaky layers)
+  float tw_delta;    // error bound of the fast T.w per unit conditioning
 };
 
 template <int MODE>
@@ -118,6 +120,13 @@ struct alignas(16) InBuf {
   float u3[Need<MODE>::u3 ? 3 * kTile : 4];
 };
 
+// per-group resolve ring (SoA)
+struct alignas(16) Ring {
+  uint32_t z16[kRing][4];  // fp16 latent code
+  uint32_t x16[kRing][6];  // fast fp16 [T.wi, T.wo]
+  int32_t row[kRing];      // absolute input row
+};
+
 template <int... I, class F>
 __device__ __forceinline__ void sfor_impl(std::integer_sequence<int, I...>, F&& f) {
   (f(std::integral_constant<int, I>{}), ...);
@@ -126,6 +135,12 @@ __device__ __forceinline__ void sfor_impl(std::integer_sequence<int, I...>, F&& 
 template <int N, class F>
 __device__ __forceinline__ void sfor(F&& f) {
   sfor_impl(std::make_integer_sequence<int, N>{}, f);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
 }
 
 __device__ __forceinline__ void split_scaled(uint32_t ra, uint32_t rb, uint32_t& hi, uint32_t& lo) {
@@ -151,65 +166,40 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Does an fp16 rounding midpoint lie within +-d of either value of the pair?
+// (their fp16 roundings of v + d and v - d differ)
+__device__ __forceinline__ uint32_t near_mid2(float a, float b, float2 d) {
+  const float2 v = make_float2(a, b);
+  const float2 up = __ffma2_rn(d, make_float2(1.f, 1.f), v);
+  const float2 dn = __ffma2_rn(d, make_float2(-1.f, -1.f), v);
+  return pack2(up.x, up.y) ^ pack2(dn.x, dn.y);
+}
+
 // Group-wide constants.
 struct GG {
   uint32_t bias0;   // TMEM bias chunk j at bias0 + 8j (lane 0)
-  uint64_t bias_desc;  // kBiasSmem: SMEM descriptor of bias tile 0 (tile j at + j * kBiasTile)
   uint64_t desc0;   // SMEM descriptor of the weight blob base (SBO = 128)
-  uint32_t bar_id;   // named barrier of the group (before every MMA issue)
-  uint32_t done_id;  // named barrier: MMA completion, released by the polling warp
-  int r;             // row of this thread in the group's tiles
+  uint32_t bar_id;  // named barrier of the group (before every MMA issue)
+  int r;            // row of this thread in the group's tiles
 };
 
-// MMA completion: one warp (PW) polls the mbarrier and releases the other
-// three, which sleep on a named barrier (one instruction each, no spinning).
-template <int PW, bool ALL>
-__device__ __forceinline__ void mma_wait(const GG& g, uint64_t* bar, uint32_t& ph) {
-  if constexpr (ALL) {  // every warp sleeps on the mbarrier itself
-    tc::mbar_wait(bar, ph);
-  } else if ((g.r >> 5) == PW) {
-    tc::mbar_wait(bar, ph);
-    asm volatile("bar.arrive %0, %1;" ::"r"(g.done_id), "r"(128) : "memory");
-  } else {
-    tc::named_bar(g.done_id, 128);
-  }
+// MMA completion: every warp sleeps on the mbarrier (try_wait with a suspend hint).
+__device__ __forceinline__ void mma_wait(uint64_t* bar, uint32_t& ph) {
+  tc::mbar_wait(bar, ph);
   ph ^= 1u;
   tc::tc_fence_after();
-}
-
-// The bias k-step of a hidden-input layer: A = bias chunk j (TMEM or SMEM).
-__device__ __forceinline__ void bias_mma(const GG& g, uint32_t d_tmem, int j, uint64_t b_desc,
-                                         uint32_t idesc) {
-  if constexpr (kBiasSmem)
-    tc::mma_ss(d_tmem, g.bias_desc + (uint64_t)((j * kBiasTile) >> 4), b_desc, idesc, 1);
-  else
-    tc::mma_ts(d_tmem, g.bias0 + 8 * j, b_desc, idesc, 1);
 }
 
 // One MMA layer: the group's 128 threads finish their TMEM stores and meet
 // at the group barrier; lane 0 of warp LW issues KA k-steps of A (TMEM) x B
 // (SMEM weights at b_off), + the bias chunk when HID, and commits to `bar`.
 // `hook` then runs on every thread (TMA refills after the barrier).
-// Issue sync: the group's TMEM stores done before lane 0 of warp LW issues.
-// Returns after the named barrier (all threads) or after this warp's arrive.
-template <bool IM, int LW>
-__device__ __forceinline__ void issue_sync(const GG& g, uint64_t* bar, uint32_t ph) {
+template <int N, int KA, bool HID, int LW, class F>
+__device__ __forceinline__ void mma_issue(const GG& g, uint32_t d_tmem, uint32_t a_tmem,
+                                          uint32_t b_off, int bias_chunk, uint64_t* bar, F&& hook) {
   tc::tmem_st_wait();
   tc::tc_fence_before();
-  if constexpr (IM) {
-    __syncwarp();
-    if ((g.r & 31) == 0) tc::mbar_arrive(bar + 1);
-    if (g.r == 32 * LW) tc::mbar_wait(bar + 1, ph);
-  } else {
-    tc::named_bar(g.bar_id, 128);
-  }
-}
-
-template <bool IM, int N, int KA, bool HID, int LW, class F>
-__device__ __forceinline__ void mma_issue(const GG& g, uint32_t d_tmem, uint32_t a_tmem,
-                                          uint32_t b_off, int bias_chunk, uint64_t* bar, uint32_t ph,
-                                          F&& hook) {
-  issue_sync<IM, LW>(g, bar, ph);
+  tc::named_bar(g.bar_id, 128);
   if (g.r == 32 * LW) {
     tc::tc_fence_after();
     constexpr uint32_t idesc = tc::idesc_f16(128, N);
@@ -218,7 +208,7 @@ __device__ __forceinline__ void mma_issue(const GG& g, uint32_t d_tmem, uint32_t
     const uint64_t d = g.desc0 + ((uint64_t)(lbo >> 4) << 16) + (b_off >> 4);
 #pragma unroll
     for (int s = 0; s < KA; ++s) tc::mma_ts(d_tmem, a_tmem + 8 * s, d + ((s * 2 * lbo) >> 4), idesc, s > 0);
-    if constexpr (HID) bias_mma(g, d_tmem, bias_chunk, d + ((KA * 2 * lbo) >> 4), idesc);
+    if constexpr (HID) tc::mma_ts(d_tmem, g.bias0 + 8 * bias_chunk, d + ((KA * 2 * lbo) >> 4), idesc, 1);
     tc::mma_commit(bar);
   }
   hook();
@@ -227,39 +217,15 @@ struct NoOp {
   __device__ void operator()() const {}
 };
 
-// Eval (two-stage tiles): the last hidden BRDF layer of tile t (A -> D, KA
-// k-steps + bias chunk) and the frame layer of tile t+1 (X -> Y) issued
-// together — one barrier, one commit.
-template <int N, int KA, int LW>
-__device__ __forceinline__ void mma_issue_hid_frame(const GG& g, uint32_t d_tmem, uint32_t a_tmem,
-                                                    uint32_t b_off, int bias_chunk, bool frame,
-                                                    uint32_t y_tmem, uint32_t x_tmem, uint32_t frame_off,
-                                                    uint64_t* bar) {
+// Query: the frame layer (N = 16 into F) and the sampler's first layer (N =
+// SW into E) both read input chunk 0 — one barrier, one commit.
+template <int SW, int LW>
+__device__ __forceinline__ void mma_issue_first2(const GG& g, uint32_t f_tmem, uint32_t e_tmem,
+                                                 uint32_t a_tmem, uint32_t frame_off, uint32_t s1_off,
+                                                 uint64_t* bar) {
   tc::tmem_st_wait();
   tc::tc_fence_before();
   tc::named_bar(g.bar_id, 128);
-  if (g.r == 32 * LW) {
-    tc::tc_fence_after();
-    constexpr uint32_t idesc = tc::idesc_f16(128, N);
-    constexpr uint32_t lbo = N * 16;
-    const uint64_t d = g.desc0 + ((uint64_t)(lbo >> 4) << 16) + (b_off >> 4);
-#pragma unroll
-    for (int s = 0; s < KA; ++s) tc::mma_ts(d_tmem, a_tmem + 8 * s, d + ((s * 2 * lbo) >> 4), idesc, s > 0);
-    bias_mma(g, d_tmem, bias_chunk, d + ((KA * 2 * lbo) >> 4), idesc);
-    if (frame)
-      tc::mma_ts(y_tmem, x_tmem, g.desc0 + ((uint64_t)((16 * 16) >> 4) << 16) + (frame_off >> 4),
-                 tc::idesc_f16(128, 16), 0);
-    tc::mma_commit(bar);
-  }
-}
-
-// Query: the frame layer (N = 16 into F) and the sampler's first layer (N =
-// SW into E) both read input chunk 0 — one barrier, one commit.
-template <bool IM, int SW, int LW>
-__device__ __forceinline__ void mma_issue_first2(const GG& g, uint32_t f_tmem, uint32_t e_tmem,
-                                                 uint32_t a_tmem, uint32_t frame_off, uint32_t s1_off,
-                                                 uint64_t* bar, uint32_t ph) {
-  issue_sync<IM, LW>(g, bar, ph);
   if (g.r == 32 * LW) {
     tc::tc_fence_after();
     tc::mma_ts(f_tmem, a_tmem, g.desc0 + ((uint64_t)((16 * 16) >> 4) << 16) + (frame_off >> 4),
@@ -346,9 +312,8 @@ __device__ __forceinline__ void out_layer_simt(uint32_t dl, const MatParams& mp,
 
 // Stage one tile's inputs into `ib`: TMA bulk copies for full tiles (issued
 // by one thread), direct per-row copies for the partial last tile.
-// Returns true if TMA was used (consumers then wait on `bar`).
 template <int MODE>
-__device__ __forceinline__ bool stage_inputs(const QueryArgs& a, int64_t base, int64_t n, int tile,
+__device__ __forceinline__ void stage_inputs(const QueryArgs& a, int64_t base, int64_t n, int tile,
                                              InBuf<MODE>& ib, uint64_t* bar, int r, bool issuer) {
   const int64_t q0 = base + (int64_t)tile * kTile;
   if ((int64_t)tile * kTile + kTile <= n) {
@@ -367,7 +332,7 @@ __device__ __forceinline__ bool stage_inputs(const QueryArgs& a, int64_t base, i
       if constexpr (Need<MODE>::u3)
         tc::tma_load_1d(tc::smem_u32(ib.u3), a.u3 + 3 * q0, kTile * 12, bar);
     }
-    return true;
+    return;
   }
   const int64_t q = q0 + r;
   const bool v = (int64_t)tile * kTile + r < n;
@@ -381,14 +346,13 @@ __device__ __forceinline__ bool stage_inputs(const QueryArgs& a, int64_t base, i
     if constexpr (Need<MODE>::wo) ib.wo[3 * r + k] = v ? a.wo[3 * q + k] : (k == 2 ? 1.f : 0.f);
     if constexpr (Need<MODE>::u3) ib.u3[3 * r + k] = v ? a.u3[3 * q + k] : 0.f;
   }
-  return false;
 }
 
-// Texel prefetch into registers: level + taps of one row and the 4 texel
-// loads (LDG.128, L1-cached: the coarse pyramid levels live in L1).
+// Texel prefetch: level + taps of one row and its 4 texel loads (LDG.128,
+// L1-cached: the coarse pyramid levels live in L1).  The bilinear weights
+// are recomputed in float64 from the row's uv when the texels are blended.
 struct TexPrefetch {
   uint4 tex[4];
-  float fx, fy;
   int level;
 };
 
@@ -400,15 +364,13 @@ __device__ __forceinline__ void prefetch_texels(const MatParams& mp, const Query
   const float lod = a.lod_stride ? ib.lod[r] : lod0;
   p.level = choose_level(mp, lod, ib.urr[r]);
   const Taps t = make_taps(mp, p.level, u, v);
-  p.fx = t.fx;
-  p.fy = t.fy;
 #pragma unroll
   for (int k = 0; k < 4; ++k) p.tex[k] = __ldg(mp.latent + tap_index(t, k));
 }
 
 // SMEM variant (TS): the four texels go to this row's 64-byte slot in SMEM
 // by cp.async (LDGSTS, L1-allocating) — no registers held across the MLP
-// chain; only (fx, fy, level) stay live.
+// chain; only the level stays live.
 template <int MODE>
 __device__ __forceinline__ void prefetch_texels_smem(const MatParams& mp, const QueryArgs& a,
                                                      const InBuf<MODE>& ib, int r, float lod0,
@@ -417,8 +379,6 @@ __device__ __forceinline__ void prefetch_texels_smem(const MatParams& mp, const 
   const float lod = a.lod_stride ? ib.lod[r] : lod0;
   p.level = choose_level(mp, lod, ib.urr[r]);
   const Taps t = make_taps(mp, p.level, u, v);
-  p.fx = t.fx;
-  p.fy = t.fy;
 #pragma unroll
   for (int k = 0; k < 4; ++k) tc::cp_async16(row_smem + 16 * k, mp.latent + tap_index(t, k));
   tc::cp_async_commit();
@@ -433,12 +393,24 @@ __device__ __forceinline__ void land_texels_smem(uint32_t row_smem, TexPrefetch&
                  : "memory");
 }
 
-// blended latent code of one row, packed fp16 pairs (the MLP input rounding)
-__device__ __forceinline__ void blend_pack(const TexPrefetch& p, uint32_t (&zp)[4]) {
-  float2 z[4];
-  blend4x2(z, p.tex, p.fx, p.fy);
+// Blended latent code of one row as packed fp16 pairs (the MLP input
+// rounding): float64 weights and blend, as latent.py:93-97.
+template <int MODE>
+__device__ __forceinline__ void blend_pack(const MatParams& mp, const TexPrefetch& p, const InBuf<MODE>& ib,
+                                           int r, uint32_t (&zp)[4]) {
+  const LevelDesc L = mp.lv[p.level];
+  double w[4];
+  weights64(frac64(ib.uv[2 * r], L.w), frac64(ib.uv[2 * r + 1], L.h), w);
+  float z[8];
+#if NMQ_X_F32BLEND
+  float2 z2[4];
+  blend4x2(z2, p.tex, (float)w[1] + (float)w[3], (float)w[2] + (float)w[3]);
+  for (int c = 0; c < 4; ++c) { z[2*c] = z2[c].x; z[2*c+1] = z2[c].y; }
+#else
+  blend64<true>(p.tex, w, z);
+#endif
 #pragma unroll
-  for (int c = 0; c < 4; ++c) zp[c] = pack2(z[c].x, z[c].y);
+  for (int c = 0; c < 4; ++c) zp[c] = pack2(z[2 * c], z[2 * c + 1]);
 }
 
 // Per-slot state (registers; every index is compile-time after unrolling).
@@ -458,49 +430,72 @@ struct SlotSt {
   TexPrefetch nx;   // texels of the slot's next tile
 };
 
+// Resolve up to 128 ring entries [head, head + cnt): thread r takes entry
+// head + r, recomputes its direction inputs in the reference's arithmetic and,
+// where an fp16 value differs from the fast one, the warp re-evaluates the
+// decoder for that row and overwrites its outputs.  Every thread of the
+// group calls it (warp-collective shuffles inside).
+__device__ __noinline__ void resolve_batch(const MatParams& mp, const QueryArgs& a, const Ring& ring,
+                                           uint32_t head, uint32_t cnt, int r, bool seg_out) {
+  const bool act = (uint32_t)r < cnt;
+  const uint32_t slot = (head + (uint32_t)r) % (uint32_t)kRing;
+  uint32_t zh[4] = {0u, 0u, 0u, 0u}, xe[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+  int32_t row = 0;
+  bool mism = false;
+  if (act) {
+    row = ring.row[slot];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) zh[c] = ring.z16[slot][c];
+    const V3 wi = ldg3(a.wi, row), wo = ldg3(a.wo, row);
+    tw_exact(mp, zh, wi, wo, xe);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) mism |= xe[c] != ring.x16[slot][c];
+  }
+  uint32_t mm = __ballot_sync(0xffffffffu, mism);
+  while (mm) {
+    const int src = __ffs(mm) - 1;
+    mm &= mm - 1;
+    const uint32_t in16[10] = {zh[0], zh[1], zh[2], zh[3], xe[0], xe[1], xe[2], xe[3], xe[4], xe[5]};
+    float y[6];
+    brdf_simt_warp(mp, in16, src, y);
+    if ((r & 31) == src) {
+      const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + row) : (int64_t)row;
+      // queued rows are above the horizon (below it the output is 0 either way)
+      stg3(a.rgb, q, v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])));
+      if (mp.albedo && a.albedo) stg3(a.albedo, q, v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f)));
+    }
+  }
+}
+
 template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG>
 __global__ void __launch_bounds__(G * 128, 1)
 fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
             const __grid_constant__ FastConsts fc) {
   extern __shared__ __align__(128) uint8_t smem[];
-  __shared__ uint64_t mma_bar[G][NS][2];  // [0] MMA completion, [1] issue (kIssMbar)
+  __shared__ uint64_t mma_bar[G][NS];  // MMA completion
   __shared__ uint64_t in_bar[G][NS][2];
   __shared__ uint64_t w_bar;  // weights staged by TMA
   __shared__ uint32_t tbase_sh;
+  __shared__ uint32_t ring_tail[G];  // resolve ring: entries appended so far (group counter)
   constexpr bool kBrdf = Need<MODE>::brdf, kSamp = Need<MODE>::samp;
   // stage layout of one tile (see the file comment)
   // query: the sampler's first layer reads the same input chunk 0 as the
   // frame layer, so both are issued together (its D in a third region E) and
   // the sampler chain starts at the BRDF output stage: one round trip less
   constexpr bool kQM = kBrdf && kSamp;
-  // eval, two stages per tile (NMQ_EVAL2): tile t's output layer runs in
-  // tile t+1's first stage, and tile t+1's frame layer is issued with tile
-  // t's last hidden layer — 2 MMA round trips per tile instead of 3, for
-  // 32 more TMEM columns per group (X: next tile's input chunks, Y: its
-  // frame-layer D)
-  constexpr bool kE2 = NMQ_EVAL2 && MODE == kModeEval && NS == 1 && BNH == 2 && !TS;
-  // eval (NMQ_EVAL_OUT_MMA): the BRDF output layer on the tensor core too
-  // (hi/lo split of the last hidden layer, N = 16 MMA, read back one stage later)
-  constexpr bool kOM = NMQ_EVAL_OUT_MMA && MODE == kModeEval && !kE2;
   constexpr int kOutB = kBrdf ? BNH : -1;                   // BRDF output stage
-  constexpr int kOutR = kOM ? BNH + 1 : kOutB;              // BRDF output read back
   constexpr int kS0 = kBrdf ? (kQM ? BNH : BNH + 1) : 0;    // stage issuing sampler layer 2
-  constexpr int kFinal = kSamp ? kS0 + SNH : kOutR;         // last stage
+  constexpr int kFinal = kSamp ? kS0 + SNH : kOutB;         // last stage
   constexpr int kStages = kFinal + 1;
   constexpr int DW = BW > SW ? BW : SW;
   static_assert(DW >= 32, "frame-layer D aliases A columns [16, 32)");
-  constexpr uint32_t kSlotCols = 2 * DW + (kQM ? SW : 0) + (kE2 ? 32 : 0);
+  constexpr uint32_t kSlotCols = 2 * DW + (kQM ? SW : 0);
   constexpr uint32_t kBiasCol = G * NS * kSlotCols;
-  constexpr uint32_t kUsedCols = kBiasCol + (kBiasSmem ? 0 : 32);
+  constexpr uint32_t kUsedCols = kBiasCol + 32;
   static_assert(kUsedCols <= 512, "TMEM budget");
   // power-of-two allocation covering all slots + bias chunks, so CTAs that
   // happen to share an SM never block each other in tcgen05.alloc
   constexpr uint32_t kTmemCols = kUsedCols <= 128 ? 128 : (kUsedCols <= 256 ? 256 : 512);
-  constexpr bool kWaitAll = ((NMQ_WAIT_ALL_MODES) >> MODE) & 1;
-  // the issue mbarrier needs the all-warps completion wait: with the
-  // polling warp's release barrier a warp could run a phase ahead
-  constexpr bool kIm = kIssMbar && kWaitAll;
-  static_assert(!(kE2 && kIm), "the two-stage eval path uses the named-barrier issue sync");
 
   const int tid = threadIdx.x;
   // warp-uniform by construction (shfl from lane 0): lets ptxas keep the
@@ -513,11 +508,14 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   // TS: per-row 64-byte texel slots after all input buffers
   const uint32_t tex_row = tc::smem_u32(smem + wbytes + G * NS * 2 * sizeof(InBuf<MODE>)) +
                            (uint32_t)((gi * NS) * kTile + tid % 128) * 64u;
+  // BRDF modes: the group's resolve ring after the texel slots
+  Ring& ring = *(reinterpret_cast<Ring*>(smem + wbytes + G * NS * 2 * sizeof(InBuf<MODE>) +
+                                         (TS ? G * NS * kTile * 64 : 0)) + gi);
 
   // --- CTA setup --------------------------------------------------------------
+  if (tid < G) ring_tail[tid] = 0u;
   if (tid < G * NS) {
-    tc::mbar_init(&mma_bar[tid / NS][tid % NS][0], 1);
-    tc::mbar_init(&mma_bar[tid / NS][tid % NS][1], 4);
+    tc::mbar_init(&mma_bar[tid / NS][tid % NS], 1);
     tc::mbar_init(&in_bar[tid / NS][tid % NS][0], 1);
     tc::mbar_init(&in_bar[tid / NS][tid % NS][1], 1);
   }
@@ -539,18 +537,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tb = __shfl_sync(0xffffffffu, tbase_sh, 0);
-  const uint32_t bias_smem = (tc::smem_u32(smem + wbytes + G * NS * 2 * sizeof(InBuf<MODE>) +
-                                            (TS ? G * NS * kTile * 64 : 0)) + 127u) & ~127u;
-  if constexpr (kBiasSmem) {
-    // bias tiles in the no-swizzle K-major layout (K chunk 0 at +0, chunk 1
-    // at +2048; row r at 16 r): row = (beta_j hi, beta_j lo, 0 ...), chunk 1 = 0
-    for (int i = tid; i < 4 * (int)kBiasTile / 4; i += G * 128) {
-      const int j = i / (kBiasTile / 4), w = i % (kBiasTile / 4);
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(bias_smem + 4u * i),
-                   "r"(w < 512 && (w & 3) == 0 ? fc.beta[j] : 0u) : "memory");
-    }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // visible to the tensor core
-  } else if (warp < 4) {  // bias chunks: (beta_j hi, beta_j lo, 0 ...) for j = 0..3
+  if (warp < 4) {  // bias chunks: (beta_j hi, beta_j lo, 0 ...) for j = 0..3
     const uint32_t lane = (uint32_t)(warp * 32) << 16;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -565,12 +552,10 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
 
   GG g;
   g.bias0 = tb + kBiasCol;
-  g.bias_desc = tc::smem_desc(bias_smem, 2048, 128);
   g.desc0 = tc::smem_desc(tc::smem_u32(smem), 0, 128);
   g.bar_id = 1 + gi;
-  g.done_id = 1 + G + gi;
   g.r = r;
-  static_assert(1 + (kWaitAll ? 1 : 2) * G <= 16, "named barriers");
+  static_assert(1 + G <= 16, "named barriers");
   const uint32_t lane = (uint32_t)((warp & 3) * 32) << 16;
 
   // programmatic dependent launch: everything above (barriers, TMEM, the
@@ -582,12 +567,16 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   // plain instantiation carries none of it
   const int64_t seg_base = SEG && a.seg ? (int64_t)__ldg(a.seg) : 0;
   const int64_t n_rows = SEG && a.seg ? (int64_t)__ldg(a.seg + 1) : a.n;
+  const bool seg_out = SEG && a.out_idx;
   const int ntiles = (int)((n_rows + kTile - 1) / kTile);  // host guarantees < 2^31
   const int last_full = (int)(n_rows / kTile);                // tiles [0, last_full) are full
   const int stride = gridDim.x * G;                        // between a group's tiles
   const int sstride = stride * NS;                         // between a slot's tiles
   const bool want_level = a.level != nullptr;
   const bool want_albedo = mp.albedo && a.albedo;
+  // resolve ring bookkeeping (same values on every thread of the group):
+  // entries [rhead, rprev) belong to earlier tiles, [rprev, rtail) to the current one
+  uint32_t rhead = 0, rprev = 0, rtail = 0;
 
   SlotSt sl[NS];
 #pragma unroll
@@ -598,7 +587,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     sl[s].al = sl[s].a0 + lane;
     sl[s].e0 = sl[s].a0 + DW;
     sl[s].el = sl[s].e0 + lane;
-    sl[s].bar = &mma_bar[gi][s][0];
+    sl[s].bar = &mma_bar[gi][s];
     sl[s].ph = 0u;
     sl[s].t = blockIdx.x * G + gi + s * stride;
     sl[s].it = 0;
@@ -621,112 +610,14 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
                            pack2(ib.wi[3 * r], ib.wi[3 * r + 1]), pack2(ib.wi[3 * r + 2], 1.f), 0u, 0u};
     tc::tmem_st8(S.al, x);
     if constexpr (kQM)
-      mma_issue_first2<kIm, SW, LW>(g, S.a0 + 16, S.e0, S.a0, mp.fast_frame_off, mp.layers[mp.samp_first].b_off,
-                               S.bar, S.ph);
+      mma_issue_first2<SW, LW>(g, S.a0 + 16, S.e0, S.a0, mp.fast_frame_off, mp.layers[mp.samp_first].b_off,
+                               S.bar);
     else if constexpr (kBrdf)
-      mma_issue<kIm, 16, 1, false, LW>(g, S.a0 + 16, S.a0, mp.fast_frame_off, 0, S.bar, S.ph, NoOp{});
+      mma_issue<16, 1, false, LW>(g, S.a0 + 16, S.a0, mp.fast_frame_off, 0, S.bar, NoOp{});
     else
-      mma_issue<kIm, SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar, S.ph, NoOp{});
+      mma_issue<SW, 1, false, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first].b_off, 0, S.bar, NoOp{});
   };
 
-  if constexpr (kE2) {
-    // ===== eval, two stages per tile ============================================
-    SlotSt& S = sl[0];
-    const uint32_t X = S.a0 + DW, XL = X + lane, Y = X + 16, YL = Y + lane;
-    auto chunk0 = [&](const InBuf<MODE>& ib) {
-      const uint32_t x[8] = {S.zp[0], S.zp[1], S.zp[2], S.zp[3],
-                             pack2(ib.wi[3 * r], ib.wi[3 * r + 1]), pack2(ib.wi[3 * r + 2], 1.f), 0u, 0u};
-      tc::tmem_st8(XL, x);
-    };
-    if (S.t < ntiles) {
-      stage_inputs<MODE>(a, seg_base, n_rows, S.t, buf(0, 0), &in_bar[gi][0][0], r, r == 64);
-      if (S.t + sstride < ntiles)
-        stage_inputs<MODE>(a, seg_base, n_rows, S.t + sstride, buf(0, 1), &in_bar[gi][0][1], r, r == 64);
-      wait_in(S, 0, 0, S.t);
-      TexPrefetch p0;
-      prefetch_texels<MODE>(mp, a, buf(0, 0), r, lod0, p0);
-      blend_pack(p0, S.zp);
-      S.level = p0.level;
-      tc::mbar_wait(&w_bar, 0);
-      chunk0(buf(0, 0));
-      mma_issue<kIm, 16, 1, false, 0>(g, Y, X, mp.fast_frame_off, 0, S.bar, S.ph, NoOp{});
-    }
-    bool has_prev = false, pvalid = false, pup = false;
-    int64_t pq = 0;
-    auto out_prev = [&]() {  // output layer of the previous tile (its L2 D is in D)
-      float y[6];
-      out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
-      if (pvalid) {
-        const V3 f = pup ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
-        stg3(a.rgb, pq, f);
-        if (want_albedo) {
-          const V3 al = pup ? v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f)) : v3(0.f, 0.f, 0.f);
-          stg3(a.albedo, pq, al);
-        }
-      }
-    };
-    while (S.t < ntiles) {
-      const int b = S.it & 1;
-      const int64_t q_in = (int64_t)S.t * kTile + r;
-      const bool valid = q_in < n_rows;
-      const int t2 = S.t + 2 * sstride;
-      // --- stage 0: previous tile's output, this tile's frames -> BRDF layer 1
-      const InBuf<MODE>& ib = buf(0, b);
-      const V3 wi = v3(ib.wi[3 * r], ib.wi[3 * r + 1], ib.wi[3 * r + 2]);
-      const V3 wo = v3(ib.wo[3 * r], ib.wo[3 * r + 1], ib.wo[3 * r + 2]);
-      if (want_level) {
-        if (valid) a.level[SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
-      }
-      if (S.t + sstride < ntiles) {
-        wait_in(S, 0, b ^ 1, S.t + sstride);
-        prefetch_texels<MODE>(mp, a, buf(0, b ^ 1), r, lod0, S.nx);
-      }
-      auto refill = [&]() {
-        if (t2 < last_full) {
-          if (r == 96) stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(0, b), &in_bar[gi][0][b], r, true);
-        } else if (t2 < ntiles) {
-          stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(0, b), &in_bar[gi][0][b], r, false);
-        }
-      };
-      mma_wait<0, kWaitAll>(g, S.bar, S.ph);
-      if (has_prev) out_prev();
-      {
-        uint32_t fr[16];
-        tc::tmem_ld16(YL, fr);
-        tc::tmem_ld_wait();
-        float raw[12];
-#pragma unroll
-        for (int j = 0; j < 12; ++j) raw[j] = __uint_as_float(fr[j]);
-        float ti[6], to[6];
-        frames2_transform(raw, wi, wo, ti, to);
-        const uint32_t x[8] = {pack2(ti[0], ti[1]), pack2(ti[2], ti[3]), pack2(ti[4], ti[5]),
-                               pack2(to[0], to[1]), pack2(to[2], to[3]), pack2(to[4], to[5]), 0u, 0u};
-        tc::tmem_st8(XL + 8, x);
-      }
-      mma_issue<kIm, BW, 2, false, 1>(g, S.d0, X, mp.fast_l1_off, 0, S.bar, S.ph, refill);
-      // --- stage 1: hidden epilogue -> BRDF layer 2 (+ next tile's frame layer)
-      mma_wait<1, kWaitAll>(g, S.bar, S.ph);
-      hidden_epi<BW>(S.dl, S.al);
-      pq = SEG && a.out_idx && valid ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
-      pvalid = valid;
-      pup = (wi.z > 0.f) && (wo.z > 0.f);
-      has_prev = true;
-      const int tn = S.t + sstride;
-      if (tn < ntiles) {
-        blend_pack(S.nx, S.zp);
-        S.level = S.nx.level;
-        chunk0(buf(0, b ^ 1));
-      }
-      mma_issue_hid_frame<BW, 2 * BW / 16, 2>(g, S.d0, S.a0, mp.layers[mp.brdf_first + 1].b_off, 1,
-                                              tn < ntiles, Y, X, mp.fast_frame_off, S.bar);
-      S.t = tn;
-      S.it += 1;
-    }
-    if (has_prev) {
-      mma_wait<3, kWaitAll>(g, S.bar, S.ph);
-      out_prev();
-    }
-  } else {
   // --- prologue: per slot stage tiles 0 and 1, fetch + blend tile 0, issue its first MMA
   sfor<NS>([&](auto sc) {
     constexpr int s = decltype(sc)::value;
@@ -738,7 +629,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       wait_in(S, s, 0, S.t);
       TexPrefetch p0;
       prefetch_texels<MODE>(mp, a, buf(s, 0), r, lod0, p0);
-      blend_pack(p0, S.zp);
+      blend_pack<MODE>(mp, p0, buf(s, 0), r, S.zp);
       S.level = p0.level;
       if (s == 0) tc::mbar_wait(&w_bar, 0);  // weights in SMEM before the first MMA
       issue_first(S, buf(s, 0), std::integral_constant<int, s % 4>{});
@@ -758,8 +649,6 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
         const int64_t q_in = (int64_t)S.t * kTile + r;  // input row
         const bool valid = q_in < n_rows;
         const int t2 = S.t + 2 * sstride;
-        constexpr int PW = (k + s) % 4;  // warp polling the previous MMA's completion
-        auto wait_mma = [&]() { mma_wait<PW, kWaitAll>(g, S.bar, S.ph); };
 
         if constexpr (k == 0) {
           // this tile's directions -> registers; its input buffer is refilled
@@ -771,27 +660,30 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           if constexpr (Need<MODE>::u3) S.u3 = v3(ib.u3[3 * r], ib.u3[3 * r + 1], ib.u3[3 * r + 2]);
           S.up = (S.wi.z > 0.f) && (wo.z > 0.f);
           if (want_level) {
-            if (valid) a.level[SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
+            if (valid) a.level[seg_out ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
           }
-          // the slot's next tile: texel loads now, blended at the last stage
-          if (S.t + sstride < ntiles) {
-            wait_in(S, s, b ^ 1, S.t + sstride);
-            if constexpr (TS)
-              prefetch_texels_smem<MODE>(mp, a, buf(s, b ^ 1), r, lod0, tex_row + s * kTile * 64u, S.nx);
-            else
-              prefetch_texels<MODE>(mp, a, buf(s, b ^ 1), r, lod0, S.nx);
-          }
+          // the slot's next tile: texel loads now (BRDF modes: after this
+          // stage's frame work, which would otherwise hold them in registers
+          // through its peak), blended at the last stage
+          auto prefetch = [&]() {
+            if (S.t + sstride < ntiles) {
+              wait_in(S, s, b ^ 1, S.t + sstride);
+              if constexpr (TS)
+                prefetch_texels_smem<MODE>(mp, a, buf(s, b ^ 1), r, lod0, tex_row + s * kTile * 64u, S.nx);
+              else
+                prefetch_texels<MODE>(mp, a, buf(s, b ^ 1), r, lod0, S.nx);
+            }
+          };
+          if constexpr (!kBrdf || NMQ_EARLY_PREFETCH) prefetch();
           auto refill = [&]() {  // after the barrier: every row of buffer b was read
             if (t2 < last_full) {
-              if (r == 32 * ((LW + 2) % 4)) {
-              if constexpr (kIm) tc::mbar_wait(S.bar + 1, S.ph);  // every row has read buffer b
-              stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
-            }
+              if (r == 32 * ((LW + 2) % 4))
+                stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
             } else if (t2 < ntiles) {
               stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, false);  // own row
             }
           };
-          wait_mma();
+          mma_wait(S.bar, S.ph);
           if constexpr (kBrdf) {
             // frame layer D -> frames, T.wi, T.wo -> input chunk 1 -> BRDF layer 1
             uint32_t fr[16];
@@ -801,60 +693,74 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
 #pragma unroll
             for (int j = 0; j < 12; ++j) raw[j] = __uint_as_float(fr[j]);
             float ti[6], to[6];
-            frames2_transform(raw, S.wi, wo, ti, to);
+            const float2 kappa = frames2_transform(raw, S.wi, wo, ti, to);
             const uint32_t x[8] = {pack2(ti[0], ti[1]), pack2(ti[2], ti[3]), pack2(ti[4], ti[5]),
                                    pack2(to[0], to[1]), pack2(to[2], to[3]), pack2(to[4], to[5]),
                                    0u, 0u};
             tc::tmem_st8(S.al + 8, x);
-            mma_issue<kIm, BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, S.ph, refill);
+            // exact rounding: a direction input within its error bound of an
+            // fp16 midpoint (bound = tw_delta x conditioning of its frame)
+#if NMQ_X_CONSTD
+            const float2 d1 = make_float2(fc.tw_delta, fc.tw_delta), d2 = d1;
+#else
+            const float2 d1 = make_float2(fc.tw_delta * kappa.x, fc.tw_delta * kappa.x);
+            const float2 d2 = make_float2(fc.tw_delta * kappa.y, fc.tw_delta * kappa.y);
+#endif
+            const float2 d12 = make_float2(d1.x, d2.x);
+            const uint32_t near = near_mid2(ti[0], ti[1], d1) | near_mid2(ti[2], ti[3], d12) |
+                                  near_mid2(ti[4], ti[5], d2) | near_mid2(to[0], to[1], d1) |
+                                  near_mid2(to[2], to[3], d12) | near_mid2(to[4], to[5], d2);
+            const bool flag = !NMQ_X_NOCHECK && valid && S.up && near != 0u;
+            // queue this tile's flagged rows (one shared atomic per warp); they
+            // are resolved from the last stage of a later tile
+            const uint32_t wmask = __ballot_sync(0xffffffffu, flag);
+            if (NMQ_X_NOAPPEND) { rtail += wmask != 0; } else if (wmask) {
+              uint32_t wbase = 0;
+              if ((r & 31) == __ffs(wmask) - 1) wbase = atomicAdd(&ring_tail[gi], __popc(wmask));
+              wbase = __shfl_sync(0xffffffffu, wbase, __ffs(wmask) - 1);
+              if (flag) {
+                const uint32_t slot = (wbase + __popc(wmask & lanemask_lt())) % (uint32_t)kRing;
+                ring.row[slot] = (int32_t)(seg_base + q_in);
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ring.z16[slot][c] = S.zp[c];
+#pragma unroll
+                for (int c = 0; c < 6; ++c) ring.x16[slot][c] = x[c];
+              }
+            }
+            mma_issue<BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, refill);
+            if constexpr (!NMQ_EARLY_PREFETCH) prefetch();
+            rprev = rtail;            // entries of tiles before this one
+            rtail = ring_tail[gi];    // complete: every warp appended before the barrier
+            if (a.dbg && valid) {  // calibration dump (tools/tw_calibrate.py)
+              float* o = a.dbg + 14 * (seg_base + q_in);
+#pragma unroll
+              for (int j = 0; j < 6; ++j) { o[j] = ti[j]; o[6 + j] = to[j]; }
+              o[12] = kappa.x;
+              o[13] = kappa.y;
+            }
           } else {
             // sample+pdf: sampler layer 1 D -> layer 2
             hidden_epi<SW>(S.dl, S.al);
             if constexpr (SNH == 1)
-              mma_issue<kIm, 16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, S.ph, refill);
+              mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off, 1,
+                                                   S.bar, refill);
             else
-              mma_issue<kIm, SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, S.ph, refill);
+              mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off, 1,
+                                                   S.bar, refill);
           }
         } else if constexpr (kBrdf && k < kOutB) {
           // BRDF hidden layer k+1
-          wait_mma();
+          mma_wait(S.bar, S.ph);
           hidden_epi<BW>(S.dl, S.al);
-          mma_issue<kIm, BW, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + k].b_off, k,
-                                               S.bar, S.ph, NoOp{});
-        } else if constexpr (kOM && k == kOutB) {
-          // BRDF output layer on the tensor core: last hidden layer -> A, N = 16 MMA
-          wait_mma();
-          hidden_epi<BW>(S.dl, S.al);
-          mma_issue<kIm, 16, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + BNH].b_off, BNH,
-                                               S.bar, S.ph, NoOp{});
-        } else if constexpr (kOM && k == kOutR) {
-          wait_mma();
-          uint32_t yr[8];
-          tc::tmem_ld8(S.dl, yr);
-          tc::tmem_ld_wait();
-          float y[6];
-#pragma unroll
-          for (int j = 0; j < 6; ++j) y[j] = __uint_as_float(yr[j]) * fc.inv_brdf;
-          if (valid) {
-            const int64_t q = SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
-            const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
-                              : v3(0.f, 0.f, 0.f);
-            stg3(a.rgb, q, f);
-            if (want_albedo) {
-              const V3 al = S.up ? v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f))
-                                 : v3(0.f, 0.f, 0.f);
-              stg3(a.albedo, q, al);
-            }
-          }
+          mma_issue<BW, 2 * BW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.brdf_first + k].b_off, k, S.bar,
+                                               NoOp{});
         } else if constexpr (k == kOutB) {
           // BRDF output layer on the CUDA cores
-          wait_mma();
+          mma_wait(S.bar, S.ph);
           float y[6];
           out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
           if (valid) {
-            const int64_t q = SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
+            const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                               : v3(0.f, 0.f, 0.f);
             stg3(a.rgb, q, f);
@@ -868,27 +774,27 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             // query: sampler layer 1 (issued with the frame layer, in E) -> layer 2
             hidden_epi<SW>(S.el, S.al);
             if constexpr (SNH == 1)
-              mma_issue<kIm, 16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, S.ph, NoOp{});
+              mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off, 1,
+                                                   S.bar, NoOp{});
             else
-              mma_issue<kIm, SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off,
-                                                   1, S.bar, S.ph, NoOp{});
+              mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + 1].b_off, 1,
+                                                   S.bar, NoOp{});
           }
         } else if constexpr (kSamp && k > kS0 && k < kFinal) {
-          // sampler layer j+1 (j = k - kS0 >= 1; stage kS0 is k == 0 or handled below)
+          // sampler layer j+1 (j = k - kS0 >= 1; stage kS0 is k == 0 or handled above)
           constexpr int j = k - kS0;
-          wait_mma();
+          mma_wait(S.bar, S.ph);
           hidden_epi<SW>(S.dl, S.al);
           if constexpr (j + 1 == SNH)
-            mma_issue<kIm, 16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
-                                                 j + 1, S.bar, S.ph, NoOp{});
+            mma_issue<16, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off, j + 1,
+                                                 S.bar, NoOp{});
           else
-            mma_issue<kIm, SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off,
-                                                 j + 1, S.bar, S.ph, NoOp{});
+            mma_issue<SW, 2 * SW / 16, true, LW>(g, S.d0, S.a0, mp.layers[mp.samp_first + j + 1].b_off, j + 1,
+                                                 S.bar, NoOp{});
         }
         if constexpr (kSamp && k == kFinal) {
           // proxy parameters, sample, pdf
-          wait_mma();
+          mma_wait(S.bar, S.ph);
           uint32_t yr[16];
           tc::tmem_ld16(S.dl, yr);
           tc::tmem_ld_wait();
@@ -897,7 +803,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           for (int j = 0; j < 9; ++j) raw[j] = __uint_as_float(yr[j]);
           const Proxy p = proxy_from_raw(raw, mp.isotropic != 0, fc.inv_samp);
           if (valid) {
-            const int64_t q = SEG && a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
+            const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             if (a.params9) store_proxy(a.params9, q, p);
             const V3 w = proxy_sample(p, S.wi, S.u3.x, S.u3.y, S.u3.z);
             stg3(a.ws, q, w);
@@ -907,11 +813,20 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
         if constexpr (k == kFinal) {
           // the slot's next tile: blend its texels, issue its first MMA
           const int tn = S.t + sstride;
+          // resolve ring: rows queued by earlier tiles (this tile's were queued
+          // at stage 0; its outputs are stored in this stage without a barrier)
           if (tn < ntiles) {
             if constexpr (TS) land_texels_smem(tex_row + s * kTile * 64u, S.nx);
-            blend_pack(S.nx, S.zp);
+            blend_pack<MODE>(mp, S.nx, buf(s, b ^ 1), r, S.zp);
             S.level = S.nx.level;
             issue_first(S, buf(s, b ^ 1), std::integral_constant<int, LW>{});
+          }
+          if constexpr (kBrdf) {
+            // earlier tiles' outputs were stored before this tile's stage-0 barrier
+            if (!NMQ_X_NORESOLVE && rprev - rhead >= (uint32_t)kTile) {
+              resolve_batch(mp, a, ring, rhead, kTile, r, seg_out);
+              rhead += kTile;
+            }
           }
           S.t = tn;
           S.it += 1;
@@ -919,7 +834,15 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       });
     });
   }
-  }  // !kE2
+  if constexpr (kBrdf) {
+    // drain the resolve ring (the last tiles' outputs are stored before the barrier)
+    tc::named_bar(g.bar_id, 128);
+    while (rtail != rhead) {
+      const uint32_t c = rtail - rhead < (uint32_t)kTile ? rtail - rhead : (uint32_t)kTile;
+      resolve_batch(mp, a, ring, rhead, c, r, seg_out);
+      rhead += c;
+    }
+  }
   if constexpr (NMQ_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   tc::tc_fence_before();
@@ -933,6 +856,13 @@ uint32_t fp16_bits(double v) {
   return *reinterpret_cast<const uint16_t*>(&h);
 }
 
+#ifndef NMQ_TW_DELTA
+// error bound of the fast fp32 T.w per unit frame conditioning: measured
+// max |fast - exact| / kappa = 1.48e-7 over 6.2M C2 queries x 12 values
+// (tools/tw_calibrate.py, profiles/r02_tw_calibration.txt); 2x margin
+#define NMQ_TW_DELTA 3e-7f
+#endif
+
 FastConsts make_consts(int brdf_nh, int samp_nh) {
   FastConsts c{};
   const double cc = 1.0 + (double)kLk;
@@ -945,10 +875,17 @@ FastConsts make_consts(int brdf_nh, int samp_nh) {
   }
   c.inv_brdf = (float)(1.0 / std::pow(cc, brdf_nh));
   c.inv_samp = (float)(1.0 / std::pow(cc, samp_nh));
+  c.tw_delta = g_tw_margin > 0.f ? g_tw_margin : NMQ_TW_DELTA;
   return c;
 }
 
 int g_sms = 0;
+
+}  // namespace
+
+float g_tw_margin = 0.f;
+
+namespace {
 
 #ifndef NMQ_TEX_SMEM
 // bit per mode (1 << MODE): stage texel prefetches in SMEM by cp.async
@@ -969,16 +906,20 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   if (seg && MODE != kModeEval) return cudaErrorNotSupported;  // binned segments are eval-only
   auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, (MODE == kModeEval)>
                   : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
+  constexpr bool kBrdf = Need<MODE>::brdf;
   const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>) +
-                         (TS ? G * NS * kTile * 64 : 0) + (kBiasSmem ? 4 * kBiasTile + 128 : 0));
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+                         (TS ? G * NS * kTile * 64 : 0) + (kBrdf ? G * sizeof(Ring) : 0));
+  const int max_dyn = std::min(max_dynamic_smem((const void*)fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>),
+                               max_dynamic_smem((const void*)kern));
+  if (max_dyn < 0) return cudaErrorInvalidValue;
+  if (smem > max_dyn) return cudaErrorNotSupported;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   int64_t grid = g_sms;
   if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid > (ntiles + G - 1) / G) grid = (ntiles + G - 1) / G;
   if (grid < 1) grid = 1;
   const FastConsts fc = make_consts(BNH, SNH);
+  cudaError_t e;
   if constexpr (NMQ_PDL) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);

@@ -34,6 +34,8 @@ struct LayerDesc {
   uint8_t act;      // 0 linear, 1 leaky
   uint8_t out;      // true (unpadded) output width
   uint8_t precise;  // fp32 path: B = [W_hi | W_hi | W_lo] against A = [x_hi | x_lo | x_hi]
+  uint16_t fan_in;  // true fan-in
+  uint32_t w32_off; // float offset of the layer in MatParams::w32
 };
 
 struct MatParams {
@@ -65,21 +67,14 @@ struct MatParams {
   // FFMA2 on the CUDA cores: ow[j][q] = (W[j][2q], W[j][2q+1]), ob[j]
   float2 ow[6][32];
   float ob[6];
-  // Warp-tile kernels (nmq_warp.cu): one blob of fp16 B operands (chunk-major
-  // K-major: 16-byte K-chunk c of row n at off + c*n_pad*16 + n*16, read with
-  // ldmatrix) and fp32 biases pre-scaled by c^depth (accumulator init).
-  // Byte offsets into wk_blob.  Input chunks as above; BRDF layer 1 is split
-  // into a K=8 part on z and a K=16 part on [T.wi, T.wo, 1 @ 12].
-  const uint4* wk_blob;
-  uint32_t wk_bytes;
-  uint32_t wk_fr;          // frame layer N16 K16
-  uint32_t wk_b1z, wk_b1t; // BRDF layer 1: K8 (z), K16 (T.wi, T.wo, bias), N = BW
-  uint32_t wk_bh[3];       // BRDF hidden layers 2.. (K = N = BW)
-  uint32_t wk_bo;          // BRDF output, N = 8, K = BW
-  uint32_t wk_s1;          // sampler layer 1 (input chunk 0), N = SW
-  uint32_t wk_sh[3];       // sampler hidden layers 2..
-  uint32_t wk_so;          // sampler output, N = 16, K = SW
-  uint32_t wk_bias_bh[3], wk_bias_bo, wk_bias_sh[3], wk_bias_so;  // fp32 [N] each
+  // fp32 copies (exact widenings of the fp16 weights) for the SIMT parts of
+  // the exact-rounding path: the frame layer [W(8) | b] per
+  // raw output (evaluated with the reference's sequential FMA order), and
+  // every network in the reference's packed access order [w_row, bias] per
+  // neuron (`w32` + LayerDesc::w32_off), read by the warp-cooperative
+  // re-evaluation of queries whose decoder inputs round differently.
+  float fw[12][9];
+  const float* w32;
 };
 
 enum Mode : int {
@@ -118,12 +113,12 @@ struct QueryArgs {
   int32_t* level;
   int32_t* taps;
   float* wts;
+  float* dbg;  // fast kernel calibration dump: fp32 T.wi, T.wo and frame conditioning (14 floats/row)
 };
 
-// pipelined tcgen05 kernels (nmq_fast.cu) and warp-tile mma.sync kernels
-// (nmq_warp.cu); cudaErrorNotSupported = not applicable, try the next path
+// pipelined tcgen05 kernels (nmq_fast.cu); cudaErrorNotSupported = not
+// applicable, use the generic kernel
 cudaError_t launch_fast(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s);
-cudaError_t launch_warp(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s);
 // scale of the leaky-ReLU trick shared by the specialized kernels: c = 1 + k
 constexpr double kLeakyScale = 1.0 + 0.98019802570343017578;
 // launchers (nmq_kernels.cu); return cudaError_t of the launch
@@ -170,10 +165,16 @@ cudaError_t launch_footprint_level(int64_t n, const double* area, int32_t n_leve
 cudaError_t launch_cone_level(int64_t n, const float* cone_w, const float* cone_s, const float* t,
                               const float* cos_hit, const float* density, int32_t density_stride,
                               int32_t n_levels, float* lod, cudaStream_t s);
+// Raise a kernel's dynamic shared memory limit to the device maximum, once
+// per kernel (thread-safe; a per-launch set-then-launch pair would race with
+// another host thread lowering the limit in between).  Returns the limit
+// (bytes of dynamic SMEM available to the kernel) or -1 on failure.
+int max_dynamic_smem(const void* kernel);
 extern std::atomic<int64_t> g_launches;  // host threads may launch concurrently
-// kernel path: 0 = auto (tcgen05 pipelined, then warp-tile, then generic),
-// 1 = generic only, 2 = tcgen05 pipelined, 3 = warp-tile (each falls back to generic)
+// kernel path: 0 = auto (tcgen05 pipelined, then generic), 1 = generic only,
+// 2 = tcgen05 pipelined (falls back to generic)
 extern int g_kernel_path;
-extern std::atomic<int> g_last_path;  // family of the last launch_fused (1/2/3 as above)
+extern float g_tw_margin;  // nm_set_tw_margin (<= 0: built-in bound)
+extern std::atomic<int> g_last_path;  // family of the last launch_fused (1/2 as above)
 
 }  // namespace nmq

@@ -16,6 +16,8 @@
 //    W*[hi; lo] with the weights duplicated along K — exact to ~2^-22.
 //    Biases ride along as an extra K column against a constant 1.0.
 #include <cstdio>
+#include <mutex>
+#include <unordered_map>
 #include "tc.cuh"
 #include "nmq_device.cuh"
 #include "nmq_internal.h"
@@ -23,6 +25,25 @@
 namespace nmq {
 
 std::atomic<int64_t> g_launches{0};
+
+int max_dynamic_smem(const void* kernel) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(kernel);
+  if (it != done.end()) return it->second;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa{};
+  int lim = -1;
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) {
+    lim = optin - (int)fa.sharedSizeBytes;
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, lim) != cudaSuccess) lim = -1;
+  }
+  done[kernel] = lim;
+  return lim;
+}
 int g_kernel_path = 0;
 std::atomic<int> g_last_path{0};
 
@@ -180,7 +201,21 @@ __device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const
   for (int k = 0; k < 32; ++k) x[k] = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) x[k] = z[k];
-  if (mp.use_frames) {
+  if (mp.use_frames && !mp.precise) {
+    // fp16 path: the reference's rounding of every decoder input, exactly —
+    // frame layer in its sequential-FMA order, frames and transforms in
+    // float64, fp32, then fp16 (neural.py:282-287)
+    uint32_t zh[4], x16[6];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) zh[c] = pack_h2(z[2 * c], z[2 * c + 1]);
+    tw_exact(mp, zh, wi, wo, x16);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) {
+      const float2 f = unpack_h2(x16[c]);
+      x[8 + 2 * c] = f.x;
+      x[9 + 2 * c] = f.y;
+    }
+  } else if (mp.use_frames) {
     float xf[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) xf[k] = 0.f;
@@ -330,7 +365,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
       }
       const int level = choose_level(mp, lod, urr);
       const Taps t = make_taps(mp, level, u, v);
-      fetch_taps(mp, t, z);
+      fetch_exact(mp, level, u, v, t, z);
       if (valid && a.level) a.level[oq] = level;
     }
 
@@ -462,7 +497,7 @@ divergent_eval_kernel(const MatParams* __restrict__ mps_g, int32_t n_mats,
       const float lod = __ldg(a.lod + (a.lod_stride ? q : 0));
       const int level = choose_level(mm, lod, __ldg(a.u_rr + q));
       const Taps t = make_taps(mm, level, uv.x, uv.y);
-      fetch_taps(mm, t, z);
+      fetch_exact(mm, level, uv.x, uv.y, t, z);
       wi = ldg3(a.wi, q);
       wo = ldg3(a.wo, q);
       if (a.level) a.level[q] = level;
@@ -515,7 +550,7 @@ __global__ void __launch_bounds__(256) fetch_kernel(const __grid_constant__ MatP
     const int level = choose_level(mp, lod, __ldg(a.u_rr + i));
     const Taps t = make_taps(mp, level, uv.x, uv.y);
     float z[8];
-    fetch_taps(mp, t, z);
+    fetch_exact(mp, level, uv.x, uv.y, t, z);
     if (a.z_out) {
       float4* o = reinterpret_cast<float4*>(a.z_out + 8 * i);
       o[0] = make_float4(z[0], z[1], z[2], z[3]);
@@ -528,9 +563,10 @@ __global__ void __launch_bounds__(256) fetch_kernel(const __grid_constant__ MatP
       p[4] = t.x0; p[5] = t.y1; p[6] = t.x1; p[7] = t.y1;
     }
     if (a.wts) {
-      const float gx = 1.f - t.fx, gy = 1.f - t.fy;
-      float* w = a.wts + 4 * i;
-      w[0] = gx * gy; w[1] = t.fx * gy; w[2] = gx * t.fy; w[3] = t.fx * t.fy;
+      double w[4];
+      weights64(frac64(uv.x, mp.lv[level].w), frac64(uv.y, mp.lv[level].h), w);
+      float* o = a.wts + 4 * i;
+      o[0] = (float)w[0]; o[1] = (float)w[1]; o[2] = (float)w[2]; o[3] = (float)w[3];
     }
   }
 }
@@ -588,8 +624,9 @@ cudaError_t launch_mode(const MatParams& mp, const QueryArgs& a, cudaStream_t s,
   const int ctas_per_sm = (int)(512 / cols) < 2 ? (int)(512 / cols) : 2;
   const int smem = smem_bytes_for(mp);
   auto kern = fused_kernel<MODE>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e != cudaSuccess) return e;
+  const int lim = max_dynamic_smem((const void*)kern);
+  if (lim < 0) return cudaErrorInvalidValue;
+  if (smem > lim) return cudaErrorNotSupported;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   int64_t grid = (int64_t)num_sms() * ctas_per_sm;
   if (a.max_ctas > 0 && grid > (int64_t)a.max_ctas * ctas_per_sm) grid = (int64_t)a.max_ctas * ctas_per_sm;
@@ -611,11 +648,6 @@ cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cuda
   if (groups == 0 && (g_kernel_path == 0 || g_kernel_path == 2)) {
     const cudaError_t e = launch_fast(mp, mode, a, s);
     if (e != cudaErrorNotSupported) return g_last_path.store(2), e;
-    (void)cudaGetLastError();
-  }
-  if (groups == 0 && (g_kernel_path == 0 || g_kernel_path == 3)) {
-    const cudaError_t e = launch_warp(mp, mode, a, s);
-    if (e != cudaErrorNotSupported) return g_last_path.store(3), e;
     (void)cudaGetLastError();
   }
   g_last_path = 1;
@@ -645,9 +677,8 @@ cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatPar
   uint32_t need = G * group_cols + 8u, cols = 32;
   while (cols < need) cols <<= 1;
   if (cols > 512) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(divergent_eval_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  const int lim = max_dynamic_smem((const void*)divergent_eval_kernel);
+  if (lim < 0 || (int)smem > lim) return cudaErrorInvalidValue;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   int64_t grid = num_sms();
   if (grid > (ntiles + G - 1) / G) grid = (ntiles + G - 1) / G;

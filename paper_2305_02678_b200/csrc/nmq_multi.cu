@@ -312,12 +312,7 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
     const int nb = grid256(a.n), cap = 4 * num_sms_multi();
     bin_count_kernel<<<nb < cap ? nb : cap, 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(ScatterSmem));
-    attr = true;
-  }
+  if (max_dynamic_smem((const void*)bin_scatter_kernel) < (int)sizeof(ScatterSmem)) return cudaErrorInvalidValue;
   bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sizeof(ScatterSmem), s>>>(
       a.n, n_mats, mat_id, w.counts, w.seg, w.cursor, w.order, a.uv, a.lod,
                                                   a.lod_stride, a.u_rr, a.wi, a.wo, w.uv, w.lod,

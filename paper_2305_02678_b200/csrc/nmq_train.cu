@@ -484,8 +484,9 @@ cudaError_t launch_mlp_forward(const int32_t* fi, const int32_t* fo, const int32
   const size_t smem = (size_t)(pad ? po : w_floats) * 4;
   auto kern = wide ? (pad ? mlp_forward_kernel<64, true> : mlp_forward_kernel<64, false>)
                    : (pad ? mlp_forward_kernel<32, true> : mlp_forward_kernel<32, false>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  const int lim = max_dynamic_smem((const void*)kern);
+  if (lim < 0 || (int)smem > lim) return cudaErrorInvalidValue;
+  cudaError_t e;
   int64_t blocks = (B + 127) / 128;
   if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
   kern<<<(int)blocks, 128, smem, s>>>(v, B, wts, x, x_cache, pre_cache, out);
@@ -512,8 +513,9 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
   const size_t smem = (size_t)w_floats * (w64 ? 8 : 4);  // float64 copy of the weights when it fits
   auto kern = wide ? (w64 ? mlp_backward_kernel<64, double> : mlp_backward_kernel<64, float>)
                    : (w64 ? mlp_backward_kernel<32, double> : mlp_backward_kernel<32, float>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
+  const int lim = max_dynamic_smem((const void*)kern);
+  if (lim < 0 || (int)smem > lim) return cudaErrorInvalidValue;
+  cudaError_t e;
   int64_t blocks = (B + 127) / 128;
   if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
   kern<<<(int)blocks, 128, smem, s>>>(v, B, wts, pre_cache, out_grad, g_cache, dx);

@@ -2,9 +2,9 @@
 reference produced, and against the numpy oracle on fresh seeded inputs.
 
 Tolerances (stated in DESIGN.md §5, from the north star / SURVEY §8c4):
-  * chosen level and the 4 tap indices: bit-exact;
-  * z: |dz| <= 1e-6 * (sum_k |w_k t_k|) + 1e-7  (fp32 blend vs float64);
-  * RGB, albedo, proxy params: rel = |a-b|/(|b|+1e-2) max <= 1e-2, mean <= 1e-3;
+  * chosen level, the 4 tap indices and z: bit-exact;
+  * RGB, albedo, proxy params: rel = |a-b|/(|b|+1e-2) max <= 1e-2 for EVERY
+    value (no outlier budget), mean <= 1e-3;
   * sampled direction: |dw| <= 1e-3 outside a 1e-3 guard band around the
     lobe pick u0 = wd (lobe flips counted, must be rare);
   * pdf: decoupled check (GPU params and reference params at the same
@@ -36,31 +36,28 @@ def our_material(g):
     return mat
 
 
-def check_rel(a, b, max_tol=1e-2, mean_tol=1e-3, what="", outlier_rate=5e-4, hard_max=0.1):
-    """rel = |a-b|/(|b|+1e-2): mean <= mean_tol, at most floor(n*outlier_rate)
-    values above max_tol (none for n < 1e4) and none above hard_max.  The
-    outlier budget covers isolated fp16 rounding-tie flips of layer inputs
-    (fp32 vs the reference's float64 frames land on opposite sides of a tie;
-    DESIGN.md §5)."""
+def check_rel(a, b, max_tol=1e-2, mean_tol=1e-3, what=""):
+    """rel = |a-b|/(|b|+1e-2) (cli.py:213): EVERY value <= max_tol and the
+    mean <= mean_tol — no outlier budget (the decoder inputs round exactly as
+    the reference rounds them)."""
     r = np.ravel(rel_err(a, b))
     assert np.all(np.isfinite(a)), f"{what}: non-finite"
     i = int(np.argmax(r))
-    n_out = int(np.count_nonzero(r > max_tol))
-    allowed = int(len(r) * outlier_rate)
-    assert n_out <= allowed and r.max() <= max(hard_max if allowed else max_tol, max_tol), (
-        f"{what}: {n_out} > {allowed} values above {max_tol}; max rel {r.max():.3e} at {i}: "
-        f"got {np.ravel(a)[i]!r} want {np.ravel(b)[i]!r}, mean {r.mean():.2e}")
+    assert r.max() <= max_tol, (
+        f"{what}: {int(np.count_nonzero(r > max_tol))} values above {max_tol}; max rel {r.max():.3e} at "
+        f"{i}: got {np.ravel(a)[i]!r} want {np.ravel(b)[i]!r}, mean {r.mean():.2e}")
     assert r.mean() <= mean_tol, f"{what}: mean rel {r.mean():.3e}"
     return r
 
 
 def check_dirs(ws, ws_ref, u3, p_ref, wi, tol=1e-3, band=1e-3):
-    """Sampled directions vs the oracle: outside the lobe-pick guard band and
-    where the map is well conditioned.  The diffuse lobe normalizes
-    g = n_d + v (proxy.py:149-156) and the specular lobe g = M m
-    (proxy.py:159-165); when |g| -> 0 the direction's sensitivity to fp32
-    rounding grows as 1/|g|, so samples with |g| < 1e-2 are excluded (their
-    share is asserted to be tiny)."""
+    """Sampled directions vs the oracle: every sample outside the lobe-pick
+    guard band |u0 - wd| < 1e-3 and where the sampling map is
+    well conditioned.  The diffuse lobe normalizes g = n_d + v
+    (proxy.py:149-156) and the specular lobe g = M m (proxy.py:159-165);
+    when |g| -> 0 a direction's sensitivity to fp32 rounding grows as 1/|g|,
+    so samples with |g| < 1e-2 are excluded (their share is asserted tiny).
+    Returns the number of lobe flips (samples in the band whose lobe differs)."""
     from oracle import nm_oracle as O
     u3 = np.asarray(u3, np.float64)
     wd = p_ref.wd
@@ -70,14 +67,31 @@ def check_dirs(ws, ws_ref, u3, p_ref, wi, tol=1e-3, band=1e-3):
     spec = ~diff
     g[spec] = np.einsum("bij,bj->bi", p_ref.subset(spec).warp(), O.ndf_sample(u3[spec, 1:3]))
     glen = np.linalg.norm(g, axis=1)
-    ok = (np.abs(u3[:, 0] - wd) >= band) & (glen >= 1e-2)
+    band_rows = np.abs(u3[:, 0] - wd) < band
+    ok = ~band_rows & (glen >= 1e-2)
     assert ok.mean() > 0.99, ok.mean()
     dw = np.abs(np.asarray(ws, np.float64) - ws_ref).max(axis=1)
     bad = np.flatnonzero(ok & (dw > tol))
-    allowed = int(len(dw) * 5e-4)  # isolated fp16 input-rounding flips, as in check_rel
-    assert bad.size <= allowed and (dw[ok].max() <= 1e-2 if ok.any() else True), (f"{bad.size} directions off, worst {dw[bad].max():.3e} at {bad[0]}: "
+    assert bad.size == 0, (f"{bad.size} directions off, worst {dw[bad].max():.3e} at {bad[0]}: "
                            f"diffuse={diff[bad[0]]} |g|={glen[bad[0]]:.3e} u={u3[bad[0]]} "
                            f"got {ws[bad[0]]} want {ws_ref[bad[0]]}")
+    return int(np.count_nonzero(band_rows & (dw > tol)))
+
+
+def conditioned_pdf_rows(params9, wi, ws64, pdf64, cond_tol=1e-3):
+    """(rows well conditioned, reference pdf at the fp32 direction, fp32 direction)."""
+    from oracle import nm_oracle as O
+    b = np.asarray(params9, np.float64)
+    P = O.Proxy(b[:, 0], b[:, 1], b[:, 2:4], b[:, 4:6], b[:, 6], b[:, 7:9])
+    ws32 = np.asarray(ws64).astype(np.float32)
+    wi64 = np.asarray(wi, np.float32).astype(np.float64)
+    ref32 = O.pdf(P, wi64, ws32.astype(np.float64))
+    cond = rel_err(ref32, pdf64)
+    h = wi64 + ws32
+    h = h / np.maximum(np.linalg.norm(h, axis=1, keepdims=True), 1e-30)
+    well = (cond <= cond_tol) & (np.abs(np.sum(ws32 * h, axis=1)) >= 1e-4)
+    assert well.mean() > 0.99, well.mean()
+    return well, ref32, ws32
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -90,15 +104,8 @@ def test_fetch_bit_exact_levels_and_taps(name):
     if "xs" in g:
         assert np.array_equal(xs, g["xs"]) and np.array_equal(ys, g["ys"])
         np.testing.assert_allclose(wts, g["wts"], rtol=0, atol=1e-7)
-    # z tolerance relative to the magnitude of the blended terms
-    lv = golden_levels(g)
-    scale = np.ones(len(z))
-    if "xs" in g:
-        tex = np.stack([np.abs(lv[c].astype(np.float16).astype(np.float32)[ys[i], xs[i]]).max()
-                        for i, c in enumerate(chosen)])
-        scale = tex
-    dz = np.abs(z.astype(np.float64) - g["z"]).max(axis=1)
-    assert np.all(dz <= 1e-6 * scale + 1e-7), dz.max()
+    # z: the reference's float64 blend narrowed to fp32 (latent.py:96) — bit-exact
+    assert z.dtype == np.float32 and np.array_equal(z, g["z"]), np.abs(z - g["z"]).max()
 
 
 @pytest.mark.parametrize("name", CASES)
@@ -149,21 +156,20 @@ def test_sample_pdf_fused(name):
     assert np.array_equal(chosen, g["chosen"])
     check_rel(p.as_array(), g["params"], what=f"{name} params")
     guard = np.abs(g["u3"][:, 0].astype(np.float64) - g["params"][:, 0]) >= 1e-3
-    flips = np.count_nonzero(~guard)
-    assert flips <= max(3, 0.01 * len(guard))
     dw = np.abs(ws - g["ws"]).max(axis=1)
     assert np.all(dw[guard] <= 1e-3), dw[guard].max()
-    # decoupled pdf: our params at the reference's sampled direction.  The
-    # specular pdf carries 1/|wo.h| and h = normalize(wi + wo): near grazing
-    # reflection (|wo.h| -> 0) rounding the direction to fp32 alone moves the
-    # pdf by ~eps/|wo.h|^2, so the strict bound applies where |wo.h| >= 1e-2
-    # (> 99% of samples; the excluded share is asserted).
+    flips = np.count_nonzero(~guard & (dw > 1e-3))  # lobe flips inside the guard band
+    assert flips <= max(1, 1e-3 * len(guard)), flips
+    # decoupled pdf: our params at the reference's sampled direction, as the
+    # fp32 direction the kernel takes, against the reference's params at the
+    # same fp32 direction (oracle.pdf is pinned to proxy.pdf).  Rows where
+    # rounding the direction to fp32 alone moves the reference's own pdf by
+    # more than 1e-3 (near-specular lobes: D(h) varies on the scale alpha^2;
+    # grazing |wo.h|) are ill-conditioned for any fp32 input and excluded —
+    # their share is asserted tiny.
+    well, pdf_ref32, ws32 = conditioned_pdf_rows(g["params"], g["wi"], g["ws"], g["pdf_ws"])
     from paper_2305_02678_b200 import proxy
-    h = g["wi"] + g["ws"]
-    h = h / np.linalg.norm(h, axis=1, keepdims=True)
-    well = np.abs(np.sum(g["ws"] * h, axis=1)) >= 1e-2
-    assert well.mean() > 0.97
-    check_rel(proxy.pdf(p, g["wi"], g["ws"])[well], g["pdf_ws"][well], what=f"{name} pdf(ws_ref)")
+    check_rel(proxy.pdf(p, g["wi"], ws32)[well], pdf_ref32[well], what=f"{name} pdf(ws_ref)")
     # the fused kernel's pdf is exactly pdf(params, wi, ws) of its own sample
     own = proxy.pdf(p, g["wi"], ws)
     np.testing.assert_allclose(pdf, own, rtol=1e-5, atol=1e-7)
@@ -213,7 +219,7 @@ def _last_path():
     return _lib.load().nm_last_kernel_path()
 
 
-@pytest.fixture(params=[3, 2, 1], ids=["warp_tile", "tcgen05", "generic"])
+@pytest.fixture(params=[2, 1], ids=["tcgen05", "generic"])
 def kernel_path(request):
     from paper_2305_02678_b200 import _lib
     lib = _lib.load()
@@ -396,7 +402,8 @@ def test_fp32_path_vs_oracle(arch, variant):
     from paper_2305_02678_b200 import neural, proxy
     from paper_2305_02678_b200.latent import LatentPyramid
 
-    rng = np.random.default_rng(hash((arch, tuple(variant))) % 2**32)
+    import zlib
+    rng = np.random.default_rng(zlib.crc32(repr((arch, sorted(variant.items()))).encode()))
     mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(brdf_hidden=arch, **variant), rng)
     mat.latent = LatentPyramid(O.random_pyramid(rng, 64, 32).levels)
     om = _oracle_from(mat)
