@@ -149,6 +149,8 @@ def load():
         fn.argtypes = args
     if os.environ.get("NMQ_KERNEL_PATH"):  # experiments: force a kernel family (see nmq.h)
         lib.nm_set_kernel_path(int(os.environ["NMQ_KERNEL_PATH"]))
+    if os.environ.get("NMQ_TW_MARGIN"):  # experiments: exact-rounding queue bound (see nmq.h)
+        lib.nm_set_tw_margin(float(os.environ["NMQ_TW_MARGIN"]))
     _lib = lib
     return lib
 

@@ -549,6 +549,16 @@ __device__ __forceinline__ void frame_raw_seq(const MatParams& m, const uint32_t
 struct D3 {
   double x, y, z;
 };
+// 1/sqrt(x) for normal x > 0 to ~1 ulp: the hardware approximation refined by
+// two Newton steps (no library call; only a 1e-16 relative error matters here)
+__device__ __forceinline__ double drsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  y = y * fma(-h * y, y, 1.5);
+  return y;
+}
 __device__ __forceinline__ double ddot(D3 a, D3 b) { return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x)); }
 __device__ __forceinline__ D3 dcross(D3 a, D3 b) {
   return {fma(a.y, b.z, -a.z * b.y), fma(a.z, b.x, -a.x * b.z), fma(a.x, b.y, -a.y * b.x)};
@@ -563,18 +573,18 @@ __device__ __forceinline__ D3 dscale(D3 a, double s) { return {a.x * s, a.y * s,
 __device__ __forceinline__ void frame_tw64(const float* raw, V3 wi, V3 wo, float (&ti)[3], float (&to)[3]) {
   const D3 rn = {raw[0], raw[1], raw[2]};
   D3 rt = {raw[3], raw[4], raw[5]};
-  const D3 n = dscale(rn, rsqrt(fmax(ddot(rn, rn), 1e-24)));
+  const D3 n = dscale(rn, drsqrt(fmax(ddot(rn, rn), 1e-24)));
   D3 c = dcross(n, rt);
   double c2 = ddot(c, c);
   if (c2 < 1e-16) {  // |c| < 1e-8: fallback tangent n x e_argmin|n| (first index on ties)
     const double ax = fabs(n.x), ay = fabs(n.y), az = fabs(n.z);
     const D3 e = (ax <= ay && ax <= az) ? D3{1.0, 0.0, 0.0} : (ay <= az ? D3{0.0, 1.0, 0.0} : D3{0.0, 0.0, 1.0});
     const D3 f = dcross(n, e);
-    rt = dscale(f, rsqrt(ddot(f, f)));
+    rt = dscale(f, drsqrt(ddot(f, f)));
     c = dcross(n, rt);
     c2 = ddot(c, c);
   }
-  const D3 b = dscale(c, rsqrt(fmax(c2, 1e-24)));
+  const D3 b = dscale(c, drsqrt(fmax(c2, 1e-24)));
   const D3 t = dcross(b, n);
   const D3 di = {wi.x, wi.y, wi.z}, dout = {wo.x, wo.y, wo.z};
   ti[0] = (float)ddot(t, di); ti[1] = (float)ddot(b, di); ti[2] = (float)ddot(n, di);

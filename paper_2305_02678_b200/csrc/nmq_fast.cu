@@ -12,8 +12,7 @@
 // SIMT stage of slot s+1.  A tile's stages (eval, 2x32):
 //
 //     0  frame layer D -> frames, T.wi, T.wo (input chunk 1) -> BRDF layer 1;
-//        rows whose T.w may round differently from the reference go to the
-//        group's resolve ring, which is drained 128 rows at a time
+//        rows whose T.w may round differently from the reference are queued
 //     1  scaled leaky + hi/lo split                           -> BRDF layer 2
 //     2  BRDF output layer (CUDA cores), rgb store; blend the slot's next
 //        tile's prefetched texels -> input chunk 0 -> its frame layer
@@ -40,14 +39,21 @@
 // tensor-core frame layer and the fp32 frames here are within a small,
 // conditioning-scaled bound of those values; a row whose fast value lies
 // within that bound of an fp16 rounding midpoint is queued (input row, fp16
-// latent code, fast fp16 inputs) and later resolved in the reference's own
-// arithmetic (frame_raw_seq + frame_tw64); if its fp16 inputs differ, the
-// warp re-evaluates the BRDF decoder for it on the CUDA cores (fp32) and
-// overwrites its output.
+// latent code, fast fp16 inputs) in a per-CTA region of a global queue.  A
+// follow-up kernel (resolve_kernel, same stream, programmatic dependent
+// launch) recomputes each queued row's inputs in the reference's own
+// arithmetic (frame_raw_seq + frame_tw64); where an fp16 value differs, the
+// warp re-evaluates the BRDF decoder for that row on the CUDA cores (fp32)
+// and overwrites its output.  Nothing of it sits in the pipelined loop: a
+// call there constrains its register allocation (the prefetched texels
+// spill) and an SMEM ring takes the L1 the coarse pyramid levels live in
+// (both measured: -40 % / -8 % on C2).
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <utility>
 #include "tc.cuh"
 #include "nmq_device.cuh"
@@ -77,28 +83,22 @@ using namespace dev;
 #endif
 
 constexpr float kLk = 0.98019802570343017578f;  // fp32(99/101)
-#ifndef NMQ_X_NORESOLVE
-#define NMQ_X_NORESOLVE 0
-#endif
-#ifndef NMQ_X_NOCHECK
-#define NMQ_X_NOCHECK 0
-#endif
-#ifndef NMQ_EARLY_PREFETCH
-#define NMQ_EARLY_PREFETCH 1
-#endif
-#ifndef NMQ_X_NOAPPEND
-#define NMQ_X_NOAPPEND 0
-#endif
-#ifndef NMQ_X_F32BLEND
-#define NMQ_X_F32BLEND 0
-#endif
-constexpr int kRing = 384;  // resolve ring entries per group (3 batches: see the drain rule)
+
+// Exact-rounding queue of one launch: CTA b owns entries [b * cap, (b+1) * cap)
+// of `ent` (3 x 16 B each: {row, x16[0..2]}, {x16[3..5], z16[0]},
+// {z16[1..3], 0}) and writes how many it used to cnt[b] when it exits.
+struct ResolveQ {
+  uint4* ent;
+  uint32_t* cnt;
+  uint32_t cap;
+};
 
 struct FastConsts {
   uint32_t beta[4];  // fp16 (hi | lo << 16) of c^j
   float inv_brdf;    // 1 / c^(brdf leaky layers)
   float inv_samp;    // 1 / c^(sampler leaky layers)
   float tw_delta;    // error bound of the fast T.w per unit conditioning
+  ResolveQ q;        // BRDF modes
 };
 
 template <int MODE>
@@ -118,13 +118,6 @@ struct alignas(16) InBuf {
   float wi[3 * kTile];
   float wo[Need<MODE>::wo ? 3 * kTile : 4];
   float u3[Need<MODE>::u3 ? 3 * kTile : 4];
-};
-
-// per-group resolve ring (SoA)
-struct alignas(16) Ring {
-  uint32_t z16[kRing][4];  // fp16 latent code
-  uint32_t x16[kRing][6];  // fast fp16 [T.wi, T.wo]
-  int32_t row[kRing];      // absolute input row
 };
 
 template <int... I, class F>
@@ -236,27 +229,27 @@ __device__ __forceinline__ void mma_issue_first2(const GG& g, uint32_t f_tmem, u
   }
 }
 
-// D[0, W) -> scaled leaky -> (hi, lo) into A
+// D[0, W) -> scaled leaky -> (hi, lo) into A, in chunks of NMQ_EPI_COLS
+// columns (16 keeps the stage's register peak low; 32 halves the TMEM waits)
+#ifndef NMQ_EPI_COLS
+#define NMQ_EPI_COLS 16  // measured: 16 > 32 on C2 (30.1 vs 27.8 G q/s with the same kernel otherwise)
+#endif
 template <int W>
 __device__ __forceinline__ void hidden_epi(uint32_t dl, uint32_t al) {
-  if constexpr (W == 16) {
-    uint32_t r[16];
-    tc::tmem_ld16(dl, r);
+  constexpr int C = W < NMQ_EPI_COLS ? W : NMQ_EPI_COLS;
+#pragma unroll
+  for (int c0 = 0; c0 < W; c0 += C) {
+    uint32_t r[C];
+    if constexpr (C == 16) tc::tmem_ld16(dl + c0, r);
+    else tc::tmem_ld32(dl + c0, r);
     tc::tmem_ld_wait();
-    uint32_t hi[8], lo[8];
+    uint32_t hi[C / 2], lo[C / 2];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) split_scaled(r[2 * j], r[2 * j + 1], hi[j], lo[j]);
-    tc::tmem_st8(al, hi);
-    tc::tmem_st8(al + 8, lo);
-  } else {
-#pragma unroll
-    for (int c0 = 0; c0 < W; c0 += 32) {
-      uint32_t r[32];
-      tc::tmem_ld32(dl + c0, r);
-      tc::tmem_ld_wait();
-      uint32_t hi[16], lo[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) split_scaled(r[2 * j], r[2 * j + 1], hi[j], lo[j]);
+    for (int j = 0; j < C / 2; ++j) split_scaled(r[2 * j], r[2 * j + 1], hi[j], lo[j]);
+    if constexpr (C == 16) {
+      tc::tmem_st8(al + c0 / 2, hi);
+      tc::tmem_st8(al + W / 2 + c0 / 2, lo);
+    } else {
       tc::tmem_st16(al + c0 / 2, hi);
       tc::tmem_st16(al + W / 2 + c0 / 2, lo);
     }
@@ -402,13 +395,7 @@ __device__ __forceinline__ void blend_pack(const MatParams& mp, const TexPrefetc
   double w[4];
   weights64(frac64(ib.uv[2 * r], L.w), frac64(ib.uv[2 * r + 1], L.h), w);
   float z[8];
-#if NMQ_X_F32BLEND
-  float2 z2[4];
-  blend4x2(z2, p.tex, (float)w[1] + (float)w[3], (float)w[2] + (float)w[3]);
-  for (int c = 0; c < 4; ++c) { z[2*c] = z2[c].x; z[2*c+1] = z2[c].y; }
-#else
   blend64<true>(p.tex, w, z);
-#endif
 #pragma unroll
   for (int c = 0; c < 4; ++c) zp[c] = pack2(z[2 * c], z[2 * c + 1]);
 }
@@ -430,44 +417,152 @@ struct SlotSt {
   TexPrefetch nx;   // texels of the slot's next tile
 };
 
-// Resolve up to 128 ring entries [head, head + cnt): thread r takes entry
-// head + r, recomputes its direction inputs in the reference's arithmetic and,
-// where an fp16 value differs from the fast one, the warp re-evaluates the
-// decoder for that row and overwrites its outputs.  Every thread of the
-// group calls it (warp-collective shuffles inside).
-__device__ __noinline__ void resolve_batch(const MatParams& mp, const QueryArgs& a, const Ring& ring,
-                                           uint32_t head, uint32_t cnt, int r, bool seg_out) {
-  const bool act = (uint32_t)r < cnt;
-  const uint32_t slot = (head + (uint32_t)r) % (uint32_t)kRing;
-  uint32_t zh[4] = {0u, 0u, 0u, 0u}, xe[6] = {0u, 0u, 0u, 0u, 0u, 0u};
-  int32_t row = 0;
-  bool mism = false;
-  if (act) {
-    row = ring.row[slot];
+// Follow-up of a BRDF-mode launch: blocks (b, *) resolve the rows CTA b
+// queued.  Phase 1, one thread per entry: recompute the row's direction
+// inputs in the reference's arithmetic (tw_exact) and compare them with the
+// fast ones; rows that differ go to a block list.  Phase 2, one warp per
+// listed row: the BRDF decoder on the CUDA cores in fp32 (lane j owns hidden
+// units j and j + 32, weights staged in SMEM), overwriting the row's output.
+constexpr int kResolveThreads = 128;
+constexpr int kMaxBrdfLayers = 4;
+
+// fp32 BRDF weights in SMEM: layer l at resolve_w_off(l), row j at
+// j * stride_l: [w(fan_in), bias, pad to 16 bytes]
+__host__ __device__ inline int resolve_stride(const MatParams& mp, int l) {
+  return (mp.layers[mp.brdf_first + l].fan_in + 1 + 3) & ~3;
+}
+__host__ __device__ inline int resolve_w_off(const MatParams& mp, int l) {
+  int o = 0;
+  for (int i = 0; i < l; ++i) o += mp.layers[mp.brdf_first + i].out * resolve_stride(mp, i);
+  return o;
+}
+
+template <int BW, int BNH>
+__global__ void __launch_bounds__(kResolveThreads)
+resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
+               const __grid_constant__ FastConsts fc) {
+  constexpr int NL = BNH + 1;  // BRDF layers
+  static_assert(NL <= kMaxBrdfLayers, "layers");
+  extern __shared__ __align__(16) float sw[];
+  __shared__ int32_t l_row[kResolveThreads];
+  __shared__ uint32_t l_in16[kResolveThreads][10];
+  __shared__ uint32_t n_list;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // stage the BRDF weights (fp32, the reference's packed order) with
+  // 16-byte aligned rows; independent of the fast kernel's results
+  int w_off[NL], w_st[NL];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) zh[c] = ring.z16[slot][c];
-    const V3 wi = ldg3(a.wi, row), wo = ldg3(a.wo, row);
-    tw_exact(mp, zh, wi, wo, xe);
-#pragma unroll
-    for (int c = 0; c < 6; ++c) mism |= xe[c] != ring.x16[slot][c];
+  for (int l = 0; l < NL; ++l) {
+    w_off[l] = resolve_w_off(mp, l);
+    w_st[l] = resolve_stride(mp, l);
+    const LayerDesc& L = mp.layers[mp.brdf_first + l];
+    const int fi = L.fan_in, fo = L.out;
+    for (int i = tid; i < fo * (fi + 1); i += kResolveThreads)
+      sw[w_off[l] + (i / (fi + 1)) * w_st[l] + i % (fi + 1)] = __ldg(mp.w32 + L.w32_off + i);
   }
-  uint32_t mm = __ballot_sync(0xffffffffu, mism);
-  while (mm) {
-    const int src = __ffs(mm) - 1;
-    mm &= mm - 1;
-    const uint32_t in16[10] = {zh[0], zh[1], zh[2], zh[3], xe[0], xe[1], xe[2], xe[3], xe[4], xe[5]};
-    float y[6];
-    brdf_simt_warp(mp, in16, src, y);
-    if ((r & 31) == src) {
-      const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + row) : (int64_t)row;
-      // queued rows are above the horizon (below it the output is 0 either way)
-      stg3(a.rgb, q, v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])));
-      if (mp.albedo && a.albedo) stg3(a.albedo, q, v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f)));
+  if (tid == 0) n_list = 0u;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast kernel's queue and outputs
+  const uint32_t n = fc.q.cnt[blockIdx.x];
+  const uint4* ent = fc.q.ent + 3 * (size_t)blockIdx.x * fc.q.cap;
+  const bool seg_out = a.out_idx != nullptr;
+  __syncthreads();
+  const uint32_t step = kResolveThreads * gridDim.y;
+  for (uint32_t b0 = blockIdx.y * kResolveThreads; b0 < n; b0 += step) {
+    const uint32_t i = b0 + tid;
+    if (i < n) {
+      const uint4 e0 = __ldg(ent + 3 * i), e1 = __ldg(ent + 3 * i + 1), e2 = __ldg(ent + 3 * i + 2);
+      const int32_t row = (int32_t)e0.x;
+      const uint32_t zh[4] = {e1.w, e2.x, e2.y, e2.z};
+      const V3 wi = ldg3(a.wi, row), wo = ldg3(a.wo, row);
+      uint32_t xe[6];
+      tw_exact(mp, zh, wi, wo, xe);
+      if (xe[0] != e0.y || xe[1] != e0.z || xe[2] != e0.w || xe[3] != e1.x || xe[4] != e1.y || xe[5] != e1.z) {
+        const uint32_t k = atomicAdd(&n_list, 1u);
+        l_row[k] = row;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) l_in16[k][c] = zh[c];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) l_in16[k][4 + c] = xe[c];
+      }
     }
+    __syncthreads();
+    const uint32_t nl = n_list;
+    for (uint32_t k = warp; k < nl; k += kResolveThreads / 32) {
+      // layer 0: inputs [z(8), T.wi(6), T.wo(6)] as fp16 (the reference rounds them once)
+      float x[20];
+#pragma unroll
+      for (int c = 0; c < 10; ++c) {
+        const float2 f = unpack_h2(l_in16[k][c]);
+        x[2 * c] = f.x;
+        x[2 * c + 1] = f.y;
+      }
+      float h0 = 0.f, h1 = 0.f;
+      {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int j = lane + 32 * u;
+          if (j < BW) {
+            const float* w = sw + w_off[0] + j * w_st[0];
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < 20; ++q) acc = __fmaf_rn(x[q], w[q], acc);
+            acc += w[20];
+            acc = acc >= 0.f ? acc : kLeaky * acc;
+            (u ? h1 : h0) = acc;
+          }
+        }
+      }
+#pragma unroll
+      for (int l = 1; l < BNH; ++l) {  // hidden layers BW -> BW
+        float n0 = 0.f, n1 = 0.f;
+        const float* w0 = sw + w_off[l] + (lane < BW ? lane : 0) * w_st[l];
+        const float* w1 = sw + w_off[l] + (lane + 32 < BW ? lane + 32 : 0) * w_st[l];
+#pragma unroll
+        for (int q = 0; q < BW; ++q) {  // every lane takes part in the shuffles
+          const float hq = __shfl_sync(0xffffffffu, q < 32 ? h0 : h1, q & 31);
+          n0 = __fmaf_rn(hq, w0[q], n0);
+          if (BW > 32) n1 = __fmaf_rn(hq, w1[q], n1);
+        }
+        n0 += w0[BW];
+        n0 = lane < BW ? (n0 >= 0.f ? n0 : kLeaky * n0) : 0.f;
+        if (BW > 32) {
+          n1 += w1[BW];
+          n1 = lane + 32 < BW ? (n1 >= 0.f ? n1 : kLeaky * n1) : 0.f;
+        }
+        h0 = n0;
+        h1 = n1;
+      }
+      // output layer BW -> 3 (6 with albedo): partial products, warp sums
+      const float* wo_ = sw + w_off[BNH];
+      const int st = w_st[BNH], fo = mp.layers[mp.brdf_first + BNH].out;
+      float y[6];
+#pragma unroll
+      for (int o = 0; o < 6; ++o) {
+        float p = 0.f;
+        if (o < fo) {
+          if (lane < BW) p = h0 * wo_[o * st + lane];
+          if (lane + 32 < BW) p = __fmaf_rn(h1, wo_[o * st + lane + 32], p);
+#pragma unroll
+          for (int d = 16; d > 0; d >>= 1) p += __shfl_xor_sync(0xffffffffu, p, d);
+          p += wo_[o * st + BW];
+        }
+        y[o] = p;
+      }
+      if (lane == 0) {
+        const int32_t row = l_row[k];
+        const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + row) : (int64_t)row;
+        // queued rows are above the horizon (below it the output is 0 either way)
+        stg3(a.rgb, q, v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])));
+        if (mp.albedo && a.albedo) stg3(a.albedo, q, v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f)));
+      }
+    }
+    __syncthreads();
+    if (tid == 0) n_list = 0u;
+    __syncthreads();
   }
 }
 
-template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG>
+template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG, bool DBG = false>
 __global__ void __launch_bounds__(G * 128, 1)
 fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
             const __grid_constant__ FastConsts fc) {
@@ -476,7 +571,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   __shared__ uint64_t in_bar[G][NS][2];
   __shared__ uint64_t w_bar;  // weights staged by TMA
   __shared__ uint32_t tbase_sh;
-  __shared__ uint32_t ring_tail[G];  // resolve ring: entries appended so far (group counter)
+  __shared__ uint32_t q_cnt;  // BRDF modes: rows this CTA queued for exact resolution
   constexpr bool kBrdf = Need<MODE>::brdf, kSamp = Need<MODE>::samp;
   // stage layout of one tile (see the file comment)
   // query: the sampler's first layer reads the same input chunk 0 as the
@@ -508,12 +603,9 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   // TS: per-row 64-byte texel slots after all input buffers
   const uint32_t tex_row = tc::smem_u32(smem + wbytes + G * NS * 2 * sizeof(InBuf<MODE>)) +
                            (uint32_t)((gi * NS) * kTile + tid % 128) * 64u;
-  // BRDF modes: the group's resolve ring after the texel slots
-  Ring& ring = *(reinterpret_cast<Ring*>(smem + wbytes + G * NS * 2 * sizeof(InBuf<MODE>) +
-                                         (TS ? G * NS * kTile * 64 : 0)) + gi);
 
   // --- CTA setup --------------------------------------------------------------
-  if (tid < G) ring_tail[tid] = 0u;
+  if (tid == 0) q_cnt = 0u;
   if (tid < G * NS) {
     tc::mbar_init(&mma_bar[tid / NS][tid % NS], 1);
     tc::mbar_init(&in_bar[tid / NS][tid % NS][0], 1);
@@ -574,9 +666,6 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   const int sstride = stride * NS;                         // between a slot's tiles
   const bool want_level = a.level != nullptr;
   const bool want_albedo = mp.albedo && a.albedo;
-  // resolve ring bookkeeping (same values on every thread of the group):
-  // entries [rhead, rprev) belong to earlier tiles, [rprev, rtail) to the current one
-  uint32_t rhead = 0, rprev = 0, rtail = 0;
 
   SlotSt sl[NS];
 #pragma unroll
@@ -662,19 +751,14 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           if (want_level) {
             if (valid) a.level[seg_out ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in] = S.level;
           }
-          // the slot's next tile: texel loads now (BRDF modes: after this
-          // stage's frame work, which would otherwise hold them in registers
-          // through its peak), blended at the last stage
-          auto prefetch = [&]() {
-            if (S.t + sstride < ntiles) {
-              wait_in(S, s, b ^ 1, S.t + sstride);
-              if constexpr (TS)
-                prefetch_texels_smem<MODE>(mp, a, buf(s, b ^ 1), r, lod0, tex_row + s * kTile * 64u, S.nx);
-              else
-                prefetch_texels<MODE>(mp, a, buf(s, b ^ 1), r, lod0, S.nx);
-            }
-          };
-          if constexpr (!kBrdf || NMQ_EARLY_PREFETCH) prefetch();
+          // the slot's next tile: texel loads now, blended at the last stage
+          if (S.t + sstride < ntiles) {
+            wait_in(S, s, b ^ 1, S.t + sstride);
+            if constexpr (TS)
+              prefetch_texels_smem<MODE>(mp, a, buf(s, b ^ 1), r, lod0, tex_row + s * kTile * 64u, S.nx);
+            else
+              prefetch_texels<MODE>(mp, a, buf(s, b ^ 1), r, lod0, S.nx);
+          }
           auto refill = [&]() {  // after the barrier: every row of buffer b was read
             if (t2 < last_full) {
               if (r == 32 * ((LW + 2) % 4))
@@ -700,38 +784,29 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             tc::tmem_st8(S.al + 8, x);
             // exact rounding: a direction input within its error bound of an
             // fp16 midpoint (bound = tw_delta x conditioning of its frame)
-#if NMQ_X_CONSTD
-            const float2 d1 = make_float2(fc.tw_delta, fc.tw_delta), d2 = d1;
-#else
             const float2 d1 = make_float2(fc.tw_delta * kappa.x, fc.tw_delta * kappa.x);
             const float2 d2 = make_float2(fc.tw_delta * kappa.y, fc.tw_delta * kappa.y);
-#endif
             const float2 d12 = make_float2(d1.x, d2.x);
             const uint32_t near = near_mid2(ti[0], ti[1], d1) | near_mid2(ti[2], ti[3], d12) |
                                   near_mid2(ti[4], ti[5], d2) | near_mid2(to[0], to[1], d1) |
                                   near_mid2(to[2], to[3], d12) | near_mid2(to[4], to[5], d2);
-            const bool flag = !NMQ_X_NOCHECK && valid && S.up && near != 0u;
-            // queue this tile's flagged rows (one shared atomic per warp); they
-            // are resolved from the last stage of a later tile
+            const bool flag = valid && S.up && near != 0u;
+            // queue the tile's flagged rows (one shared atomic per warp)
             const uint32_t wmask = __ballot_sync(0xffffffffu, flag);
-            if (NMQ_X_NOAPPEND) { rtail += wmask != 0; } else if (wmask) {
+            if (wmask) {
+              const int lead = __ffs(wmask) - 1;
               uint32_t wbase = 0;
-              if ((r & 31) == __ffs(wmask) - 1) wbase = atomicAdd(&ring_tail[gi], __popc(wmask));
-              wbase = __shfl_sync(0xffffffffu, wbase, __ffs(wmask) - 1);
+              if ((r & 31) == lead) wbase = atomicAdd(&q_cnt, __popc(wmask));
+              wbase = __shfl_sync(0xffffffffu, wbase, lead);
               if (flag) {
-                const uint32_t slot = (wbase + __popc(wmask & lanemask_lt())) % (uint32_t)kRing;
-                ring.row[slot] = (int32_t)(seg_base + q_in);
-#pragma unroll
-                for (int c = 0; c < 4; ++c) ring.z16[slot][c] = S.zp[c];
-#pragma unroll
-                for (int c = 0; c < 6; ++c) ring.x16[slot][c] = x[c];
+                uint4* e = fc.q.ent + 3 * ((size_t)blockIdx.x * fc.q.cap + wbase + __popc(wmask & lanemask_lt()));
+                e[0] = make_uint4((uint32_t)(seg_base + q_in), x[0], x[1], x[2]);
+                e[1] = make_uint4(x[3], x[4], x[5], S.zp[0]);
+                e[2] = make_uint4(S.zp[1], S.zp[2], S.zp[3], 0u);
               }
             }
             mma_issue<BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, refill);
-            if constexpr (!NMQ_EARLY_PREFETCH) prefetch();
-            rprev = rtail;            // entries of tiles before this one
-            rtail = ring_tail[gi];    // complete: every warp appended before the barrier
-            if (a.dbg && valid) {  // calibration dump (tools/tw_calibrate.py)
+            if (DBG && valid) {  // calibration dump (tools/tw_calibrate.py)
               float* o = a.dbg + 14 * (seg_base + q_in);
 #pragma unroll
               for (int j = 0; j < 6; ++j) { o[j] = ti[j]; o[6 + j] = to[j]; }
@@ -813,20 +888,11 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
         if constexpr (k == kFinal) {
           // the slot's next tile: blend its texels, issue its first MMA
           const int tn = S.t + sstride;
-          // resolve ring: rows queued by earlier tiles (this tile's were queued
-          // at stage 0; its outputs are stored in this stage without a barrier)
           if (tn < ntiles) {
             if constexpr (TS) land_texels_smem(tex_row + s * kTile * 64u, S.nx);
             blend_pack<MODE>(mp, S.nx, buf(s, b ^ 1), r, S.zp);
             S.level = S.nx.level;
             issue_first(S, buf(s, b ^ 1), std::integral_constant<int, LW>{});
-          }
-          if constexpr (kBrdf) {
-            // earlier tiles' outputs were stored before this tile's stage-0 barrier
-            if (!NMQ_X_NORESOLVE && rprev - rhead >= (uint32_t)kTile) {
-              resolve_batch(mp, a, ring, rhead, kTile, r, seg_out);
-              rhead += kTile;
-            }
           }
           S.t = tn;
           S.it += 1;
@@ -834,21 +900,13 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       });
     });
   }
-  if constexpr (kBrdf) {
-    // drain the resolve ring (the last tiles' outputs are stored before the barrier)
-    tc::named_bar(g.bar_id, 128);
-    while (rtail != rhead) {
-      const uint32_t c = rtail - rhead < (uint32_t)kTile ? rtail - rhead : (uint32_t)kTile;
-      resolve_batch(mp, a, ring, rhead, c, r, seg_out);
-      rhead += c;
-    }
-  }
   if constexpr (NMQ_PDL) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 0) tc::tmem_free<kTmemCols>(tb);
+  if (kBrdf && tid == 0) fc.q.cnt[blockIdx.x] = q_cnt;
 }
 
 uint32_t fp16_bits(double v) {
@@ -894,6 +952,64 @@ namespace {
 #define NMQ_TEX_SMEM (1 << kModeSamplePdf)
 #endif
 
+// Exact-rounding queue storage: one grow-only buffer per (device, stream) —
+// launches on one stream are ordered, so consecutive launches reuse it;
+// concurrent streams never share one.  Growth is stream-ordered
+// (cudaMallocAsync / cudaFreeAsync on the launch stream).
+struct QueueBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_qmu;
+std::map<std::pair<int, cudaStream_t>, QueueBuf> g_queues;
+
+cudaError_t queue_for(cudaStream_t s, size_t bytes, void** out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(g_qmu);
+  QueueBuf& q = g_queues[{dev, s}];
+  if (q.bytes < bytes) {
+    if (q.p) {
+      const cudaError_t e = cudaFreeAsync(q.p, s);
+      if (e != cudaSuccess) return e;
+      q.p = nullptr;
+      q.bytes = 0;
+    }
+    const size_t want = bytes + bytes / 4;
+    const cudaError_t e = cudaMallocAsync(&q.p, want, s);
+    if (e != cudaSuccess) return e;
+    q.bytes = want;
+  }
+  *out = q.p;
+  return cudaSuccess;
+}
+
+// non-segment launches larger than this run as several (fast, resolve)
+// pairs, which bounds the queue at kChunkRows entries per stream
+constexpr int64_t kChunkRows = int64_t(1) << 24;
+constexpr unsigned kResolveSlices = 16;  // resolve blocks per fast-kernel CTA
+
+template <class K>
+cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, const MatParams& mp,
+                       const QueryArgs& a, const FastConsts& fc) {
+  if constexpr (NMQ_PDL) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, mp, a, fc);
+  } else {
+    kern<<<grid, block, smem, s>>>(mp, a, fc);
+    return cudaGetLastError();
+  }
+}
+
 template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS,
           bool TS = ((NMQ_TEX_SMEM >> MODE) & 1) != 0>
 cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t s) {
@@ -904,11 +1020,34 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   }
   const bool seg = a.seg || a.out_idx;
   if (seg && MODE != kModeEval) return cudaErrorNotSupported;  // binned segments are eval-only
-  auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, (MODE == kModeEval)>
-                  : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
   constexpr bool kBrdf = Need<MODE>::brdf;
+  if (kBrdf && !seg && a.n > kChunkRows) {
+    for (int64_t c0 = 0; c0 < a.n; c0 += kChunkRows) {
+      QueryArgs c = a;
+      c.n = a.n - c0 < kChunkRows ? a.n - c0 : kChunkRows;
+      c.uv = a.uv + 2 * c0;
+      c.lod = a.lod_stride ? a.lod + c0 : a.lod;
+      c.u_rr = a.u_rr + c0;
+      c.wi = a.wi + 3 * c0;
+      if (a.wo) c.wo = a.wo + 3 * c0;
+      if (a.u3) c.u3 = a.u3 + 3 * c0;
+      if (a.rgb) c.rgb = a.rgb + 3 * c0;
+      if (a.albedo) c.albedo = a.albedo + 3 * c0;
+      if (a.ws) c.ws = a.ws + 3 * c0;
+      if (a.pdf) c.pdf = a.pdf + c0;
+      if (a.params9) c.params9 = a.params9 + 9 * c0;
+      if (a.level) c.level = a.level + c0;
+      if (a.dbg) c.dbg = a.dbg + 14 * c0;
+      const cudaError_t e = launch_fast_t<MODE, BW, BNH, SW, SNH, G, NS, TS>(mp, c, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, (MODE == kModeEval)>
+                  : (a.dbg && MODE == kModeEval) ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false, true>
+                                                 : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
   const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>) +
-                         (TS ? G * NS * kTile * 64 : 0) + (kBrdf ? G * sizeof(Ring) : 0));
+                         (TS ? G * NS * kTile * 64 : 0));
   const int max_dyn = std::min(max_dynamic_smem((const void*)fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>),
                                max_dynamic_smem((const void*)kern));
   if (max_dyn < 0) return cudaErrorInvalidValue;
@@ -918,25 +1057,29 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid > (ntiles + G - 1) / G) grid = (ntiles + G - 1) / G;
   if (grid < 1) grid = 1;
-  const FastConsts fc = make_consts(BNH, SNH);
-  cudaError_t e;
-  if constexpr (NMQ_PDL) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(G * 128);
-    cfg.dynamicSmemBytes = (size_t)smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kern, mp, a, fc);
+  FastConsts fc = make_consts(BNH, SNH);
+  if constexpr (kBrdf) {
+    // a CTA runs at most G * NS * ceil(ntiles / (grid * G * NS)) tiles
+    const int64_t per = (int64_t)G * NS * ((ntiles + grid * G * NS - 1) / (grid * G * NS)) * kTile;
+    void* qb = nullptr;
+    const size_t ent_bytes = (size_t)grid * per * 48;
+    cudaError_t e = queue_for(s, ent_bytes + (size_t)grid * 4, &qb);
     if (e != cudaSuccess) return e;
-  } else {
-    kern<<<(int)grid, G * 128, smem, s>>>(mp, a, fc);
+    fc.q.ent = reinterpret_cast<uint4*>(qb);
+    fc.q.cnt = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(qb) + ent_bytes);
+    fc.q.cap = (uint32_t)per;
   }
+  cudaError_t e = launch_pdl(kern, dim3((unsigned)grid), dim3(G * 128), (size_t)smem, s, mp, a, fc);
+  if (e != cudaSuccess) return e;
   ++g_launches;
+  if constexpr (kBrdf) {
+    const int rs = resolve_w_off(mp, BNH + 1) * 4;
+    if (max_dynamic_smem((const void*)resolve_kernel<BW, BNH>) < rs) return cudaErrorInvalidValue;
+    e = launch_pdl(resolve_kernel<BW, BNH>, dim3((unsigned)grid, kResolveSlices), dim3(kResolveThreads),
+                   (size_t)rs, s, mp, a, fc);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+  }
   return cudaGetLastError();
 }
 
