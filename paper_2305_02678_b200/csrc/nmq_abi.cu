@@ -377,8 +377,11 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
     if ((rc = pack_chain(fv, pk, mp, nl, "frame layer")) != NM_OK) { delete m; return rc; }
     append_w32(fv, mp.precise, w32, mp, mp.frame_layer);
     // frame layer [W | b] in fp32 for the sequential-FMA evaluation (mlp.py:207)
-    for (int n = 0; n < 6 * d->n_frames; ++n)
-      for (int k = 0; k <= 8; ++k) mp.fw[n][k] = w32[mp.layers[mp.frame_layer].w32_off + n * 9 + k];
+    for (int n = 0; n < 6; ++n)
+      for (int k = 0; k <= 8; ++k) {
+        const size_t o = mp.layers[mp.frame_layer].w32_off;
+        mp.fw2[n][k] = make_float2(w32[o + n * 9 + k], d->n_frames == 2 ? w32[o + (n + 6) * 9 + k] : 0.f);
+      }
   }
   const int brdf_in = d->use_frames ? 8 + 6 * d->n_frames : 14;
   mp.brdf_in = brdf_in;

@@ -524,8 +524,7 @@ __device__ __forceinline__ float2 unpack_h2(uint32_t v) {
 // fp32 `x @ W.T` (OpenBLAS sgemm: one fused multiply-add per k, k = 0..7,
 // in order; pinned by tests/test_oracle_golden.py) then `+ b` (mlp.py:207).
 // x = the fp16 latent code (4 packed pairs).
-__device__ __forceinline__ void frame_raw_seq(const MatParams& m, const uint32_t (&zh)[4], int n_out,
-                                              float (&raw)[12]) {
+__device__ __forceinline__ void frame_raw_seq(const MatParams& m, const uint32_t (&zh)[4], float (&raw)[12]) {
   float x[8];
 #pragma unroll
   for (int c = 0; c < 4; ++c) {
@@ -533,16 +532,15 @@ __device__ __forceinline__ void frame_raw_seq(const MatParams& m, const uint32_t
     x[2 * c] = f.x;
     x[2 * c + 1] = f.y;
   }
+  // output j of both frames at once (two independent fp32 FMA chains per FFMA2)
 #pragma unroll
-  for (int j = 0; j < 12; ++j) {
-    if (j < n_out) {
-      float acc = x[0] * m.fw[j][0];
+  for (int j = 0; j < 6; ++j) {
+    float2 acc = __fmul2_rn(make_float2(x[0], x[0]), m.fw2[j][0]);
 #pragma unroll
-      for (int k = 1; k < 8; ++k) acc = __fmaf_rn(x[k], m.fw[j][k], acc);
-      raw[j] = __fadd_rn(acc, m.fw[j][8]);
-    } else {
-      raw[j] = 0.f;
-    }
+    for (int k = 1; k < 8; ++k) acc = __ffma2_rn(make_float2(x[k], x[k]), m.fw2[j][k], acc);
+    acc = __fadd2_rn(acc, m.fw2[j][8]);
+    raw[j] = acc.x;
+    raw[j + 6] = acc.y;
   }
 }
 
@@ -595,13 +593,13 @@ __device__ __forceinline__ void frame_tw64(const float* raw, V3 wi, V3 wo, float
 // x16 = fp16 pairs of [T.wi (3 per frame), T.wo (3 per frame)] for n_frames
 // frames, from the latent code's fp16 pairs.
 __device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
-                                         uint32_t (&x16)[6]) {
+                                         uint32_t (&x16)[6], uint32_t frames = 3u) {
   float raw[12];
-  frame_raw_seq(m, zh, 6 * m.n_frames, raw);
+  frame_raw_seq(m, zh, raw);
   float ti[6], to[6];
 #pragma unroll
   for (int f = 0; f < 2; ++f) {
-    if (f < m.n_frames) {
+    if (f < m.n_frames && ((frames >> f) & 1u)) {
       float a[3], b[3];
       frame_tw64(raw + 6 * f, wi, wo, a, b);
 #pragma unroll
@@ -621,6 +619,12 @@ __device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh
     x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], to[0]); x16[2] = pack_h2(to[1], to[2]);
     x16[3] = x16[4] = x16[5] = 0u;
   }
+}
+
+// fp16 halves of the 2-frame decoder direction words that belong to frame 0
+// (the rest to frame 1): [t1.wi b1.wi | n1.wi t2.wi | b2.wi n2.wi | same for wo]
+__device__ __forceinline__ uint32_t frame0_halves(int word) {
+  return (word == 0 || word == 3) ? 0xFFFFFFFFu : ((word == 1 || word == 4) ? 0x0000FFFFu : 0u);
 }
 
 // Warp-cooperative re-evaluation of one query's BRDF decoder on the CUDA

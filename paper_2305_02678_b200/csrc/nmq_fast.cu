@@ -85,8 +85,10 @@ using namespace dev;
 constexpr float kLk = 0.98019802570343017578f;  // fp32(99/101)
 
 // Exact-rounding queue of one launch: CTA b owns entries [b * cap, (b+1) * cap)
-// of `ent` (3 x 16 B each: {row, x16[0..2]}, {x16[3..5], z16[0]},
-// {z16[1..3], 0}) and writes how many it used to cnt[b] when it exits.
+// of `ent` (kQueueWords x 16 B each: {row, x16[0..2]}, {x16[3..5], z16[0]},
+// {z16[1..3], wi.x}, {wi.y, wi.z, wo.x, wo.y}, {wo.z, frames to resolve, 0, 0}) and writes how
+// many it used to cnt[b] when it exits.
+constexpr int kQueueWords = 5;
 struct ResolveQ {
   uint4* ent;
   uint32_t* cnt;
@@ -422,143 +424,140 @@ struct SlotSt {
 // inputs in the reference's arithmetic (tw_exact) and compare them with the
 // fast ones; rows that differ go to a block list.  Phase 2, one warp per
 // listed row: the BRDF decoder on the CUDA cores in fp32 (lane j owns hidden
-// units j and j + 32, weights staged in SMEM), overwriting the row's output.
-constexpr int kResolveThreads = 128;
-constexpr int kMaxBrdfLayers = 4;
+// units j and j + 32), its fp16 weights read straight from the material's
+// UMMA blob (row n's 8-value K chunk c at b_off + c * n_pad * 16 + n * 16:
+// one 16-byte load each, all issued up front) and the output layer from the
+// fp32 copy in the parameter block.
+constexpr int kResolveThreads = 512;
 
-// fp32 BRDF weights in SMEM: layer l at resolve_w_off(l), row j at
-// j * stride_l: [w(fan_in), bias, pad to 16 bytes]
-__host__ __device__ inline int resolve_stride(const MatParams& mp, int l) {
-  return (mp.layers[mp.brdf_first + l].fan_in + 1 + 3) & ~3;
-}
-__host__ __device__ inline int resolve_w_off(const MatParams& mp, int l) {
-  int o = 0;
-  for (int i = 0; i < l; ++i) o += mp.layers[mp.brdf_first + i].out * resolve_stride(mp, i);
-  return o;
+__device__ __forceinline__ void load_row8(const MatParams& mp, uint32_t off, int n_pad, int n, int c,
+                                          float (&w)[8]) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(mp.wblob) + off +
+                                                       (size_t)c * n_pad * 16 + (size_t)n * 16));
+  const uint32_t u[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = unpack_h2(u[i]);
+    w[2 * i] = f.x;
+    w[2 * i + 1] = f.y;
+  }
 }
 
 template <int BW, int BNH>
-__global__ void __launch_bounds__(kResolveThreads)
+__global__ void __launch_bounds__(kResolveThreads, 2)
 resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
                const __grid_constant__ FastConsts fc) {
-  constexpr int NL = BNH + 1;  // BRDF layers
-  static_assert(NL <= kMaxBrdfLayers, "layers");
-  extern __shared__ __align__(16) float sw[];
-  __shared__ int32_t l_row[kResolveThreads];
-  __shared__ uint32_t l_in16[kResolveThreads][10];
-  __shared__ uint32_t n_list;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  // stage the BRDF weights (fp32, the reference's packed order) with
-  // 16-byte aligned rows; independent of the fast kernel's results
-  int w_off[NL], w_st[NL];
-#pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    w_off[l] = resolve_w_off(mp, l);
-    w_st[l] = resolve_stride(mp, l);
-    const LayerDesc& L = mp.layers[mp.brdf_first + l];
-    const int fi = L.fan_in, fo = L.out;
-    for (int i = tid; i < fo * (fi + 1); i += kResolveThreads)
-      sw[w_off[l] + (i / (fi + 1)) * w_st[l] + i % (fi + 1)] = __ldg(mp.w32 + L.w32_off + i);
-  }
-  if (tid == 0) n_list = 0u;
+  const int lane = threadIdx.x & 31;
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast kernel's queue and outputs
   const uint32_t n = fc.q.cnt[blockIdx.x];
-  const uint4* ent = fc.q.ent + 3 * (size_t)blockIdx.x * fc.q.cap;
+  const uint4* ent = fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap;
   const bool seg_out = a.out_idx != nullptr;
-  __syncthreads();
   const uint32_t step = kResolveThreads * gridDim.y;
-  for (uint32_t b0 = blockIdx.y * kResolveThreads; b0 < n; b0 += step) {
-    const uint32_t i = b0 + tid;
+  for (uint32_t b0 = blockIdx.y * kResolveThreads; b0 < n; b0 += step) {  // warp-uniform trip count
+    const uint32_t i = b0 + threadIdx.x;
+    uint32_t zh[4] = {0u, 0u, 0u, 0u}, xe[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+    int32_t row = 0;
+    bool mism = false;
     if (i < n) {
-      const uint4 e0 = __ldg(ent + 3 * i), e1 = __ldg(ent + 3 * i + 1), e2 = __ldg(ent + 3 * i + 2);
-      const int32_t row = (int32_t)e0.x;
-      const uint32_t zh[4] = {e1.w, e2.x, e2.y, e2.z};
-      const V3 wi = ldg3(a.wi, row), wo = ldg3(a.wo, row);
-      uint32_t xe[6];
-      tw_exact(mp, zh, wi, wo, xe);
-      if (xe[0] != e0.y || xe[1] != e0.z || xe[2] != e0.w || xe[3] != e1.x || xe[4] != e1.y || xe[5] != e1.z) {
-        const uint32_t k = atomicAdd(&n_list, 1u);
-        l_row[k] = row;
+      const uint4* e = ent + kQueueWords * (size_t)i;
+      const uint4 e0 = __ldg(e), e1 = __ldg(e + 1), e2 = __ldg(e + 2), e3 = __ldg(e + 3), e4 = __ldg(e + 4);
+      row = (int32_t)e0.x;
+      zh[0] = e1.w; zh[1] = e2.x; zh[2] = e2.y; zh[3] = e2.z;
+      const V3 wi = v3(__uint_as_float(e2.w), __uint_as_float(e3.x), __uint_as_float(e3.y));
+      const V3 wo = v3(__uint_as_float(e3.z), __uint_as_float(e3.w), __uint_as_float(e4.x));
+      // only frames with a value near a rounding midpoint need the float64 path
+      // (warp-uniform choice: a per-lane one would serialize both paths anyway)
+      const uint32_t fm = __reduce_or_sync(__activemask(), e4.y);
+      tw_exact(mp, zh, wi, wo, xe, fm);
+      const uint32_t xf[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) l_in16[k][c] = zh[c];
-#pragma unroll
-        for (int c = 0; c < 6; ++c) l_in16[k][4 + c] = xe[c];
+      for (int c = 0; c < 6; ++c) {
+        const uint32_t own = (fm & 1u ? frame0_halves(c) : 0u) | (fm & 2u ? ~frame0_halves(c) : 0u);
+        xe[c] = (xe[c] & own) | (xf[c] & ~own);  // frames not recomputed keep their fast values
+        mism |= xe[c] != xf[c];
       }
     }
-    __syncthreads();
-    const uint32_t nl = n_list;
-    for (uint32_t k = warp; k < nl; k += kResolveThreads / 32) {
-      // layer 0: inputs [z(8), T.wi(6), T.wo(6)] as fp16 (the reference rounds them once)
+    // the warp re-evaluates each of its rows whose inputs round differently
+    uint32_t mm = __ballot_sync(0xffffffffu, mism);
+    while (mm) {
+      const int src = __ffs(mm) - 1;
+      mm &= mm - 1;
+      // BRDF layer 1 on input chunk [z(8) | wi-slot, bias @ 3 | T.wi(6), T.wo(6)]
+      // (the pipelined kernels' K order, fill_fast_layers): rows j, j + 32
       float x[20];
 #pragma unroll
       for (int c = 0; c < 10; ++c) {
-        const float2 f = unpack_h2(l_in16[k][c]);
+        const float2 f = unpack_h2(__shfl_sync(0xffffffffu, c < 4 ? zh[c & 3] : xe[(c - 4) % 6], src));
         x[2 * c] = f.x;
         x[2 * c + 1] = f.y;
       }
-      float h0 = 0.f, h1 = 0.f;
-      {
+      const int j0 = lane < BW ? lane : 0, j1 = lane + 32 < BW ? lane + 32 : 0;
+      float w1[2][4][8];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int j = lane + 32 * u;
-          if (j < BW) {
-            const float* w = sw + w_off[0] + j * w_st[0];
-            float acc = 0.f;
+      for (int u = 0; u < (BW > 32 ? 2 : 1); ++u)
 #pragma unroll
-            for (int q = 0; q < 20; ++q) acc = __fmaf_rn(x[q], w[q], acc);
-            acc += w[20];
-            acc = acc >= 0.f ? acc : kLeaky * acc;
-            (u ? h1 : h0) = acc;
-          }
-        }
+        for (int c = 0; c < 4; ++c) load_row8(mp, mp.fast_l1_off, BW, u ? j1 : j0, c, w1[u][c]);
+      float h[2] = {0.f, 0.f};
+#pragma unroll
+      for (int u = 0; u < (BW > 32 ? 2 : 1); ++u) {
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = __fmaf_rn(x[q], w1[u][0][q], acc);  // z
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc = __fmaf_rn(x[8 + q], w1[u][2][q], acc);  // T.wi, T.wo[0..1]
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc = __fmaf_rn(x[16 + q], w1[u][3][q], acc);  // T.wo[2..5]
+        acc += w1[u][1][3];  // bias
+        h[u] = acc >= 0.f ? acc : kLeaky * acc;
       }
 #pragma unroll
-      for (int l = 1; l < BNH; ++l) {  // hidden layers BW -> BW
-        float n0 = 0.f, n1 = 0.f;
-        const float* w0 = sw + w_off[l] + (lane < BW ? lane : 0) * w_st[l];
-        const float* w1 = sw + w_off[l] + (lane + 32 < BW ? lane + 32 : 0) * w_st[l];
+      for (int l = 1; l < BNH; ++l) {  // hidden layers BW -> BW: K chunks [W (BW/8) | W | bias]
+        const LayerDesc& L = mp.layers[mp.brdf_first + l];
+        float w[2][BW / 8][8], bb[2][8];
+#pragma unroll
+        for (int u = 0; u < (BW > 32 ? 2 : 1); ++u) {
+#pragma unroll
+          for (int c = 0; c < BW / 8; ++c) load_row8(mp, L.b_off, BW, u ? j1 : j0, c, w[u][c]);
+          load_row8(mp, L.b_off, BW, u ? j1 : j0, 2 * BW / 8, bb[u]);
+        }
+        float acc[2] = {0.f, 0.f};
 #pragma unroll
         for (int q = 0; q < BW; ++q) {  // every lane takes part in the shuffles
-          const float hq = __shfl_sync(0xffffffffu, q < 32 ? h0 : h1, q & 31);
-          n0 = __fmaf_rn(hq, w0[q], n0);
-          if (BW > 32) n1 = __fmaf_rn(hq, w1[q], n1);
+          const float hq = __shfl_sync(0xffffffffu, q < 32 ? h[0] : h[1], q & 31);
+#pragma unroll
+          for (int u = 0; u < (BW > 32 ? 2 : 1); ++u) acc[u] = __fmaf_rn(hq, w[u][q / 8][q % 8], acc[u]);
         }
-        n0 += w0[BW];
-        n0 = lane < BW ? (n0 >= 0.f ? n0 : kLeaky * n0) : 0.f;
-        if (BW > 32) {
-          n1 += w1[BW];
-          n1 = lane + 32 < BW ? (n1 >= 0.f ? n1 : kLeaky * n1) : 0.f;
+#pragma unroll
+        for (int u = 0; u < (BW > 32 ? 2 : 1); ++u) {
+          const float v = acc[u] + bb[u][0];
+          h[u] = v >= 0.f ? v : kLeaky * v;
         }
-        h0 = n0;
-        h1 = n1;
       }
-      // output layer BW -> 3 (6 with albedo): partial products, warp sums
-      const float* wo_ = sw + w_off[BNH];
-      const int st = w_st[BNH], fo = mp.layers[mp.brdf_first + BNH].out;
+      if (lane >= BW) h[0] = 0.f;
+      // output layer BW -> 3 (6 with albedo), fp32 copy in the parameter block: warp sums
+      // (weights from the fp32 copy in global memory: a per-lane index into the
+      // constant bank would serialize the warp)
+      const LayerDesc& LO = mp.layers[mp.brdf_first + BNH];
+      const float* wout = mp.w32 + LO.w32_off;
       float y[6];
 #pragma unroll
       for (int o = 0; o < 6; ++o) {
         float p = 0.f;
-        if (o < fo) {
-          if (lane < BW) p = h0 * wo_[o * st + lane];
-          if (lane + 32 < BW) p = __fmaf_rn(h1, wo_[o * st + lane + 32], p);
-#pragma unroll
-          for (int d = 16; d > 0; d >>= 1) p += __shfl_xor_sync(0xffffffffu, p, d);
-          p += wo_[o * st + BW];
+        if (o < LO.out) {
+          p = lane < BW ? h[0] * __ldg(wout + o * (BW + 1) + lane) : 0.f;
+          if (BW > 32) p = __fmaf_rn(h[1], __ldg(wout + o * (BW + 1) + 32 + lane), p);
         }
-        y[o] = p;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) p += __shfl_xor_sync(0xffffffffu, p, d);
+        y[o] = p + mp.ob[o];
       }
-      if (lane == 0) {
-        const int32_t row = l_row[k];
+      if (lane == src) {
         const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + row) : (int64_t)row;
         // queued rows are above the horizon (below it the output is 0 either way)
         stg3(a.rgb, q, v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])));
         if (mp.albedo && a.albedo) stg3(a.albedo, q, v3(fmaxf(y[3], 0.f), fmaxf(y[4], 0.f), fmaxf(y[5], 0.f)));
       }
     }
-    __syncthreads();
-    if (tid == 0) n_list = 0u;
-    __syncthreads();
   }
 }
 
@@ -787,10 +786,12 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             const float2 d1 = make_float2(fc.tw_delta * kappa.x, fc.tw_delta * kappa.x);
             const float2 d2 = make_float2(fc.tw_delta * kappa.y, fc.tw_delta * kappa.y);
             const float2 d12 = make_float2(d1.x, d2.x);
-            const uint32_t near = near_mid2(ti[0], ti[1], d1) | near_mid2(ti[2], ti[3], d12) |
-                                  near_mid2(ti[4], ti[5], d2) | near_mid2(to[0], to[1], d1) |
-                                  near_mid2(to[2], to[3], d12) | near_mid2(to[4], to[5], d2);
-            const bool flag = valid && S.up && near != 0u;
+            const uint32_t nw1 = near_mid2(ti[2], ti[3], d12), nw4 = near_mid2(to[2], to[3], d12);
+            const uint32_t near_f0 = near_mid2(ti[0], ti[1], d1) | near_mid2(to[0], to[1], d1) |
+                                     ((nw1 | nw4) & 0xFFFFu);
+            const uint32_t near_f1 = near_mid2(ti[4], ti[5], d2) | near_mid2(to[4], to[5], d2) |
+                                     ((nw1 | nw4) >> 16);
+            const bool flag = valid && S.up && (near_f0 | near_f1) != 0u;
             // queue the tile's flagged rows (one shared atomic per warp)
             const uint32_t wmask = __ballot_sync(0xffffffffu, flag);
             if (wmask) {
@@ -799,10 +800,13 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
               if ((r & 31) == lead) wbase = atomicAdd(&q_cnt, __popc(wmask));
               wbase = __shfl_sync(0xffffffffu, wbase, lead);
               if (flag) {
-                uint4* e = fc.q.ent + 3 * ((size_t)blockIdx.x * fc.q.cap + wbase + __popc(wmask & lanemask_lt()));
+                uint4* e = fc.q.ent + kQueueWords * ((size_t)blockIdx.x * fc.q.cap + wbase + __popc(wmask & lanemask_lt()));
                 e[0] = make_uint4((uint32_t)(seg_base + q_in), x[0], x[1], x[2]);
                 e[1] = make_uint4(x[3], x[4], x[5], S.zp[0]);
-                e[2] = make_uint4(S.zp[1], S.zp[2], S.zp[3], 0u);
+                e[2] = make_uint4(S.zp[1], S.zp[2], S.zp[3], __float_as_uint(S.wi.x));
+                e[3] = make_uint4(__float_as_uint(S.wi.y), __float_as_uint(S.wi.z), __float_as_uint(wo.x),
+                                  __float_as_uint(wo.y));
+                e[4] = make_uint4(__float_as_uint(wo.z), (near_f0 ? 1u : 0u) | (near_f1 ? 2u : 0u), 0u, 0u);
               }
             }
             mma_issue<BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, refill);
@@ -987,7 +991,7 @@ cudaError_t queue_for(cudaStream_t s, size_t bytes, void** out) {
 // non-segment launches larger than this run as several (fast, resolve)
 // pairs, which bounds the queue at kChunkRows entries per stream
 constexpr int64_t kChunkRows = int64_t(1) << 24;
-constexpr unsigned kResolveSlices = 16;  // resolve blocks per fast-kernel CTA
+constexpr unsigned kResolveSlices = 2;  // resolve blocks per fast-kernel CTA
 
 template <class K>
 cudaError_t launch_pdl(K kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, const MatParams& mp,
@@ -1062,7 +1066,7 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
     // a CTA runs at most G * NS * ceil(ntiles / (grid * G * NS)) tiles
     const int64_t per = (int64_t)G * NS * ((ntiles + grid * G * NS - 1) / (grid * G * NS)) * kTile;
     void* qb = nullptr;
-    const size_t ent_bytes = (size_t)grid * per * 48;
+    const size_t ent_bytes = (size_t)grid * per * 16 * kQueueWords;
     cudaError_t e = queue_for(s, ent_bytes + (size_t)grid * 4, &qb);
     if (e != cudaSuccess) return e;
     fc.q.ent = reinterpret_cast<uint4*>(qb);
@@ -1073,10 +1077,8 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   if (e != cudaSuccess) return e;
   ++g_launches;
   if constexpr (kBrdf) {
-    const int rs = resolve_w_off(mp, BNH + 1) * 4;
-    if (max_dynamic_smem((const void*)resolve_kernel<BW, BNH>) < rs) return cudaErrorInvalidValue;
-    e = launch_pdl(resolve_kernel<BW, BNH>, dim3((unsigned)grid, kResolveSlices), dim3(kResolveThreads),
-                   (size_t)rs, s, mp, a, fc);
+    e = launch_pdl(resolve_kernel<BW, BNH>, dim3((unsigned)grid, kResolveSlices), dim3(kResolveThreads), 0, s,
+                   mp, a, fc);
     if (e != cudaSuccess) return e;
     ++g_launches;
   }

@@ -73,7 +73,7 @@ struct MatParams {
   // every network in the reference's packed access order [w_row, bias] per
   // neuron (`w32` + LayerDesc::w32_off), read by the warp-cooperative
   // re-evaluation of queries whose decoder inputs round differently.
-  float fw[12][9];
+  float2 fw2[6][9];  // frame layer, both frames paired: (W[j][k], W[j + 6][k]), k = 8: bias
   const float* w32;
 };
 
