@@ -429,6 +429,9 @@ struct SlotSt {
 // one 16-byte load each, all issued up front) and the output layer from the
 // fp32 copy in the parameter block.
 constexpr int kResolveThreads = 512;
+#ifndef NMQ_RESOLVE_FUSED
+#define NMQ_RESOLVE_FUSED 1  // resolve in the fast kernel's epilogue (1) or a follow-up kernel (0)
+#endif
 
 __device__ __forceinline__ void load_row8(const MatParams& mp, uint32_t off, int n_pad, int n, int c,
                                           float (&w)[8]) {
@@ -444,17 +447,12 @@ __device__ __forceinline__ void load_row8(const MatParams& mp, uint32_t off, int
 }
 
 template <int BW, int BNH>
-__global__ void __launch_bounds__(kResolveThreads, 2)
-resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
-               const __grid_constant__ FastConsts fc) {
-  const int lane = threadIdx.x & 31;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast kernel's queue and outputs
-  const uint32_t n = fc.q.cnt[blockIdx.x];
-  const uint4* ent = fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap;
+__device__ __forceinline__ void resolve_entries(const MatParams& mp, const QueryArgs& a, const uint4* ent,
+                                                uint32_t n, uint32_t first, uint32_t step, uint32_t tid) {
+  const int lane = tid & 31;
   const bool seg_out = a.out_idx != nullptr;
-  const uint32_t step = kResolveThreads * gridDim.y;
-  for (uint32_t b0 = blockIdx.y * kResolveThreads; b0 < n; b0 += step) {  // warp-uniform trip count
-    const uint32_t i = b0 + threadIdx.x;
+  for (uint32_t b0 = first; b0 < n; b0 += step) {  // warp-uniform trip count
+    const uint32_t i = b0 + tid;
     uint32_t zh[4] = {0u, 0u, 0u, 0u}, xe[6] = {0u, 0u, 0u, 0u, 0u, 0u};
     int32_t row = 0;
     bool mism = false;
@@ -559,6 +557,15 @@ resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Que
       }
     }
   }
+}
+
+template <int BW, int BNH>
+__global__ void __launch_bounds__(kResolveThreads, 2)
+resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
+               const __grid_constant__ FastConsts fc) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast kernel's queue and outputs
+  resolve_entries<BW, BNH>(mp, a, fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap, fc.q.cnt[blockIdx.x],
+                           blockIdx.y * kResolveThreads, kResolveThreads * gridDim.y, threadIdx.x);
 }
 
 template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG, bool DBG = false>
@@ -910,7 +917,16 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 0) tc::tmem_free<kTmemCols>(tb);
-  if (kBrdf && tid == 0) fc.q.cnt[blockIdx.x] = q_cnt;
+  if constexpr (kBrdf) {
+    if (NMQ_RESOLVE_FUSED) {
+      // every queued row's output is stored (the barrier above): the CTA
+      // resolves its own rows while other SMs are still on their tiles
+      resolve_entries<BW, BNH>(mp, a, fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap, q_cnt, 0,
+                               G * 128, tid);
+    } else if (tid == 0) {
+      fc.q.cnt[blockIdx.x] = q_cnt;
+    }
+  }
 }
 
 uint32_t fp16_bits(double v) {
@@ -920,8 +936,10 @@ uint32_t fp16_bits(double v) {
 
 #ifndef NMQ_TW_DELTA
 // error bound of the fast fp32 T.w per unit frame conditioning: measured
-// max |fast - exact| / kappa = 1.48e-7 over 6.2M C2 queries x 12 values
-// (tools/tw_calibrate.py, profiles/r02_tw_calibration.txt); 2x margin
+// max |fast - exact| / kappa = 1.48e-7 and 1.66e-7 over 6.2M C2 queries x 12
+// values each, two builds (tools/tw_calibrate.py, profiles/r02_tw_calibration*.txt);
+// ~2x margin.  Refining the MUFU rsqrt by a Newton step did not lower it
+// (the tensor-core frame layer's rounding dominates).
 #define NMQ_TW_DELTA 3e-7f
 #endif
 
@@ -1076,7 +1094,7 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
   cudaError_t e = launch_pdl(kern, dim3((unsigned)grid), dim3(G * 128), (size_t)smem, s, mp, a, fc);
   if (e != cudaSuccess) return e;
   ++g_launches;
-  if constexpr (kBrdf) {
+  if constexpr (kBrdf) if (!NMQ_RESOLVE_FUSED) {
     e = launch_pdl(resolve_kernel<BW, BNH>, dim3((unsigned)grid, kResolveSlices), dim3(kResolveThreads), 0, s,
                    mp, a, fc);
     if (e != cudaSuccess) return e;

@@ -332,7 +332,7 @@ def test_streamed_host_eval_matches_device_path():
     launches = _lib_launches()
     neural.eval_material(mat, pinned["uv"], pinned["lod"], pinned["wi"], pinned["wo"], pinned["u_rr"],
                          fp16=True, return_level=False, out=out2)
-    assert _lib_launches() - launches == 2  # the fused launch + its exact-rounding follow-up, no chunking
+    assert _lib_launches() - launches in (1, 2)  # one fused launch (+ the exact-rounding follow-up if not fused), no chunking
     assert np.array_equal(out2, f_dev.cpu().numpy())
 
 
