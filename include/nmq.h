@@ -166,6 +166,19 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
                   float* rgb_out, int32_t mode, void* workspace, size_t workspace_bytes,
                   void* stream);
+/* The renderer's per-vertex material groups for the sampler side
+ * (render.py:361-372, 391-409): sample + pdf, and the full query (eval +
+ * sample + pdf), each row with its own material mats[mat_id[i]].  Binned
+ * modes only (NM_MULTI_BINNED / NM_MULTI_BINNED_ASYNC; DIVERGENT returns
+ * NM_ERR_UNSUPPORTED).  Same workspace as nm_eval_multi. */
+int nm_sample_pdf_multi(const nm_material* const* mats, int32_t n_mats, int64_t n, const int32_t* mat_id,
+                        const float* uv, const float* lod, int32_t lod_stride, const float* u_rr,
+                        const float* wi, const float* u3, float* wo_out, float* pdf_out, float* params9_out,
+                        int32_t mode, void* workspace, size_t workspace_bytes, void* stream);
+int nm_query_multi(const nm_material* const* mats, int32_t n_mats, int64_t n, const int32_t* mat_id,
+                   const float* uv, const float* lod, int32_t lod_stride, const float* u_rr, const float* wi,
+                   const float* wo, const float* u3, float* rgb_out, float* ws_out, float* pdf_out,
+                   int32_t mode, void* workspace, size_t workspace_bytes, void* stream);
 
 /* --- misc -------------------------------------------------------------- */
 /* nm_eval with HOST buffers; blocking (rgb_out is complete on return),

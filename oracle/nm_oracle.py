@@ -849,3 +849,52 @@ def sampler_loss_and_grads(mat, z, wi, us):
     draw /= b
     grads, _ = backward(mat.sampler, cache, draw.astype(np.float32))
     return loss, grads
+
+
+# ---------------------------------------------------------------------------
+# chi-square goodness-of-fit harness for spherical samplers (chi2.py:13-72):
+# the reference's validation recipe for sample() against pdf()
+
+def _chi2_bin_masses(pdf_fn, res_theta, res_phi, z_lo, z_hi, quad):
+    """chi2.py:13-27: integral of the density over each (cos theta, phi) bin."""
+    dz = (z_hi - z_lo) / res_theta
+    dphi = 2.0 * np.pi / res_phi
+    zi = z_lo + dz * (np.arange(res_theta * quad) + 0.5) / quad
+    pj = dphi * (np.arange(res_phi * quad) + 0.5) / quad
+    zz, pp = np.meshgrid(zi, pj, indexing="ij")
+    rr = np.sqrt(np.maximum(0.0, 1.0 - zz ** 2))
+    dirs = np.stack([rr * np.cos(pp), rr * np.sin(pp), zz], axis=-1).reshape(-1, 3)
+    vals = np.asarray(pdf_fn(dirs), np.float64).reshape(res_theta * quad, res_phi * quad)
+    cell = (dz / quad) * (dphi / quad)
+    return vals.reshape(res_theta, quad, res_phi, quad).sum(axis=(1, 3)) * cell
+
+
+def _chi2_pearson(observed, expected, min_expected):
+    """chi2.py:30-43: pool small cells, scale, Pearson statistic, p-value."""
+    from scipy import stats
+    exp_flat, obs_flat = expected.ravel(), observed.ravel()
+    big = exp_flat >= min_expected
+    exp_p = np.append(exp_flat[big], exp_flat[~big].sum())
+    obs_p = np.append(obs_flat[big], obs_flat[~big].sum())
+    keep = exp_p > 1e-9
+    exp_p, obs_p = exp_p[keep], obs_p[keep]
+    exp_p = exp_p * (obs_p.sum() / exp_p.sum())
+    stat = float(np.sum((obs_p - exp_p) ** 2 / exp_p))
+    dof = exp_p.size - 1
+    return stat, dof, float(stats.chi2.sf(stat, dof))
+
+
+def chi_square_test(sample_fn, pdf_fn, n_samples, res_theta=16, res_phi=32, significance=0.01,
+                    sphere=True, quad=48, min_expected=5.0):
+    """chi2.py:46-72 -> (passed, p_value, statistic, dof)."""
+    z_lo, z_hi = (-1.0, 1.0) if sphere else (0.0, 1.0)
+    dirs = np.asarray(sample_fn(n_samples), np.float64)
+    z = np.clip(dirs[:, 2], z_lo, np.nextafter(z_hi, -np.inf))
+    phi = np.arctan2(dirs[:, 1], dirs[:, 0]) % (2.0 * np.pi)
+    iz = ((z - z_lo) / (z_hi - z_lo) * res_theta).astype(np.int64)
+    ip = np.minimum((phi / (2.0 * np.pi) * res_phi).astype(np.int64), res_phi - 1)
+    observed = np.zeros((res_theta, res_phi))
+    np.add.at(observed, (iz, ip), 1.0)
+    expected = _chi2_bin_masses(pdf_fn, res_theta, res_phi, z_lo, z_hi, quad) * n_samples
+    stat, dof, p = _chi2_pearson(observed, expected, min_expected)
+    return p > significance, p, stat, dof

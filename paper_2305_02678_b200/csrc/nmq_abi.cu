@@ -974,43 +974,61 @@ size_t nm_multi_workspace_bytes(int64_t n, int32_t n_mats) {
   return div > bin ? div : bin;
 }
 
+static int multi_prologue(const nm_material* const* mats, int32_t n_mats, int64_t n, bool need_brdf,
+                          bool need_sampler, void* workspace, size_t workspace_bytes,
+                          std::vector<const MatParams*>& mps) {
+  if (!mats || n_mats <= 0) return fail(NM_ERR_INVALID, "no materials");
+  if (n_mats > 32) return fail(NM_ERR_UNSUPPORTED, "at most 32 materials per call");
+  if (n >= (int64_t)1 << 31) return fail(NM_ERR_UNSUPPORTED, "batch too large for one call");
+  if (!workspace || workspace_bytes < nm_multi_workspace_bytes(n, n_mats))
+    return fail(NM_ERR_INVALID, "workspace too small (see nm_multi_workspace_bytes)");
+  const int dev = mats[0]->device;
+  mps.resize(n_mats);
+  for (int k = 0; k < n_mats; ++k) {
+    if (!mats[k]) return fail(NM_ERR_INVALID, "null material");
+    if (mats[k]->device != dev) return fail(NM_ERR_INVALID, "materials on different devices");
+    if (need_brdf && !mats[k]->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+    if (need_sampler && !mats[k]->mp.has_sampler) return fail(NM_ERR_INVALID, "material has no sampler decoder");
+    mps[k] = &mats[k]->mp;
+  }
+  return NM_OK;
+}
+
+static int multi_binned_call(const std::vector<const MatParams*>& mps, int mode, const QueryArgs& a,
+                             const int32_t* mat_id, int32_t multi_mode, void* workspace, void* stream,
+                             int dev, const char* what) {
+  DeviceGuard guard(dev);
+  std::vector<int32_t> counts(mps.size());
+  int32_t bad = 0;
+  const cudaError_t e = multi_binned(mps.data(), (int32_t)mps.size(), mode, a, mat_id, workspace, counts.data(),
+                                     &bad, multi_mode == NM_MULTI_BINNED, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue && bad) return fail(NM_ERR_INVALID, "mat_id out of range");
+  return finish(nullptr, e, what);
+}
+
 int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   const int32_t* mat_id, const float* uv, const float* lod, int32_t lod_stride,
                   const float* u_rr, const float* wi, const float* wo, float* rgb_out,
                   int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
-  if (!mats || n_mats <= 0) return fail(NM_ERR_INVALID, "no materials");
-  if (n_mats > 32) return fail(NM_ERR_UNSUPPORTED, "at most 32 materials per call");
   NM_CHECK_N(n);
   if (n == 0) return NM_OK;
-  if (n >= (int64_t)1 << 31) return fail(NM_ERR_UNSUPPORTED, "batch too large for one call");
   if (!mat_id || !uv || !lod || !u_rr || !wi || !wo || !rgb_out)
     return fail(NM_ERR_INVALID, "null input");
-  if (!workspace || workspace_bytes < nm_multi_workspace_bytes(n, n_mats))
-    return fail(NM_ERR_INVALID, "workspace too small (see nm_multi_workspace_bytes)");
-  const int dev = mats[0]->device;
-  std::vector<const MatParams*> mps(n_mats);
-  for (int k = 0; k < n_mats; ++k) {
-    if (!mats[k]) return fail(NM_ERR_INVALID, "null material");
-    if (mats[k]->device != dev) return fail(NM_ERR_INVALID, "materials on different devices");
-    if (!mats[k]->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
-    if (mats[k]->mp.precise) return fail(NM_ERR_UNSUPPORTED, "multi-material eval is fp16-path only");
-    mps[k] = &mats[k]->mp;
-  }
+  std::vector<const MatParams*> mps;
+  int rc = multi_prologue(mats, n_mats, n, true, false, workspace, workspace_bytes, mps);
+  if (rc != NM_OK) return rc;
   QueryArgs a{};
   a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
   a.wi = wi; a.wo = wo; a.rgb = rgb_out;
+  const int dev = mats[0]->device;
+  if (mode == NM_MULTI_BINNED || mode == NM_MULTI_BINNED_ASYNC)
+    return multi_binned_call(mps, kModeEval, a, mat_id, mode, workspace, stream, dev, "nm_eval_multi(binned)");
+  if (mode != NM_MULTI_DIVERGENT) return fail(NM_ERR_INVALID, "unknown multi-material mode");
+  for (auto* m : mps)
+    if (m->precise) return fail(NM_ERR_UNSUPPORTED, "divergent multi-material eval is fp16-path only");
   DeviceGuard guard(dev);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  if (mode == NM_MULTI_BINNED || mode == NM_MULTI_BINNED_ASYNC) {
-    std::vector<int32_t> counts(n_mats);
-    int32_t bad = 0;
-    e = eval_binned(mps.data(), n_mats, a, mat_id, workspace, counts.data(), &bad,
-                    mode == NM_MULTI_BINNED, s);
-    if (e == cudaErrorInvalidValue && bad) return fail(NM_ERR_INVALID, "mat_id out of range");
-    return finish(nullptr, e, "nm_eval_multi(binned)");
-  }
-  if (mode != NM_MULTI_DIVERGENT) return fail(NM_ERR_INVALID, "unknown multi-material mode");
   std::vector<MatParams> host(n_mats);
   for (int k = 0; k < n_mats; ++k) host[k] = *mps[k];
   MatParams* dev_mps = reinterpret_cast<MatParams*>(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
@@ -1020,6 +1038,46 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "upload material table");
   return finish(nullptr, launch_eval_divergent(mps.data(), dev_mps, n_mats, mat_id, a, s),
                 "nm_eval_multi(divergent)");
+}
+
+int nm_sample_pdf_multi(const nm_material* const* mats, int32_t n_mats, int64_t n, const int32_t* mat_id,
+                        const float* uv, const float* lod, int32_t lod_stride, const float* u_rr,
+                        const float* wi, const float* u3, float* wo_out, float* pdf_out, float* params9_out,
+                        int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!mat_id || !uv || !lod || !u_rr || !wi || !u3 || !wo_out || !pdf_out)
+    return fail(NM_ERR_INVALID, "null input");
+  if (mode != NM_MULTI_BINNED && mode != NM_MULTI_BINNED_ASYNC)
+    return fail(NM_ERR_UNSUPPORTED, "sample+pdf over several materials runs binned");
+  std::vector<const MatParams*> mps;
+  int rc = multi_prologue(mats, n_mats, n, false, true, workspace, workspace_bytes, mps);
+  if (rc != NM_OK) return rc;
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.u3 = u3; a.ws = wo_out; a.pdf = pdf_out; a.params9 = params9_out;
+  return multi_binned_call(mps, kModeSamplePdf, a, mat_id, mode, workspace, stream, mats[0]->device,
+                           "nm_sample_pdf_multi");
+}
+
+int nm_query_multi(const nm_material* const* mats, int32_t n_mats, int64_t n, const int32_t* mat_id,
+                   const float* uv, const float* lod, int32_t lod_stride, const float* u_rr, const float* wi,
+                   const float* wo, const float* u3, float* rgb_out, float* ws_out, float* pdf_out,
+                   int32_t mode, void* workspace, size_t workspace_bytes, void* stream) {
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!mat_id || !uv || !lod || !u_rr || !wi || !wo || !u3 || !rgb_out || !ws_out || !pdf_out)
+    return fail(NM_ERR_INVALID, "null input");
+  if (mode != NM_MULTI_BINNED && mode != NM_MULTI_BINNED_ASYNC)
+    return fail(NM_ERR_UNSUPPORTED, "full queries over several materials run binned");
+  std::vector<const MatParams*> mps;
+  int rc = multi_prologue(mats, n_mats, n, true, true, workspace, workspace_bytes, mps);
+  if (rc != NM_OK) return rc;
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.wo = wo; a.u3 = u3; a.rgb = rgb_out; a.ws = ws_out; a.pdf = pdf_out;
+  return multi_binned_call(mps, kModeQuery, a, mat_id, mode, workspace, stream, mats[0]->device,
+                           "nm_query_multi");
 }
 
 }  // extern "C"

@@ -1041,7 +1041,6 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const bool seg = a.seg || a.out_idx;
-  if (seg && MODE != kModeEval) return cudaErrorNotSupported;  // binned segments are eval-only
   constexpr bool kBrdf = Need<MODE>::brdf;
   if (kBrdf && !seg && a.n > kChunkRows) {
     for (int64_t c0 = 0; c0 < a.n; c0 += kChunkRows) {
@@ -1065,7 +1064,7 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
     }
     return cudaSuccess;
   }
-  auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, (MODE == kModeEval)>
+  auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, true>
                   : (a.dbg && MODE == kModeEval) ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false, true>
                                                  : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
   const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>) +

@@ -131,9 +131,9 @@ cudaError_t launch_pdf(int64_t n, const float* p9, const float* wi, const float*
                        cudaStream_t s);
 // multi-material (nmq_multi.cu / nmq_kernels.cu)
 size_t multi_workspace_bytes(int64_t n, int32_t n_mats);
-cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const QueryArgs& a,
-                        const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
-                        bool checked, cudaStream_t s);
+cudaError_t multi_binned(const MatParams* const* mps, int32_t n_mats, int mode, const QueryArgs& a,
+                         const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
+                         bool checked, cudaStream_t s);
 cudaError_t launch_eval_divergent(const MatParams* const* mps_host, const MatParams* mps_dev,
                                   int32_t n_mats, const int32_t* mat_id, const QueryArgs& a,
                                   cudaStream_t s);

@@ -102,6 +102,7 @@ struct ScatterSmem {
   float urr[kScatterRows];
   float wi[3 * kScatterRows];
   float wo[3 * kScatterRows];
+  float u3[3 * kScatterRows];
   int32_t row[kScatterRows];
 };
 __global__ void __launch_bounds__(256) bin_scatter_kernel(
@@ -109,8 +110,9 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     int32_t* __restrict__ seg, int32_t* __restrict__ cursor,
     int32_t* __restrict__ order, const float* __restrict__ uv, const float* __restrict__ lod,
     int32_t lod_stride, const float* __restrict__ urr, const float* __restrict__ wi,
-    const float* __restrict__ wo, float* __restrict__ p_uv, float* __restrict__ p_lod,
-    float* __restrict__ p_urr, float* __restrict__ p_wi, float* __restrict__ p_wo) {
+    const float* __restrict__ wo, const float* __restrict__ u3, float* __restrict__ p_uv,
+    float* __restrict__ p_lod, float* __restrict__ p_urr, float* __restrict__ p_wi, float* __restrict__ p_wo,
+    float* __restrict__ p_u3) {
   extern __shared__ __align__(16) uint8_t sm_raw[];
   ScatterSmem& S = *reinterpret_cast<ScatterSmem*>(sm_raw);
   __shared__ int32_t cnt[kMaxMats], loc[kMaxMats + 1], base[kMaxMats], off[kMaxMats];
@@ -177,7 +179,8 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       S.wi[3 * p + j] = __ldg(wi + 3 * i + j);
-      S.wo[3 * p + j] = __ldg(wo + 3 * i + j);
+      if (wo) S.wo[3 * p + j] = __ldg(wo + 3 * i + j);
+      if (u3) S.u3[3 * p + j] = __ldg(u3 + 3 * i + j);
     }
     S.row[p] = (int32_t)i;
   }
@@ -200,7 +203,8 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     const int p = f / 3, j = f - 3 * p;
     const int64_t sl = slot_of(p);
     p_wi[3 * sl + j] = S.wi[f];
-    p_wo[3 * sl + j] = S.wo[f];
+    if (wo) p_wo[3 * sl + j] = S.wo[f];
+    if (u3) p_u3[3 * sl + j] = S.u3[f];
   }
 }
 
@@ -264,16 +268,16 @@ int grid256(int64_t n) {
 }  // namespace
 
 size_t multi_workspace_bytes(int64_t n, int32_t n_mats) {
-  // counts, offsets(+1), cursor, bad flag | order | uv lod urr wi wo
+  // counts, offsets(+1), cursor, bad flag | order | uv lod urr wi wo u3
   // (segments padded to 4 rows: n + 4 n_mats rows)
   const size_t rows = (size_t)n + 4 * (size_t)n_mats;
-  // + 256-byte alignment of each of the 8 regions
-  return 4096 + (size_t)(5 * n_mats + 3) * 4 + rows * (4 + 40);
+  // + 256-byte alignment of each of the 9 regions
+  return 4096 + (size_t)(5 * n_mats + 3) * 4 + rows * (4 + 40 + 12);
 }
 
 struct MultiWs {
   int32_t *counts, *offsets, *cursor, *bad, *seg, *order;
-  float *uv, *lod, *urr, *wi, *wo;
+  float *uv, *lod, *urr, *wi, *wo, *u3;
 };
 
 static MultiWs carve(void* ws, int64_t n_rows, int32_t n_mats) {
@@ -291,19 +295,41 @@ static MultiWs carve(void* ws, int64_t n_rows, int32_t n_mats) {
   p = align(p); w.lod = (float*)p; p += n * 4;
   p = align(p); w.urr = (float*)p; p += n * 4;
   p = align(p); w.wi = (float*)p; p += n * 12;
-  p = align(p); w.wo = (float*)p;
+  p = align(p); w.wo = (float*)p; p += n * 12;
+  p = align(p); w.u3 = (float*)p;
   return w;
 }
 
-// BINNED eval.  checked: `host_counts` / `bad` come back to the host (one
+// Per-segment launch arguments: the permuted inputs at row offset `off`,
+// outputs straight to query order through `order` (mode-dependent outputs).
+static QueryArgs segment_args(const QueryArgs& a, const MultiWs& w, int64_t off) {
+  QueryArgs sa{};
+  sa.uv = w.uv + 2 * off;
+  sa.lod = w.lod + off;
+  sa.lod_stride = 1;
+  sa.u_rr = w.urr + off;
+  sa.wi = w.wi + 3 * off;
+  sa.wo = a.wo ? w.wo + 3 * off : nullptr;
+  sa.u3 = a.u3 ? w.u3 + 3 * off : nullptr;
+  sa.rgb = a.rgb;
+  sa.albedo = a.albedo;
+  sa.ws = a.ws;
+  sa.pdf = a.pdf;
+  sa.params9 = a.params9;
+  sa.level = a.level;
+  sa.out_idx = w.order + off;
+  return sa;
+}
+
+// BINNED eval / sample+pdf / query (mode).  checked: `host_counts` / `bad` come back to the host (one
 // D2H sync per call) so out-of-range ids are reported, empty segments are
 // skipped and the others run concurrently on SM shares proportional to
 // their sizes.  !checked: no host round trip — every segment launch reads its
 // {base, count} from the device (QueryArgs::seg); ids out of range are
 // dropped (their rows are left untouched).
-cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const QueryArgs& a,
-                        const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
-                        bool checked, cudaStream_t s) {
+cudaError_t multi_binned(const MatParams* const* mps, int32_t n_mats, int mode, const QueryArgs& a,
+                         const int32_t* mat_id, void* ws, int32_t* host_counts, int32_t* bad,
+                         bool checked, cudaStream_t s) {
   if (n_mats > kMaxMats) return cudaErrorInvalidValue;
   MultiWs w = carve(ws, a.n, n_mats);
   cudaError_t e;
@@ -314,9 +340,8 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
   }
   if (max_dynamic_smem((const void*)bin_scatter_kernel) < (int)sizeof(ScatterSmem)) return cudaErrorInvalidValue;
   bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sizeof(ScatterSmem), s>>>(
-      a.n, n_mats, mat_id, w.counts, w.seg, w.cursor, w.order, a.uv, a.lod,
-                                                  a.lod_stride, a.u_rr, a.wi, a.wo, w.uv, w.lod,
-                                                  w.urr, w.wi, w.wo);
+      a.n, n_mats, mat_id, w.counts, w.seg, w.cursor, w.order, a.uv, a.lod, a.lod_stride, a.u_rr, a.wi,
+      a.wo, a.u3, w.uv, w.lod, w.urr, w.wi, w.wo, w.u3);
   g_launches += 2;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (!checked) {
@@ -332,19 +357,11 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
     std::lock_guard<std::mutex> lock(sides().mu);
     fork_streams(s, n_mats);
     for (int m = 0; m < n_mats; ++m) {
-      QueryArgs sa{};
+      QueryArgs sa = segment_args(a, w, 0);
       sa.n = a.n;  // capacity bound; the segment's rows come from w.seg
       sa.seg = w.seg + 2 * m;
-      sa.uv = w.uv;
-      sa.lod = w.lod;
-      sa.lod_stride = 1;
-      sa.u_rr = w.urr;
-      sa.wi = w.wi;
-      sa.wo = w.wo;
-      sa.rgb = a.rgb;
-      sa.out_idx = w.order;
       sa.max_ctas = per;
-      if ((e = launch_fused(*mps[m], kModeEval, sa, side_stream(m))) != cudaSuccess) return e;
+      if ((e = launch_fused(*mps[m], mode, sa, side_stream(m))) != cudaSuccess) return e;
     }
     return join_streams(s, n_mats);
   }
@@ -366,19 +383,11 @@ cudaError_t eval_binned(const MatParams* const* mps, int32_t n_mats, const Query
   for (int m = 0; m < n_mats; ++m) {
     const int64_t c = host_counts[m];
     if (c > 0) {
-      QueryArgs sa{};
+      QueryArgs sa = segment_args(a, w, off);  // results go straight back to query order
       sa.n = c;
-      sa.uv = w.uv + 2 * off;
-      sa.lod = w.lod + off;
-      sa.lod_stride = 1;
-      sa.u_rr = w.urr + off;
-      sa.wi = w.wi + 3 * off;
-      sa.wo = w.wo + 3 * off;
-      sa.rgb = a.rgb;             // results go straight back to query order
-      sa.out_idx = w.order + off;
       const int64_t share = (int64_t)nsm * c / total;
       sa.max_ctas = share >= 1 ? (int32_t)share : 1;
-      if ((e = launch_fused(*mps[m], kModeEval, sa, side_stream(m))) != cudaSuccess) return e;
+      if ((e = launch_fused(*mps[m], mode, sa, side_stream(m))) != cudaSuccess) return e;
     }
     off += (c + 3) & ~3;
   }

@@ -4,7 +4,14 @@
 ``nm_fetch``: Russian-roulette level choice (latent.py:76-82) and
 wrap-addressed bilinear taps (latent.py:56-74) computed exactly like the
 reference (float64 texel coordinates), so chosen levels and tap indices are
-bit-identical; the blend is fp32 over the stored texels.
+bit-identical, and the blend is float64 like the reference's, so z is
+bit-identical too.
+
+Like the reference, a pyramid's ``levels`` may be edited in place between
+fetches (the baking loop's Adam step, training.py:305-356): the device copy
+is refreshed whenever the levels' content changed (a full-array checksum per
+fetch).  The fp16 render copy built by ``NeuralMaterial.half()`` is cached
+until ``invalidate_half()``, exactly like the reference's (neural.py:144-161).
 
 Texels are uploaded as fp16 when every value is fp16-representable (the
 render copy ``half_copy()``, which is what the fp16 query path reads) and as
@@ -41,6 +48,8 @@ class LatentPyramid:
                 raise ValueError("levels must be (H, W, C) with a shared C")
         self.levels = [np.ascontiguousarray(l, dtype=np.float32) for l in levels]
         self._dev = {}
+        self._fp = {}
+        self._frozen = False  # True for the cached render copy (NeuralMaterial.half())
 
     @classmethod
     def zeros(cls, width, height, channels=LATENT_CHANNELS):
@@ -63,10 +72,25 @@ class LatentPyramid:
         return self.levels[0].shape[0]
 
     def invalidate(self):
-        """Drop device copies (call after editing `levels` in place)."""
+        """Drop device copies (they are also refreshed automatically when the
+        levels' content changes)."""
         for h in self._dev.values():
             h.close()
         self._dev = {}
+        self._fp = {}
+
+    def fingerprint(self):
+        """Content checksum of every level (float32 bits: wrapping sum and xor
+        of 64-bit words, plus the shapes) — detects in-place edits."""
+        out = []
+        for l in self.levels:
+            a = np.ascontiguousarray(l, dtype=np.float32)
+            flat = a.reshape(-1)
+            if flat.size % 2:
+                flat = np.concatenate([flat, np.zeros(1, np.float32)])
+            u = flat.view(np.uint64)
+            out.append((a.shape, int(np.add.reduce(u, dtype=np.uint64)), int(np.bitwise_xor.reduce(u))))
+        return tuple(out)
 
     def half_copy(self):
         """fp16 render copy: clip to +-65504, round to nearest even (latent.py:124-126)."""
@@ -83,12 +107,18 @@ class LatentPyramid:
     def device_material(self, device=None):
         dev = _io.cuda_device(device)
         h = self._dev.get(dev.index)
+        if h is not None and not self._frozen:
+            if self._fp.get(dev.index) != self.fingerprint():  # levels edited in place
+                h.close()
+                h = None
         if h is None:
             if [l.shape[:2] for l in self.levels] != level_shapes(self.width, self.height):
                 raise ValueError("levels do not follow the max(1, n//2) halving chain")
             blob, fp32 = self.texel_blob()
             h = DeviceMaterial(dev, self.width, self.height, self.n_levels, blob, latent_fp32=fp32)
             self._dev[dev.index] = h
+            if not self._frozen:
+                self._fp[dev.index] = self.fingerprint()
         return h
 
     def fetch(self, uv, level, u_rr, return_taps=False):

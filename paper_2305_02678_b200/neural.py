@@ -100,14 +100,26 @@ class NeuralMaterial:
     def invalidate_half(self):
         self._half = None
         for h in self._dev.values():
-            h.close()
+            if hasattr(h, "close"):
+                h.close()
         self._dev = {}
+
+    def _master_fingerprint(self):
+        """Checksum of the fp32 master weights and pyramid (in-place edits)."""
+        parts = []
+        for net in (self.frame_layer, self.brdf_decoder, self.sampler_decoder):
+            if net is not None:
+                for l in net.layers:
+                    parts.append((np.asarray(l.w, np.float32).tobytes(), np.asarray(l.b, np.float32).tobytes()))
+        lat = self.latent.fingerprint() if isinstance(self.latent, LatentPyramid) else None
+        return hash(tuple(parts)), lat
 
     def half(self):
         if self._half is None:
             latent = None
-            if self.latent is not None:
+            if isinstance(self.latent, LatentPyramid):
                 latent = LatentPyramid([l.astype(np.float32) for l in self.latent.half_copy()])
+                latent._frozen = True  # the reference caches its render copy too (neural.py:147-161)
             self._half = {
                 "frame": mlp.quantize(self.frame_layer) if self.frame_layer is not None else None,
                 "brdf": mlp.quantize(self.brdf_decoder),
@@ -130,8 +142,14 @@ class NeuralMaterial:
         hi/lo pairs) + the fp32 master pyramid (the reference's fp16=False path)."""
         dev = _io.cuda_device(device)
         if precise:
+            # the reference's fp16=False path reads the fp32 master weights and
+            # pyramid live (neural.py:288-293): rebuild when either changed
             key = (dev.index, "fp32")
             h = self._dev.get(key)
+            fp = self._master_fingerprint()
+            if h is not None and self._dev.get((dev.index, "fp32-fp")) != fp:
+                h.close()
+                h = None
             if h is None:
                 if isinstance(self.latent, DeviceLatent):
                     raise NotImplementedError(
@@ -148,6 +166,7 @@ class NeuralMaterial:
                                    sampler_isotropic=self.cfg.sampler_isotropic,
                                    masters=(self.frame_layer, self.brdf_decoder, self.sampler_decoder))
                 self._dev[key] = h
+                self._dev[(dev.index, "fp32-fp")] = fp
             return h
         h = self._dev.get(dev.index)
         if h is None:
@@ -395,6 +414,72 @@ def eval_material_multi(mats, mat_id, uv, level, wi, wo, u_rr, mode="binned", fp
             lod_t.data_ptr(), lod_stride, urr_t.data_ptr(), wi_t.data_ptr(), wo_t.data_ptr(),
             f.data_ptr(), MULTI_MODES[mode], ws.data_ptr(), ws_bytes, _io.stream_ptr(dev))
     return _io.out(f, np_mode)
+
+
+def _multi_inputs(mats, mat_id, uv, level, u_rr, dirs):
+    mats = list(mats)
+    if not mats:
+        raise ValueError("no materials")
+    np_mode = _io.is_numpy_like(uv)
+    handles = [m.device_material(None if np_mode else uv.device) for m in mats]
+    dev = handles[0].device
+    if any(h.device != dev for h in handles):
+        raise ValueError("materials must live on the same device")
+    uv_t = _io.as_rows(uv, 2, dev, "uv")
+    n = uv_t.shape[0]
+    lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
+    urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+    d = {k: _io.as_rows(v, 3, dev, k) for k, v in dirs.items()}
+    if isinstance(mat_id, torch.Tensor):
+        ids = mat_id.to(device=dev, dtype=torch.int32).reshape(-1).contiguous()
+    else:
+        ids = torch.from_numpy(np.ascontiguousarray(np.asarray(mat_id).reshape(-1), np.int32)).to(dev)
+    if ids.numel() != n or any(t.shape[0] != n for t in d.values()):
+        raise ValueError("mat_id, uv and the directions must share the batch size")
+    lib = _lib.load()
+    ws_bytes = int(lib.nm_multi_workspace_bytes(n, len(handles)))
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    ptrs = (ctypes.c_void_p * len(handles))(*[h.ptr for h in handles])
+    return np_mode, dev, n, ptrs, len(handles), ids, uv_t, lod_t, lod_stride, urr_t, d, ws, ws_bytes
+
+
+def sample_pdf_multi(mats, mat_id, uv, level, u_rr, wi, u, mode="binned", fp16=True, return_params=False):
+    """sample_pdf with a material per row (the renderer's per-vertex material
+    groups for the sampler side, render.py:361-372, 391-409): binned by
+    material id on the device; returns (ws, pdf[, params])."""
+    _require_fp16(fp16)
+    if mode not in MULTI_MODES:
+        raise ValueError(f"mode must be one of {sorted(MULTI_MODES)}")
+    np_mode, dev, n, ptrs, k, ids, uv_t, lod_t, stride, urr_t, d, wsp, ws_bytes = _multi_inputs(
+        mats, mat_id, uv, level, u_rr, {"wi": wi, "u": u})
+    ws = _io.empty(n, 3, dev)
+    p = _io.empty(n, 1, dev)
+    p9 = _io.empty(n, 9, dev) if return_params else None
+    lib = _lib.load()
+    _launch(lib.nm_sample_pdf_multi, ptrs, k, n, ids.data_ptr(), uv_t.data_ptr(), lod_t.data_ptr(), stride,
+            urr_t.data_ptr(), d["wi"].data_ptr(), d["u"].data_ptr(), ws.data_ptr(), p.data_ptr(), _io.ptr(p9),
+            MULTI_MODES[mode], wsp.data_ptr(), ws_bytes, _io.stream_ptr(dev))
+    res = (_io.out(ws, np_mode), _io.out(p, np_mode))
+    if return_params:
+        res = res + (ProxyParams.from_block(p9, np_mode),)
+    return res
+
+
+def query_multi(mats, mat_id, uv, level, u_rr, wi, wo, u, mode="binned", fp16=True):
+    """query() with a material per row: (f, ws, pdf), binned on the device."""
+    _require_fp16(fp16)
+    if mode not in MULTI_MODES:
+        raise ValueError(f"mode must be one of {sorted(MULTI_MODES)}")
+    np_mode, dev, n, ptrs, k, ids, uv_t, lod_t, stride, urr_t, d, wsp, ws_bytes = _multi_inputs(
+        mats, mat_id, uv, level, u_rr, {"wi": wi, "wo": wo, "u": u})
+    f = _io.empty(n, 3, dev)
+    ws = _io.empty(n, 3, dev)
+    p = _io.empty(n, 1, dev)
+    lib = _lib.load()
+    _launch(lib.nm_query_multi, ptrs, k, n, ids.data_ptr(), uv_t.data_ptr(), lod_t.data_ptr(), stride,
+            urr_t.data_ptr(), d["wi"].data_ptr(), d["wo"].data_ptr(), d["u"].data_ptr(), f.data_ptr(),
+            ws.data_ptr(), p.data_ptr(), MULTI_MODES[mode], wsp.data_ptr(), ws_bytes, _io.stream_ptr(dev))
+    return _io.out(f, np_mode), _io.out(ws, np_mode), _io.out(p, np_mode)
 
 
 # --- archive (NMATARC1, neural.py:368-419) -------------------------------------

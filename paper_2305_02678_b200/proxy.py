@@ -96,6 +96,26 @@ class ProxyParams:
         a = self.alpha
         return a[:, 0] * a[:, 1] * self.s
 
+    def matrix(self):
+        """The 3x3 slope warp M per batch entry (proxy.py:64-74)."""
+        a, r, s, ms = self.alpha, self.rho, self.s, self.mu_s
+        z = np.zeros if self._np else (lambda n: torch.zeros(n, device=self.data.device))
+        o = np.ones if self._np else (lambda n: torch.ones(n, device=self.data.device))
+        n = len(self)
+        rows = [[a[:, 0], z(n), -ms[:, 0]], [a[:, 1] * r, a[:, 1] * s, -ms[:, 1]], [z(n), z(n), o(n)]]
+        if self._np:
+            return np.stack([np.stack(rw, -1) for rw in rows], 1)
+        return torch.stack([torch.stack(rw, -1) for rw in rows], 1)
+
+    def diffuse_normal(self):
+        """Axis of the tilted cosine lobe, normalize(-mu_d.x, -mu_d.y, 1) (proxy.py:80-84)."""
+        md = self.mu_d
+        if self._np:
+            v = np.stack([-md[:, 0], -md[:, 1], np.ones(len(self))], -1)
+            return v / np.linalg.norm(v, axis=-1, keepdims=True)
+        v = torch.stack([-md[:, 0], -md[:, 1], torch.ones(len(self), device=md.device)], -1)
+        return v / v.norm(dim=-1, keepdim=True)
+
     def take(self, idx):
         if isinstance(idx, np.ndarray):
             idx = torch.from_numpy(idx).to(self.data.device)
@@ -141,3 +161,22 @@ def pdf(params, wi, wo):
     _lib.check(lib.nm_pdf(n, params.data.data_ptr(), wi_t.data_ptr(), wo_t.data_ptr(),
                           p.data_ptr(), _io.stream_ptr(dev)), "nm_pdf")
     return _io.out(p, np_mode)
+
+
+def normalize_check(params, wi, n_samples, rng, chunk=2_000_000):
+    """MC estimate of the full-sphere integral of pdf by uniform-sphere
+    sampling (proxy.py:183-196); the pdf runs on the GPU (nm_pdf)."""
+    if len(params) != 1:
+        raise ValueError("normalize_check expects a single parameter set")
+    total, done = 0.0, 0
+    while done < n_samples:
+        m = min(chunk, n_samples - done)
+        u = rng.random((m, 2))
+        z = 1.0 - 2.0 * u[:, 0]
+        r = np.sqrt(np.maximum(0.0, 1.0 - z * z))
+        phi = 2.0 * np.pi * u[:, 1]
+        d = np.stack([r * np.cos(phi), r * np.sin(phi), z], -1)  # geom.sample_uniform_sphere
+        rep = params.take(np.zeros(m, dtype=np.int64))
+        total += float(np.sum(pdf(rep, np.broadcast_to(np.asarray(wi, np.float64), (m, 3)), d)))
+        done += m
+    return total * 4.0 * np.pi / n_samples

@@ -144,3 +144,36 @@ def test_binned_async_from_concurrent_host_threads():
     [x.join() for x in th]
     for k in range(2):
         np.testing.assert_array_equal(got[k], want[k])
+
+
+@pytest.mark.parametrize("mode", ["binned", "binned_async"])
+def test_multi_material_sample_pdf_and_query(mode):
+    """The renderer's per-vertex groups on the sampler side (render.py:361-409):
+    sampler + sample + pdf, and the full query, each row with its own material."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from test_gpu_parity import check_dirs, check_rel
+
+    rng = np.random.default_rng(43)
+    mats, omats = _materials(rng)
+    n = 9001
+    uv, lod, urr, wi, wo = _queries(rng, n)
+    u3 = rng.random((n, 3)).astype(np.float32)
+    ids = rng.integers(0, len(mats), n).astype(np.int32)
+    ws, pdf, p = neural.sample_pdf_multi(mats, ids, uv, lod, urr, wi, u3, mode=mode, return_params=True)
+    f2, ws2, pdf2 = neural.query_multi(mats, ids, uv, lod, urr, wi, wo, u3, mode=mode)
+    f_ref = np.zeros((n, 3))
+    ws_ref = np.zeros((n, 3))
+    p_ref = np.zeros((n, 9))
+    for k, om in enumerate(omats):
+        m = ids == k
+        fr, wsr, _, pr, _ = O.full_query(om, uv[m], lod[m], urr[m], wi[m], wo[m], u3[m])
+        f_ref[m], ws_ref[m], p_ref[m] = fr, wsr, pr.as_array()
+    check_rel(p.as_array(), p_ref, what=f"{mode} params")
+    check_rel(f2, f_ref, what=f"{mode} query rgb")
+    P = O.Proxy(p_ref[:, 0], p_ref[:, 1], p_ref[:, 2:4], p_ref[:, 4:6], p_ref[:, 6], p_ref[:, 7:9])
+    check_dirs(ws, ws_ref, u3, P, wi)
+    check_dirs(ws2, ws_ref, u3, P, wi)
+    assert np.array_equal(ws, ws2) and np.array_equal(pdf, pdf2)  # the same kernels on the same rows
+    with pytest.raises(NotImplementedError):
+        neural.sample_pdf_multi(mats, ids, uv, lod, urr, wi, u3, mode="divergent")

@@ -205,3 +205,38 @@ def test_c4_multi_material_table1(mode):
         check_rel(fh[sel], f_ref, what=f"C4 {mode} material {k} {C4_RESOLUTIONS[k]}")
     del mats, handles
     torch.cuda.empty_cache()
+
+
+def test_c4_full_query_binned_table1():
+    """C4 full query (eval + sample + pdf) over the five Table-1 materials,
+    binned by material id on the device (nm_query_multi)."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural, synth
+    from paper_2305_02678_b200.synth import C4_RESOLUTIONS
+    dev = torch.device("cuda", 0)
+    mats = [synth.material("2x32", w, hh, seed=10 + k, device=dev) for k, (w, hh) in enumerate(C4_RESOLUTIONS)]
+    handles = [m.device_material(dev) for m in mats]
+    n = C2_N
+    nl = min(m.latent.n_levels for m in mats)
+    q = synth.queries(n, nl, seed=6, device=dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(6)
+    ids = torch.randint(0, len(mats), (n,), device=dev, generator=g, dtype=torch.int32)
+    f, ws, pdf = neural.query_multi(mats, ids, q["uv"], q["lod"], q["u_rr"], q["wi"], q["wo"], q["u3"])
+    torch.cuda.synchronize()
+    rows = subset_rows(n, 65536, seed=3)
+    hq = host(q, rows)
+    hid = ids.cpu().numpy()[rows]
+    ri = torch.as_tensor(rows, device=dev)
+    fh, wsh = f[ri].cpu().numpy(), ws[ri].cpu().numpy()
+    for k, (m, hk) in enumerate(zip(mats, handles)):
+        sel = hid == k
+        om = oracle_material(m, hk)
+        z_ref, _ = om.half()["latent"].fetch(hq["uv"][sel], hq["lod"][sel], hq["u_rr"][sel])
+        f_ref, _ = O.eval_brdf(om, z_ref, hq["wi"][sel], hq["wo"][sel], fp16=True)
+        p_ref = O.infer_proxy(om, z_ref, hq["wi"][sel], fp16=True)
+        ws_ref = O.sample(p_ref, hq["wi"][sel].astype(np.float64), hq["u3"][sel].astype(np.float64))
+        check_rel(fh[sel], f_ref, what=f"C4 query material {k}")
+        check_dirs(wsh[sel], ws_ref, hq["u3"][sel], p_ref, hq["wi"][sel])
+    del mats, handles
+    torch.cuda.empty_cache()
