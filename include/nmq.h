@@ -122,6 +122,14 @@ int nm_fetch(const nm_material* mat, int64_t n, const float* uv, const float* lo
 
 /* --- eval_material (neural.py:303-309): fetch + frames + BRDF decoder +
  *     brdf_output + horizon mask, fused (the coherent eval kernel). ------- */
+/* Deterministic trilinear fetch (optional filtering mode; the reference only
+ * states it as the roulette fetch's expectation, latent.py:84-92, checked in
+ * tests/test_acceptance.py:242-255): z = (1 - f) bilinear(floor l) +
+ * f bilinear(ceil l), l clipped to [0, L-1], in float64 from the two float32
+ * bilinear fetches (latent.py:100-107), narrowed to fp32.  level_out
+ * (nullable) receives floor(l). */
+int nm_fetch_trilinear(const nm_material* m, int64_t n, const float* uv, const float* lod,
+                       int32_t lod_stride, float* z_out, int32_t* level_out, void* stream);
 int nm_eval(const nm_material* mat, int64_t n, const float* uv, const float* lod,
             int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
             float* rgb_out, float* albedo_out, int32_t* level_out, void* stream);

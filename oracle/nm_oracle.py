@@ -225,6 +225,29 @@ class GatherPyramid(Pyramid):
         return z, chosen
 
 
+def fetch_trilinear(pyr, uv, level):
+    """Deterministic trilinear fetch: the expectation of the roulette fetch
+    over u_rr, stated in latent.py:84-92 and checked by
+    tests/test_acceptance.py:242-255 — (1 - f) * fetch_level(floor l) +
+    f * fetch_level(ceil l), l clipped to [0, L-1] as in choose_level
+    (latent.py:76-82), evaluated in float64 from the two float32 bilinear
+    fetches (latent.py:100-107) and narrowed to float32."""
+    uv = np.atleast_2d(np.asarray(uv, dtype=np.float64))
+    lv = np.clip(np.broadcast_to(np.asarray(level, dtype=np.float64), uv.shape[:-1]), 0, pyr.n_levels - 1)
+    lo = np.floor(lv)
+    f = lv - lo
+    hi = np.minimum(lo + 1, pyr.n_levels - 1)
+    z = np.empty(uv.shape[:-1] + (pyr.levels[0].shape[2],), dtype=np.float32)
+    for l in np.unique(lo):
+        m = lo == l
+        a = pyr.fetch_level(uv[m], int(l)).astype(np.float64)
+        h = int(min(l + 1, pyr.n_levels - 1))
+        b = pyr.fetch_level(uv[m], h).astype(np.float64)
+        fm = f[m][:, None]
+        z[m] = ((1.0 - fm) * a + fm * b).astype(np.float32)
+    return z
+
+
 def random_pyramid(rng, width, height, channels=LATENT_CHANNELS):
     """Synthetic latents, one standard_normal draw per level in order
     (the reference tests' generator, tests/test_latent.py:10-14)."""

@@ -533,6 +533,19 @@ int nm_fetch(const nm_material* m, int64_t n, const float* uv, const float* lod,
   return finish(m, launch_fetch(m->mp, a, (cudaStream_t)stream), "nm_fetch");
 }
 
+int nm_fetch_trilinear(const nm_material* m, int64_t n, const float* uv, const float* lod,
+                       int32_t lod_stride, float* z_out, int32_t* level_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !z_out) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = lod;  // unused
+  a.z_out = z_out; a.level = level_out; a.trilinear = 1;
+  DeviceGuard guard(m->device);
+  return finish(m, launch_fetch(m->mp, a, (cudaStream_t)stream), "nm_fetch_trilinear");
+}
+
 int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
             int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
             float* rgb_out, float* albedo_out, int32_t* level_out, void* stream) {

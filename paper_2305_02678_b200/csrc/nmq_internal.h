@@ -113,6 +113,7 @@ struct QueryArgs {
   int32_t* level;
   int32_t* taps;
   float* wts;
+  int32_t trilinear;  // fetch: deterministic trilinear filtering instead of the roulette pick
   float* dbg;  // fast kernel calibration dump: fp32 T.wi, T.wo and frame conditioning (14 floats/row)
 };
 

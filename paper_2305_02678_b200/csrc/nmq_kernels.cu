@@ -547,6 +547,26 @@ __global__ void __launch_bounds__(256) fetch_kernel(const __grid_constant__ MatP
        i += (int64_t)gridDim.x * blockDim.x) {
     const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + i);
     const float lod = __ldg(a.lod + (a.lod_stride ? i : 0));
+    if (a.trilinear) {
+      // (1 - f) * bilinear(floor l) + f * bilinear(ceil l) in float64 from the
+      // two float32 fetches (the roulette's expectation, latent.py:84-92)
+      const float top = (float)(mp.n_levels - 1);
+      const float l = fminf(fmaxf(lod, 0.f), top);
+      const int lo = (int)floorf(l), hi = lo + 1 < mp.n_levels ? lo + 1 : lo;
+      const double f = (double)l - (double)floorf(l);
+      float za[8], zb[8];
+      fetch_exact(mp, lo, uv.x, uv.y, make_taps(mp, lo, uv.x, uv.y), za);
+      fetch_exact(mp, hi, uv.x, uv.y, make_taps(mp, hi, uv.x, uv.y), zb);
+      float z[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        z[c] = (float)__dadd_rn(__dmul_rn(__dsub_rn(1.0, f), (double)za[c]), __dmul_rn(f, (double)zb[c]));
+      float4* o = reinterpret_cast<float4*>(a.z_out + 8 * i);
+      o[0] = make_float4(z[0], z[1], z[2], z[3]);
+      o[1] = make_float4(z[4], z[5], z[6], z[7]);
+      if (a.level) a.level[i] = lo;
+      continue;
+    }
     const int level = choose_level(mp, lod, __ldg(a.u_rr + i));
     const Taps t = make_taps(mp, level, uv.x, uv.y);
     float z[8];

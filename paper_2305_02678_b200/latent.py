@@ -148,6 +148,24 @@ class LatentPyramid:
                          _io.out(wts, np_mode, np.float64))
         return res
 
+    def fetch_trilinear(self, uv, level):
+        """Deterministic trilinear fetch (optional filtering mode): the roulette
+        fetch's expectation (1 - f) bilinear(floor l) + f bilinear(ceil l)
+        (latent.py:84-92), float64 from the two fp32 bilinear fetches."""
+        if self.channels != LATENT_CHANNELS:
+            raise NotImplementedError("the GPU fetch handles 8-channel latents")
+        np_mode = _io.is_numpy_like(uv)
+        h = self.device_material(None if np_mode else uv.device)
+        dev = h.device
+        uv_t = _io.as_rows(uv, 2, dev, "uv")
+        n = uv_t.shape[0]
+        lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
+        z = _io.empty(n, 8, dev)
+        lib = _lib.load()
+        _lib.check(lib.nm_fetch_trilinear(h.ptr, n, uv_t.data_ptr(), lod_t.data_ptr(), lod_stride, z.data_ptr(),
+                                          None, _io.stream_ptr(dev)), "nm_fetch_trilinear")
+        return _io.out(z, np_mode, np.float32)
+
     def fetch_level(self, uv, level):
         """Deterministic fetch at integer `level` (latent.py:100-107)."""
         n = np.atleast_2d(np.asarray(uv) if _io.is_numpy_like(uv) else uv.cpu().numpy()).shape[0]

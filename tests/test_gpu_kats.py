@@ -262,3 +262,35 @@ def test_fp32_path_sees_in_place_weight_edits():
     f, _ = neural.eval_brdf(mat, z, wi, wo, fp16=False)
     f_ref, _ = O.eval_brdf(_oracle_from(mat), z, wi, wo, fp16=False)
     check_rel(f, f_ref, max_tol=1e-3, mean_tol=1e-5, what="fp32 path after edit")
+
+
+# --- deterministic trilinear filtering (optional mode; exact oracle from
+# latent.py:84-107, tests/test_acceptance.py:242-255) ------------------------
+
+def test_trilinear_fetch_bit_exact():
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(31)
+    for w, h in ((64, 64), (24, 20)):  # power-of-two and non-power-of-two levels
+        opyr = O.random_pyramid(rng, w, h)
+        pyr = LatentPyramid(opyr.levels)
+        n = 5000
+        uv = (rng.random((n, 2)) * 3 - 1).astype(np.float32)  # wraps
+        lod = (rng.random(n) * (pyr.n_levels + 1) - 0.5).astype(np.float32)  # clips at both ends
+        z = pyr.fetch_trilinear(uv, lod)
+        z_ref = O.fetch_trilinear(opyr, uv, lod)
+        assert z.dtype == np.float32 and np.array_equal(z, z_ref), np.abs(z - z_ref).max()
+
+
+def test_trilinear_is_the_roulette_expectation():
+    """Mean of roulette fetches at l = 1.3 -> the trilinear fetch within 3 sigma."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(2)
+    pyr = LatentPyramid(O.random_pyramid(rng, 16, 16).levels)
+    uv = np.array([0.37, 0.81], np.float32)
+    n = 100_000
+    z, _ = pyr.fetch(np.tile(uv, (n, 1)), 1.3, rng.random(n))
+    zt = pyr.fetch_trilinear(uv[None, :], 1.3)[0].astype(np.float64)
+    z = z.astype(np.float64)
+    assert np.all(np.abs(z.mean(0) - zt) <= 3.0 * z.std(0) / np.sqrt(n) + 1e-7)

@@ -1,6 +1,8 @@
 """Pin the numpy oracle (oracle/nm_oracle.py) to the golden vectors that the
 REAL reference produced (oracle/make_golden.py).  CPU only."""
 
+import os
+
 import numpy as np
 import pytest
 
@@ -150,3 +152,59 @@ def test_kl_sampler_loss_oracle_matches_reference(tag):
     for i, (dw, db) in enumerate(grads):
         for a, want in ((dw, g[f"{tag}_dw{i}"]), (db, g[f"{tag}_db{i}"])):
             assert np.abs(a - want).max() <= 1e-6 * np.abs(want).max() + 1e-12
+
+
+def _reference():
+    import importlib
+    import sys
+    src = "/root/reference/pkg/src"
+    if not os.path.isdir(src):
+        pytest.skip("reference not mounted")
+    if src not in sys.path:
+        sys.path.insert(0, src)
+    return importlib.import_module("neuralmat")
+
+
+def test_oracle_trilinear_is_the_reference_expectation():
+    """O.fetch_trilinear == (1-f) fetch_level(lo) + f fetch_level(hi) of the
+    reference pyramid (latent.py:84-107, test_acceptance.py:251)."""
+    _reference()
+    from neuralmat import latent as RL
+    rng = np.random.default_rng(5)
+    opyr = O.random_pyramid(rng, 32, 32)
+    rpyr = RL.LatentPyramid([l.copy() for l in opyr.levels])
+    uv = rng.random((300, 2)).astype(np.float32)
+    for lvl in (0.0, 1.3, 2.75, 4.0, 9.0):
+        lv = min(float(np.float32(lvl)), rpyr.n_levels - 1)  # the level as the fp32 the kernels take
+        lo = int(np.floor(lv))
+        hi = min(lo + 1, rpyr.n_levels - 1)
+        f = lv - lo
+        want = ((1.0 - f) * rpyr.fetch_level(uv, lo).astype(np.float64)
+                + f * rpyr.fetch_level(uv, hi).astype(np.float64)).astype(np.float32)
+        assert np.array_equal(O.fetch_trilinear(opyr, uv, np.full(300, lvl, np.float32)), want)
+
+
+def test_oracle_chi2_harness_matches_reference():
+    """O.chi_square_test restates chi2.py:46-72: same statistic on the same samples."""
+    _reference()
+    from neuralmat import chi2 as RC
+    from neuralmat import proxy as RP
+    p = RP.ProxyParams(0.4, 0.6, (0.1, -0.2), (0.5, 0.3), 0.2, (0.1, 0.05))
+    wi = np.array([0.2, 0.1, 0.97]) / np.linalg.norm([0.2, 0.1, 0.97])
+
+    def run(test):
+        rng = np.random.default_rng(9)
+
+        def sample_fn(n):
+            rep = p.take(np.zeros(n, dtype=np.int64))
+            return RP.sample(rep, np.broadcast_to(wi, (n, 3)), rng.random((n, 3)))
+
+        def pdf_fn(d):
+            rep = p.take(np.zeros(d.shape[0], dtype=np.int64))
+            return RP.pdf(rep, np.broadcast_to(wi, d.shape), d)
+
+        return test(sample_fn, pdf_fn, 50_000)
+
+    ok_r, p_r, s_r, d_r = run(RC.chi_square_test)
+    ok_o, p_o, s_o, d_o = run(O.chi_square_test)
+    assert (ok_r, d_r) == (ok_o, d_o) and s_r == pytest.approx(s_o, rel=1e-12) and p_r == pytest.approx(p_o, rel=1e-9)
