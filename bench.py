@@ -199,6 +199,11 @@ def _cpu_eval_chunk(bounds):
     z, _ = d["pyr"].fetch(d["uv"][s:e], d["lod"][s:e], d["u_rr"][s:e])
     if d["kind"] == "eval":
         O.eval_brdf(d["mat"], z, d["wi"][s:e], d["wo"][s:e], fp16=True)
+    elif d["kind"] == "full":
+        O.eval_brdf(d["mat"], z, d["wi"][s:e], d["wo"][s:e], fp16=True)
+        p = O.infer_proxy(d["mat"], z, d["wi"][s:e], fp16=True)
+        ws = O.sample(p, d["wi"][s:e], d["u3"][s:e])
+        O.pdf(p, d["wi"][s:e], ws)
     else:
         p = O.infer_proxy(d["mat"], z, d["wi"][s:e], fp16=True)
         ws = O.sample(p, d["wi"][s:e], d["u3"][s:e])
@@ -624,6 +629,103 @@ def run_kl(args):
         }))
 
 
+def measure(args, lib, h, workload, sets, steps, warmup, stream, world, local, clocks=None):
+    """Device-timed throughput of one workload: `steps` back-to-back launches
+    of the C-ABI call with inputs resident in HBM (rotating over `sets`),
+    CUDA events on the launching stream, max over ranks.  Returns a dict."""
+    n = sets[0]["uv"].shape[0]
+    dev = sets[0]["uv"].device
+    outs = {"rgb": torch.empty((n, 3), device=dev), "ws": torch.empty((n, 3), device=dev),
+            "pdf": torch.empty((n,), device=dev)}
+    sp = stream.cuda_stream
+    fns = [launch_closure(lib, h, workload, q, outs, sp) for q in sets]
+    for i in range(warmup):
+        fns[i % len(fns)]()
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    l0 = lib.nm_launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if clocks:
+        clocks.start()  # NVML sampling on a background thread during the timed region
+    ev0.record(stream)
+    for i in range(steps):
+        fns[i % len(fns)]()
+    ev1.record(stream)
+    ev1.synchronize()
+    if clocks:
+        clocks.stop()
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = int(lib.nm_launch_count() - l0)
+    ms = ev0.elapsed_time(ev1)
+    ms_max = max_over_ranks(ms, world)
+    uniq = [unique_texels(h, q) for q in sets]
+    texel_b = 16.0 * float(np.mean(uniq)) / n
+    bpq = io_bytes(workload) + texel_b
+    fpq = {"c2": FLOPS_EVAL, "c3": FLOPS_SAMPLE, "full": FLOPS_EVAL + FLOPS_SAMPLE}[workload]
+    hbm, tflops, peak_kind = peaks()
+    kernel_s = ms / steps / 1e3
+    ach = bpq * n / kernel_s / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    return {
+        "value": n * world * steps / (ms_max / 1e3), "ms_per_step": ms_max / steps, "steps": steps,
+        "queries_per_step_per_gpu": n, "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                     "traffic": traffic, "peak_source": peak_kind, "algorithmic_bytes_per_query": bpq,
+                     "texel_bytes_per_query": texel_b,
+                     "tensor_tflops_achieved": fpq * n / kernel_s / 1e12,
+                     "tensor_frac": fpq * n / kernel_s / 1e12 / tflops,
+                     "kernel": "fast_kernel<%s> (csrc/nmq_fast.cu; exact-rounding resolve in its epilogue)" % {
+                         "c2": "kModeEval", "c3": "kModeSamplePdf", "full": "kModeQuery"}[workload]},
+    }
+
+
+def c1_case(arch="2x32"):
+    """BASELINE configs[0] exactly: one random-init material, 512^2 pyramid,
+    65,536 random (uv, wi, wo, lod) queries (SURVEY §8 d2/d3 recipe)."""
+    from oracle import nm_oracle as O  # the host-side recipe's generator (and the CPU baseline)
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(0)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(brdf_hidden=arch), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(np.random.default_rng(0), 512, 512).levels)
+    n = 65536
+    qr = np.random.default_rng(1)
+    q = {"uv": qr.random((n, 2)).astype(np.float32),
+         "lod": (qr.random(n) * (mat.latent.n_levels - 1)).astype(np.float32),
+         "u_rr": qr.random(n).astype(np.float32)}
+    wi, wo = O.draw_direction_pairs(qr, n)
+    q["wi"], q["wo"] = wi.astype(np.float32), wo.astype(np.float32)
+    q["u3"] = qr.random((n, 3)).astype(np.float32)
+    return mat, q
+
+
+def c1_cpu(mat, q, workers):
+    """The oracle's C1 full query (fetch + eval + proxy + sample + pdf, fp16
+    path) on `workers` forked processes, OPENBLAS_NUM_THREADS=1."""
+    from oracle import nm_oracle as O
+
+    def net(m):
+        return O.Net([(l.w, l.b, l.act) for l in m.layers])
+
+    om = O.Material(O.Config(**mat.cfg.to_json()), net(mat.frame_layer), net(mat.brdf_decoder),
+                    net(mat.sampler_decoder))
+    om.latent = O.Pyramid(mat.latent.levels)
+    om.half()
+    _CPU.clear()
+    _CPU.update(mat=om, pyr=om._half["latent"], kind="full", **{k: v.astype(np.float64) for k, v in q.items()})
+    n = q["uv"].shape[0]
+    if "pool" in _POOL:  # workers forked with other data: fork again
+        _POOL["pool"].terminate()
+        _POOL.clear()
+    cpu_run(n, workers)  # warm (forks the pool once)
+    return cpu_run(n, workers)
+
+
 def run_ours(args):
     if args.workload == "c4":
         return run_c4(args)
@@ -635,83 +737,96 @@ def run_ours(args):
         return run_c5(args)
     rank, world, local = dist_init(args.gpus)
     device = torch.device("cuda", local)
-    from paper_2305_02678_b200 import _lib, neural
+    from paper_2305_02678_b200 import _lib, neural, synth
     lib = _lib.load()
     mat, n, sets = build_workload(args, rank, device)
     h = mat.device_material(device)
-    outs = {"rgb": torch.empty((n, 3), device=device), "ws": torch.empty((n, 3), device=device),
-            "pdf": torch.empty((n,), device=device)}
     stream = torch.cuda.current_stream(device)
-    sp = stream.cuda_stream
-
-    # algorithmic bytes per query (exact for these inputs)
-    uniq = [unique_texels(h, q) for q in sets]
-    texel_bytes_per_q = 16.0 * float(np.mean(uniq)) / n
-    bytes_per_q = io_bytes(args.workload) + texel_bytes_per_q
-    flops_per_q = {"c2": FLOPS_EVAL, "c3": FLOPS_SAMPLE, "full": FLOPS_EVAL + FLOPS_SAMPLE}[args.workload]
-
-    # launch closures with their ctypes arguments prepared once, so the host
-    # loop only submits (~7 us/launch) and never starves the GPU
-    launches_fn = [launch_closure(lib, h, args.workload, q, outs, sp) for q in sets]
-    for i in range(args.warmup):
-        launches_fn[i % len(sets)]()
-    torch.cuda.synchronize()
     clocks = Clocks(local)
-    barrier(world)
-    torch.cuda.synchronize()
-    l0 = lib.nm_launch_count()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    clocks.start()  # NVML sampling on a background thread during the timed region
-    ev0.record(stream)
-    for i in range(args.steps):
-        launches_fn[i % len(sets)]()
-    ev1.record(stream)
-    ev1.synchronize()
-    clocks.stop()
-    torch.cuda.synchronize()
-    barrier(world)
-    launches = int(lib.nm_launch_count() - l0)
-    ms = ev0.elapsed_time(ev1)
-    ms_max = max_over_ranks(ms, world)
-    ms_step = ms_max / args.steps
-    value = n * world * args.steps / (ms_max / 1e3)
+    head = measure(args, lib, h, args.workload, sets, args.steps, args.warmup, stream, world, local, clocks)
 
-    hbm, tflops, peak_kind = peaks()
-    kernel_s = ms / args.steps / 1e3
-    achieved_gbs = bytes_per_q * n / kernel_s / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.workload}.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    subs = {}
+    if args.workload == "c2" and not args.no_subresults:
+        # the rest of the metric ("eval, sample+pdf"): C3 and the full query,
+        # each device-timed with its own roofline
+        q3 = [synth.queries(C3_N, mat.latent.n_levels, seed=7 + 100 * rank, device=device,
+                            need=("uv", "lod", "u_rr", "wi", "u3"))]
+        subs["c3_sample_pdf"] = measure(args, lib, h, "c3", q3, max(5, args.steps // 50), 3, stream, world, local)
+        subs["c3_sample_pdf"]["config"] = "C3: 4096^2, 1920x1080x16 = 33,177,600 sample+pdf queries per GPU, random lod"
+        del q3
+        subs["full_query"] = measure(args, lib, h, "full", sets, max(20, args.steps // 5), 3, stream, world, local)
+        subs["full_query"]["config"] = "eval + sample + pdf, 4096^2, 1920x1080 per GPU"
+        # C1 exactly (BASELINE configs[0]) on the GPU
+        mat1, q1 = c1_case()
+        h1 = mat1.device_material(device)
+        t1 = [{k: torch.from_numpy(v).to(device) for k, v in q1.items()}]
+        c1 = measure(args, lib, h1, "full", t1, max(50, args.steps // 2), 5, stream, world, local)
+        c1["config"] = "C1: 512^2 pyramid, 65,536 full queries (inputs fit L2)"
+        subs["c1_full_query"] = c1
+        # the reference's default fp16=False path: fp32 master weights and pyramid
+        if not args.no_fp32_path:
+            from paper_2305_02678_b200.latent import LatentPyramid, level_shapes
+            g = torch.Generator(device=device)
+            g.manual_seed(11)
+            lv = [torch.randn((hh, ww, 8), device=device, generator=g).cpu().numpy()
+                  for hh, ww in level_shapes(RES, RES)]
+            m32 = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), np.random.default_rng(0))
+            m32.latent = LatentPyramid(lv)
+            h32 = m32.device_material(device, precise=True)
+            f32 = measure(args, lib, h32, "c2", sets[:1], max(10, args.steps // 20), 3, stream, world, local)
+            f32["config"] = ("fp16=False (the reference default): fp32 master weights as fp16 hi/lo pairs, "
+                             "fp32 4096^2 pyramid, 1920x1080 eval, generic tcgen05 kernel")
+            subs["fp32_path_eval"] = f32
+            del lv, m32, h32
 
-    # ---- e2e through the public API: pinned host numpy in/out -----------------
-    e2e = None
+    # ---- e2e through the drop-in call --------------------------------------------
+    e2e = e2e_pinned = None
     if args.workload == "c2" and args.e2e_steps > 0:
-        host = []
+        # the reference's own call shape (neural.py:303-309): pageable numpy
+        # in, (f float64, albedo, chosen int64) out
+        host = [{k: v.cpu().numpy() for k, v in q.items()} for q in sets[:2]]
+        for i in range(2):
+            hq = host[i % 2]
+            neural.eval_material(mat, hq["uv"], hq["lod"], hq["wi"], hq["wo"], hq["u_rr"], fp16=True)
+        torch.cuda.synchronize()
+        barrier(world)
+        t0 = time.perf_counter()
+        for i in range(args.e2e_steps):
+            hq = host[i % 2]
+            f, _, lv = neural.eval_material(mat, hq["uv"], hq["lod"], hq["wi"], hq["wo"], hq["u_rr"], fp16=True)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+        e2e = {"value": n * world * args.e2e_steps / (e_ms / 1e3), "unit": "queries/s",
+               "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 16),
+               "steps": args.e2e_steps,
+               "api": "paper_2305_02678_b200.neural.eval_material(mat, uv, lod, wi, wo, u_rr, fp16=True) "
+                      "-> (f float64, None, chosen int64): pageable numpy in/out, the reference call shape "
+                      "(neural.py:303); H2D, kernels, D2H and the dtype conversions inside the timed region"}
+        # pinned host buffers and an fp32 `out`: the zero-copy launch
+        pin = []
         for q in sets[:2]:
             hq = {k: torch.empty(v.shape, dtype=v.dtype, pin_memory=True) for k, v in q.items()}
             for k in hq:
                 hq[k].copy_(q[k])
-            host.append({k: v.numpy() for k, v in hq.items()})
+            pin.append({k: v.numpy() for k, v in hq.items()})
         out_host = torch.empty((n, 3), dtype=torch.float32, pin_memory=True).numpy()
         for i in range(2):
-            hq = host[i % 2]
+            hq = pin[i % 2]
             neural.eval_material(mat, hq["uv"], hq["lod"], hq["wi"], hq["wo"], hq["u_rr"], fp16=True,
                                  return_level=False, out=out_host)
         torch.cuda.synchronize()
         barrier(world)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
+        t0 = time.perf_counter()
         for i in range(args.e2e_steps):
-            hq = host[i % 2]
+            hq = pin[i % 2]
             neural.eval_material(mat, hq["uv"], hq["lod"], hq["wi"], hq["wo"], hq["u_rr"], fp16=True,
                                  return_level=False, out=out_host)
-        e1.record(stream)
         torch.cuda.synchronize()
-        e_ms = max_over_ranks(e0.elapsed_time(e1), world)
-        e2e = {"value": n * world * args.e2e_steps / (e_ms / 1e3), "unit": "queries/s",
-               "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 12),
-               "steps": args.e2e_steps, "api": "paper_2305_02678_b200.neural.eval_material"}
+        e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
+        e2e_pinned = {"value": n * world * args.e2e_steps / (e_ms / 1e3), "unit": "queries/s",
+                      "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 12),
+                      "api": "eval_material on pinned numpy with out= (fp32), return_level=False: one "
+                             "zero-copy fused launch over PCIe"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -723,13 +838,19 @@ def run_ours(args):
                "sample": f"{args.cpu_sample} queries of the same {args.workload.upper()} batch "
                          f"(oracle/nm_oracle.py fp16 path, {workers} forked workers, "
                          f"OPENBLAS_NUM_THREADS=1, {cpu_model()})"}
+        if args.workload == "c2":
+            mat1, q1 = c1_case()
+            cpu["c1_full_query_1core"] = {"value": c1_cpu(mat1, q1, 1), "unit": "queries/s", "cores": 1,
+                                          "sample": "C1 exactly: 65,536 full queries, 512^2, oracle fp16 path"}
+            cpu["c1_full_query_all_cores"] = {"value": c1_cpu(mat1, q1, workers), "unit": "queries/s",
+                                              "cores": workers}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "metric": METRIC, "value": head["value"], "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "fp16 x fp16 -> fp32 tensor-core (hi/lo split), fp32 SIMT",
+            "dtype": "fp16 x fp16 -> fp32 tensor-core (hi/lo split), fp32/fp64 SIMT",
             "data": "synthetic: random-init material (reference init order), N(0,1) fp16 latents, "
                     "seeded uniform queries + half/difference direction pairs",
             "config": {"workload": {"c2": "C2 coherent fused eval, 1 material, 4096^2 latent pyramid, "
@@ -739,20 +860,15 @@ def run_ours(args):
                                         args.workload],
                        "queries_per_step_per_gpu": n, "latent": f"{RES}x{RES} 8ch fp16, 13 levels",
                        "brdf": "2x32", "sampler": "3x32", "parallelism": f"pixel-tile x{world}",
+                       "parity": "exact fp16 input rounding (levels, taps, z bit-exact; strict tolerances)",
                        "l2": f"inputs rotate over {len(sets)} sets "
                              f"({len(sets) * n * io_bytes(args.workload) / 1e6:.0f} MB) > 126 MB L2"},
-            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved_gbs / hbm, "traffic": traffic,
-                         "peak_source": peak_kind,
-                         "algorithmic_bytes_per_query": bytes_per_q,
-                         "texel_bytes_per_query": texel_bytes_per_q,
-                         "tensor_tflops_achieved": flops_per_q * n / kernel_s / 1e12,
-                         "tensor_frac": flops_per_q * n / kernel_s / 1e12 / tflops,
-                         "kernel": "fast_kernel<%s> (csrc/nmq_fast.cu)" % {
-                             "c2": "kModeEval", "c3": "kModeSamplePdf", "full": "kModeQuery"}[args.workload]},
+            "roofline": head["roofline"],
             "e2e": e2e,
+            "e2e_pinned": e2e_pinned,
+            "sub_results": subs or None,
             "cpu_baseline": cpu,
-            "gpu_launches": launches,
+            "gpu_launches": head["gpu_launches"],
             "clocks": clocks.report(),
         }
         print(json.dumps(line))
@@ -812,9 +928,21 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=C2_N)
     ap.add_argument("--ref-sample", type=int, default=262144)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-subresults", action="store_true", help="headline workload only")
+    ap.add_argument("--no-fp32-path", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the line)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd))
     try:
         if args.impl == "reference":
             run_reference(args)

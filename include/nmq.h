@@ -189,17 +189,18 @@ int nm_query_multi(const nm_material* const* mats, int32_t n_mats, int64_t n, co
                    int32_t mode, void* workspace, size_t workspace_bytes, void* stream);
 
 /* --- misc -------------------------------------------------------------- */
-/* nm_eval with HOST buffers; blocking (rgb_out is complete on return),
- * ordered after prior work on `stream`.  All buffers pinned (page-locked):
- * zero-copy, one fused launch reading the inputs and writing rgb over PCIe
- * (`chunk` unused; env NMQ_HOST_ZEROCOPY=0 disables).  Otherwise the batch
+/* nm_eval with HOST buffers; blocking (the outputs are complete on return),
+ * ordered after prior work on `stream`.  albedo_out (n,3) and level_out (n,)
+ * are optional.  All buffers pinned (page-locked): zero-copy, one fused
+ * launch reading the inputs and writing the outputs over PCIe (`chunk`
+ * unused; env NMQ_HOST_ZEROCOPY=0 disables).  Otherwise the batch
  * streams through device staging in `chunk`-query pieces (0 = 512k): one
  * stream for the H2D copies, one for the kernels, one for the D2H copies.
  * The reference call it replaces is eval_material on numpy arrays
  * (neural.py:303). */
 int nm_eval_host(const nm_material* mat, int64_t n, const float* uv, const float* lod,
                  int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
-                 float* rgb_out, int64_t chunk, void* stream);
+                 float* rgb_out, float* albedo_out, int32_t* level_out, int64_t chunk, void* stream);
 
 /* Training-side kernels (device pointers, async on `stream`).
  *  nm_texel_grads: exact adjoint of the fetch (latent.py:109-119

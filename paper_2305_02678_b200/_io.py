@@ -23,9 +23,30 @@ def is_numpy_like(x):
     return not isinstance(x, torch.Tensor)
 
 
-def as_rows(x, cols, device, name="array"):
+def check_exact_f32(x, name):
+    """Texel coordinates, levels and roulette numbers select taps and levels
+    bit for bit; the kernels take them as fp32.  A wider float input whose
+    values fp32 cannot represent exactly is rejected (narrowing it could move
+    floor(u*w - 0.5) or the u_rr < frac decision of latent.py:59-82 across a
+    boundary, breaking the bit-exact contract) — pass fp32 (e.g.
+    ``.astype(np.float32)``) to accept that rounding explicitly."""
+    if isinstance(x, torch.Tensor):
+        if x.dtype == torch.float64 and not torch.equal(x.to(torch.float32).to(torch.float64), x):
+            raise ValueError(f"{name}: float64 values not exactly representable in fp32 (pass fp32)")
+        return
+    a = np.asarray(x)
+    if a.dtype.kind == "f" and a.dtype.itemsize > 4:
+        a32 = a.astype(np.float32)
+        if not np.array_equal(a32.astype(a.dtype), a, equal_nan=True):
+            raise ValueError(f"{name}: float64 values not exactly representable in fp32 (pass fp32)")
+
+
+def as_rows(x, cols, device, name="array", exact=False):
     """(B, cols) fp32 contiguous device tensor; 1-D input of length `cols` is
-    promoted to one row (np.atleast_2d semantics, latent.py:90)."""
+    promoted to one row (np.atleast_2d semantics, latent.py:90).  exact: see
+    check_exact_f32."""
+    if exact:
+        check_exact_f32(x, name)
     if isinstance(x, torch.Tensor):
         t = x
         if t.dim() == 1 and cols > 1:
@@ -44,8 +65,10 @@ def as_rows(x, cols, device, name="array"):
     return t
 
 
-def as_vec(x, n, device, name="array"):
+def as_vec(x, n, device, name="array", exact=False):
     """(n,) fp32 device tensor; scalars broadcast (returns (tensor, stride))."""
+    if exact and not isinstance(x, (int, float)):
+        check_exact_f32(x, name)
     if isinstance(x, torch.Tensor):
         t = x.to(device=device, dtype=torch.float32).reshape(-1).contiguous()
     else:

@@ -105,7 +105,8 @@ SIGNATURES = {
     "nm_fetch_trilinear": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p,
                                    ctypes.c_void_p, ctypes.c_void_p]),
     "nm_eval_host": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p,
-                             c_float_p, c_float_p, c_float_p, c_i64, ctypes.c_void_p]),
+                             c_float_p, c_float_p, c_float_p, c_float_p, ctypes.c_void_p, c_i64,
+                             ctypes.c_void_p]),
     "nm_texel_grads": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, ctypes.c_void_p, c_float_p, c_float_p,
                                ctypes.c_void_p]),
     "nm_mlp_create": (c_i32, [ctypes.c_void_p, c_i32, ctypes.c_void_p]),

@@ -605,7 +605,7 @@ HostStage g_stage[16];
 
 int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* lod,
                  int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
-                 float* rgb_out, int64_t chunk, void* stream) {
+                 float* rgb_out, float* albedo_out, int32_t* level_out, int64_t chunk, void* stream) {
   if (!m) return fail(NM_ERR_INVALID, "null material");
   NM_CHECK_N(n);
   if (n == 0) return NM_OK;
@@ -623,10 +623,11 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
       const char* v = getenv("NMQ_HOST_ZEROCOPY");
       return v ? atoi(v) : 1;
     }();
-    const void* hp[6] = {uv, lod, u_rr, wi, wo, rgb_out};
-    void* dp[6];
+    const void* hp[8] = {uv, lod, u_rr, wi, wo, rgb_out, albedo_out, level_out};
+    void* dp[8] = {};
     bool mapped = zc != 0;
-    for (int i = 0; i < 6 && mapped; ++i) {
+    for (int i = 0; i < 8 && mapped; ++i) {
+      if (!hp[i]) continue;  // optional outputs
       cudaPointerAttributes at;
       if (cudaPointerGetAttributes(&at, hp[i]) != cudaSuccess || at.type != cudaMemoryTypeHost ||
           !at.devicePointer) {
@@ -640,7 +641,7 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
       QueryArgs a{};
       a.n = n; a.uv = (const float*)dp[0]; a.lod = (const float*)dp[1]; a.lod_stride = lod_stride ? 1 : 0;
       a.u_rr = (const float*)dp[2]; a.wi = (const float*)dp[3]; a.wo = (const float*)dp[4];
-      a.rgb = (float*)dp[5];
+      a.rgb = (float*)dp[5]; a.albedo = (float*)dp[6]; a.level = (int32_t*)dp[7];
       if ((e = launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream)) != cudaSuccess)
         return cuda_fail(e, "nm_eval_host");
       if ((e = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
@@ -649,7 +650,7 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
   }
   HostStage& H = g_stage[m->device & 15];
   std::lock_guard<std::mutex> lock(H.mu);
-  const size_t per_row = 8 + 4 + 4 + 12 + 12 + 12;  // uv lod u_rr wi wo | rgb
+  const size_t per_row = 8 + 4 + 4 + 12 + 12 + 12 + 12 + 4;  // uv lod u_rr wi wo | rgb albedo level
   const size_t need = NMQ_HOST_SLOTS * (size_t)chunk * per_row + 1024;
   if (H.bytes < need) {
     if (H.buf) cudaFree(H.buf);
@@ -680,6 +681,8 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
     float* d_wi = d_urr + chunk;
     float* d_wo = d_wi + 3 * chunk;
     float* d_rgb = d_wo + 3 * chunk;
+    float* d_alb = d_rgb + 3 * chunk;
+    int32_t* d_lv = reinterpret_cast<int32_t*>(d_alb + 3 * chunk);
     if (reuse) cudaStreamWaitEvent(H.h2d, H.ev_k[s], 0);  // older chunk's kernel has read the inputs
     cudaMemcpyAsync(d_uv, uv + 2 * c0, c * 8, cudaMemcpyHostToDevice, H.h2d);
     if (lod_stride) cudaMemcpyAsync(d_lod, lod + c0, c * 4, cudaMemcpyHostToDevice, H.h2d);
@@ -693,10 +696,14 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
     QueryArgs a{};
     a.n = c; a.uv = d_uv; a.lod = d_lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = d_urr;
     a.wi = d_wi; a.wo = d_wo; a.rgb = d_rgb;
+    a.albedo = albedo_out ? d_alb : nullptr;
+    a.level = level_out ? d_lv : nullptr;
     if ((e = launch_fused(m->mp, kModeEval, a, H.run)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
     cudaEventRecord(H.ev_k[s], H.run);
     cudaStreamWaitEvent(H.d2h, H.ev_k[s], 0);
     cudaMemcpyAsync(rgb_out + 3 * c0, d_rgb, c * 12, cudaMemcpyDeviceToHost, H.d2h);
+    if (albedo_out) cudaMemcpyAsync(albedo_out + 3 * c0, d_alb, c * 12, cudaMemcpyDeviceToHost, H.d2h);
+    if (level_out) cudaMemcpyAsync(level_out + c0, d_lv, c * 4, cudaMemcpyDeviceToHost, H.d2h);
     cudaEventRecord(H.ev_out[s], H.d2h);
   }
   for (cudaStream_t st : {H.h2d, H.run, H.d2h})

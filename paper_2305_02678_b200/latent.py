@@ -128,10 +128,10 @@ class LatentPyramid:
         np_mode = _io.is_numpy_like(uv)
         h = self.device_material(None if np_mode else uv.device)
         dev = h.device
-        uv_t = _io.as_rows(uv, 2, dev, "uv")
+        uv_t = _io.as_rows(uv, 2, dev, "uv", exact=True)
         n = uv_t.shape[0]
-        lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
-        urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+        lod_t, lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
+        urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
         z = _io.empty(n, 8, dev)
         lv = _io.empty(n, 1, dev, torch.int32)
         taps = _io.empty(n, 8, dev, torch.int32) if return_taps else None
@@ -157,9 +157,9 @@ class LatentPyramid:
         np_mode = _io.is_numpy_like(uv)
         h = self.device_material(None if np_mode else uv.device)
         dev = h.device
-        uv_t = _io.as_rows(uv, 2, dev, "uv")
+        uv_t = _io.as_rows(uv, 2, dev, "uv", exact=True)
         n = uv_t.shape[0]
-        lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
+        lod_t, lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
         z = _io.empty(n, 8, dev)
         lib = _lib.load()
         _lib.check(lib.nm_fetch_trilinear(h.ptr, n, uv_t.data_ptr(), lod_t.data_ptr(), lod_stride, z.data_ptr(),

@@ -249,10 +249,10 @@ class _QueryInputs:
         self.np_mode = _io.is_numpy_like(uv)
         self.h = mat.device_material(None if self.np_mode else uv.device, precise=not fp16)
         dev = self.dev = self.h.device
-        self.uv = _io.as_rows(uv, 2, dev, "uv")
+        self.uv = _io.as_rows(uv, 2, dev, "uv", exact=True)
         n = self.n = self.uv.shape[0]
-        self.lod, self.lod_stride = _io.as_vec(level, n, dev, "level")
-        self.urr, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+        self.lod, self.lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
+        self.urr, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
         for k in need:
             t = _io.as_rows(dirs[k], 3, dev, k)
             if t.shape[0] != n:
@@ -260,15 +260,19 @@ class _QueryInputs:
             setattr(self, k, t)
 
 
-def _stream_eval(mat, uv, level, wi, wo, u_rr, out):
-    """eval_material for a large host batch through nm_eval_host: chunked
-    H2D / fused kernel / D2H overlapped on three internal streams, all in native
-    code.  None if not applicable (albedo head, non-contiguous shapes...)."""
-    if mat.cfg.albedo_head:
-        return None
+def _host_eval(mat, uv, level, wi, wo, u_rr, out, return_level):
+    """eval_material on host (numpy) arrays through nm_eval_host, all in
+    native code: pinned buffers go zero-copy (one fused launch over PCIe),
+    pageable ones stream in chunks (H2D / fused kernel / D2H overlapped on
+    three internal streams).  Returns (f, albedo, level) with the reference's
+    dtypes (f/albedo float64, level int64; f is `out` when given), or None if
+    the arrays are not plain host rows."""
     n = np.shape(uv)[0] if np.ndim(uv) == 2 else 0
-    if n < 2 * _io.STREAM_CHUNK:
+    if n == 0:
         return None
+    for x, name in ((uv, "uv"), (level, "level"), (u_rr, "u_rr")):
+        if not isinstance(x, (int, float)):
+            _io.check_exact_f32(x, name)
     h_uv, h_wi, h_wo = _io.host_rows(uv, 2, "uv"), _io.host_rows(wi, 3, "wi"), _io.host_rows(wo, 3, "wo")
     h_lod = np.ascontiguousarray(np.asarray(level, dtype=np.float32)).reshape(-1)
     h_urr = np.ascontiguousarray(np.asarray(u_rr, dtype=np.float32)).reshape(-1)
@@ -278,12 +282,17 @@ def _stream_eval(mat, uv, level, wi, wo, u_rr, out):
     if out is not None and (out.dtype != np.float32 or out.shape != (n, 3) or not out.flags.c_contiguous):
         return None
     f_host = out if out is not None else np.empty((n, 3), np.float32)
+    alb = np.empty((n, 3), np.float32) if mat.cfg.albedo_head else None
+    lv = np.empty(n, np.int32) if return_level else None
     h = mat.device_material(None)
     lib = _lib.load()
     _launch(lib.nm_eval_host, h.ptr, n, h_uv.ctypes.data, h_lod.ctypes.data, int(h_lod.shape[0] == n),
             h_urr.ctypes.data, h_wi.ctypes.data, h_wo.ctypes.data, f_host.ctypes.data,
+            None if alb is None else alb.ctypes.data, None if lv is None else lv.ctypes.data,
             _io.STREAM_CHUNK, _io.stream_ptr(h.device))
-    return f_host if out is not None else f_host.astype(np.float64)
+    f = f_host if out is not None else f_host.astype(np.float64)
+    return (f, None if alb is None else alb.astype(np.float64),
+            None if lv is None else lv.astype(np.int64))
 
 
 def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, out=None):
@@ -292,10 +301,10 @@ def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, o
     `out` may pass a preallocated (B,3) fp32 device tensor, or a host (ideally
     pinned) fp32 buffer, for f.  Large host batches without albedo or level
     outputs stream through the GPU in overlapped chunks."""
-    if fp16 and not return_level and _io.is_numpy_like(uv) and (out is None or isinstance(out, np.ndarray)):
-        f = _stream_eval(mat, uv, level, wi, wo, u_rr, out)
-        if f is not None:
-            return f, None, None
+    if fp16 and _io.is_numpy_like(uv) and (out is None or isinstance(out, np.ndarray)):
+        r = _host_eval(mat, uv, level, wi, wo, u_rr, out, return_level)
+        if r is not None:
+            return r
     q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), fp16=fp16, wi=wi, wo=wo)
     on_dev = isinstance(out, torch.Tensor) and out.is_cuda
     f = out if on_dev else _io.empty(q.n, 3, q.dev)
@@ -393,10 +402,10 @@ def eval_material_multi(mats, mat_id, uv, level, wi, wo, u_rr, mode="binned", fp
     dev = handles[0].device
     if any(h.device != dev for h in handles):
         raise ValueError("materials must live on the same device")
-    uv_t = _io.as_rows(uv, 2, dev, "uv")
+    uv_t = _io.as_rows(uv, 2, dev, "uv", exact=True)
     n = uv_t.shape[0]
-    lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
-    urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+    lod_t, lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
+    urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
     wi_t = _io.as_rows(wi, 3, dev, "wi")
     wo_t = _io.as_rows(wo, 3, dev, "wo")
     if isinstance(mat_id, torch.Tensor):
@@ -425,10 +434,10 @@ def _multi_inputs(mats, mat_id, uv, level, u_rr, dirs):
     dev = handles[0].device
     if any(h.device != dev for h in handles):
         raise ValueError("materials must live on the same device")
-    uv_t = _io.as_rows(uv, 2, dev, "uv")
+    uv_t = _io.as_rows(uv, 2, dev, "uv", exact=True)
     n = uv_t.shape[0]
-    lod_t, lod_stride = _io.as_vec(level, n, dev, "level")
-    urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr")
+    lod_t, lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
+    urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
     d = {k: _io.as_rows(v, 3, dev, k) for k, v in dirs.items()}
     if isinstance(mat_id, torch.Tensor):
         ids = mat_id.to(device=dev, dtype=torch.int32).reshape(-1).contiguous()
