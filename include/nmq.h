@@ -49,6 +49,9 @@ enum nm_act { NM_ACT_LINEAR = 0, NM_ACT_LEAKY = 1 }; /* mlp.py:22 _ACT_CODES */
  * segments, coherent kernel per segment, ids validated (one host round trip);
  * BINNED_ASYNC: the same without the host round trip (segment sizes stay on
  * the device; rows with out-of-range ids are left untouched). */
+/* nm_query_f64 modes */
+enum nm_query_mode { NM_QUERY_EVAL = 0, NM_QUERY_SAMPLE_PDF = 1, NM_QUERY_FULL = 2 };
+
 enum nm_multi_mode { NM_MULTI_DIVERGENT = 0, NM_MULTI_BINNED = 1, NM_MULTI_BINNED_ASYNC = 2 };
 
 /* One quantized network exactly as the reference holds it
@@ -122,6 +125,25 @@ int nm_fetch(const nm_material* mat, int64_t n, const float* uv, const float* lo
 
 /* --- eval_material (neural.py:303-309): fetch + frames + BRDF decoder +
  *     brdf_output + horizon mask, fused (the coherent eval kernel). ------- */
+/* float64 coordinates (uv (n,2), lod, u_rr), the reference's own dtype
+ * (latent.py:59-82 computes in float64; render.py:369 passes float64): level
+ * pick, taps and weights exactly as numpy does them, so levels / taps / z stay
+ * bit-exact for any float64 input (the fp32 entry points are exact for
+ * fp32-representable inputs).  Directions stay fp32.  Runs on the generic
+ * kernels. */
+int nm_fetch_f64(const nm_material* m, int64_t n, const double* uv, const double* lod, int32_t lod_stride,
+                 const double* u_rr, float* z_out, int32_t* level_out, int32_t* taps_out, float* wts_out,
+                 void* stream);
+int nm_query_f64(const nm_material* m, int32_t mode, int64_t n, const double* uv, const double* lod,
+                 int32_t lod_stride, const double* u_rr, const float* wi, const float* wo, const float* u3,
+                 float* rgb_out, float* albedo_out, float* ws_out, float* pdf_out, float* params9_out,
+                 int32_t* level_out, void* stream);
+/* Eval reduced to the per-pixel sample mean in the kernel epilogue (the
+ * renderer's spp accumulation, render.py:565): rows are pixel * spp + s,
+ * spp a power of two, n a multiple of spp; img_out (n / spp, 3) fp32 is
+ * overwritten.  Per-sample rgb never reaches memory. */
+int nm_eval_spp(const nm_material* m, int64_t n, const float* uv, const float* lod, int32_t lod_stride,
+                const float* u_rr, const float* wi, const float* wo, int32_t spp, float* img_out, void* stream);
 /* Deterministic trilinear fetch (optional filtering mode; the reference only
  * states it as the roulette fetch's expectation, latent.py:84-92, checked in
  * tests/test_acceptance.py:242-255): z = (1 - f) bilinear(floor l) +

@@ -23,22 +23,48 @@ def is_numpy_like(x):
     return not isinstance(x, torch.Tensor)
 
 
-def check_exact_f32(x, name):
-    """Texel coordinates, levels and roulette numbers select taps and levels
-    bit for bit; the kernels take them as fp32.  A wider float input whose
-    values fp32 cannot represent exactly is rejected (narrowing it could move
-    floor(u*w - 0.5) or the u_rr < frac decision of latent.py:59-82 across a
-    boundary, breaking the bit-exact contract) — pass fp32 (e.g.
-    ``.astype(np.float32)``) to accept that rounding explicitly."""
+def inexact_f64(x):
+    """True if x holds float64 values fp32 cannot represent exactly (python
+    float scalars included): texel coordinates, levels and roulette numbers
+    select levels and taps bit for bit, so such inputs take the float64
+    coordinate entry points (nm_fetch_f64 / nm_query_f64) instead of being
+    narrowed (latent.py:59-82 computes them in float64)."""
     if isinstance(x, torch.Tensor):
-        if x.dtype == torch.float64 and not torch.equal(x.to(torch.float32).to(torch.float64), x):
-            raise ValueError(f"{name}: float64 values not exactly representable in fp32 (pass fp32)")
-        return
+        return x.dtype == torch.float64 and not torch.equal(x.to(torch.float32).to(torch.float64), x)
+    if isinstance(x, float):
+        return float(np.float32(x)) != x
     a = np.asarray(x)
     if a.dtype.kind == "f" and a.dtype.itemsize > 4:
-        a32 = a.astype(np.float32)
-        if not np.array_equal(a32.astype(a.dtype), a, equal_nan=True):
-            raise ValueError(f"{name}: float64 values not exactly representable in fp32 (pass fp32)")
+        return not np.array_equal(a.astype(np.float32).astype(a.dtype), a, equal_nan=True)
+    return False
+
+
+def check_exact_f32(x, name):
+    """Entry points without a float64 coordinate path reject float64 values
+    fp32 cannot represent (see inexact_f64) instead of narrowing them."""
+    if inexact_f64(x):
+        raise ValueError(f"{name}: float64 values not exactly representable in fp32 (pass fp32)")
+
+
+def as_rows64(x, cols, device, name="array"):
+    """(B, cols) float64 contiguous device tensor (float64 coordinates)."""
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float64))
+    if t.dim() == 1 and cols > 1:
+        t = t[None, :]
+    t = t.to(device=device, dtype=torch.float64).contiguous()
+    if cols > 1 and (t.dim() != 2 or t.shape[1] != cols):
+        raise ValueError(f"{name}: expected shape (B, {cols}), got {tuple(t.shape)}")
+    return t
+
+
+def as_vec64(x, n, device, name="array"):
+    t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(np.asarray(x, np.float64)))
+    t = t.to(device=device, dtype=torch.float64).reshape(-1).contiguous()
+    if t.numel() == 1 and n != 1:
+        return t, 0
+    if t.numel() != n:
+        raise ValueError(f"{name}: expected {n} values, got {t.numel()}")
+    return t, 1
 
 
 def as_rows(x, cols, device, name="array", exact=False):
@@ -67,7 +93,7 @@ def as_rows(x, cols, device, name="array", exact=False):
 
 def as_vec(x, n, device, name="array", exact=False):
     """(n,) fp32 device tensor; scalars broadcast (returns (tensor, stride))."""
-    if exact and not isinstance(x, (int, float)):
+    if exact:
         check_exact_f32(x, name)
     if isinstance(x, torch.Tensor):
         t = x.to(device=device, dtype=torch.float32).reshape(-1).contiguous()

@@ -16,6 +16,7 @@ NM_ERR_INVALID = -1
 NM_ERR_CUDA = -2
 NM_ERR_UNSUPPORTED = -3
 
+NM_QUERY_EVAL, NM_QUERY_SAMPLE_PDF, NM_QUERY_FULL = 0, 1, 2
 NM_MULTI_DIVERGENT = 0
 NM_MULTI_BINNED = 1
 NM_MULTI_BINNED_ASYNC = 2
@@ -102,6 +103,11 @@ SIGNATURES = {
     "nm_query_multi": (c_i32, [ctypes.c_void_p, c_i32, c_i64, ctypes.c_void_p, c_float_p, c_float_p, c_i32,
                                c_float_p, c_float_p, c_float_p, c_float_p, c_float_p, c_float_p, c_float_p, c_i32,
                                ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]),
+    "nm_fetch_f64": (c_i32, [ctypes.c_void_p, c_i64, ctypes.c_void_p, ctypes.c_void_p, c_i32, ctypes.c_void_p,
+                             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
+    "nm_query_f64": (c_i32, [ctypes.c_void_p, c_i32, c_i64] + [ctypes.c_void_p] * 14),
+    "nm_eval_spp": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p, c_float_p,
+                            c_float_p, c_i32, c_float_p, ctypes.c_void_p]),
     "nm_fetch_trilinear": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p,
                                    ctypes.c_void_p, ctypes.c_void_p]),
     "nm_eval_host": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p,

@@ -546,6 +546,63 @@ int nm_fetch_trilinear(const nm_material* m, int64_t n, const float* uv, const f
   return finish(m, launch_fetch(m->mp, a, (cudaStream_t)stream), "nm_fetch_trilinear");
 }
 
+int nm_fetch_f64(const nm_material* m, int64_t n, const double* uv, const double* lod, int32_t lod_stride,
+                 const double* u_rr, float* z_out, int32_t* level_out, int32_t* taps_out, float* wts_out,
+                 void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.uv64 = uv; a.lod64 = lod; a.lod_stride = lod_stride ? 1 : 0; a.urr64 = u_rr;
+  a.z_out = z_out; a.level = level_out; a.taps = taps_out; a.wts = wts_out;
+  DeviceGuard guard(m->device);
+  return finish(m, launch_fetch(m->mp, a, (cudaStream_t)stream), "nm_fetch_f64");
+}
+
+int nm_query_f64(const nm_material* m, int32_t mode, int64_t n, const double* uv, const double* lod,
+                 int32_t lod_stride, const double* u_rr, const float* wi, const float* wo, const float* u3,
+                 float* rgb_out, float* albedo_out, float* ws_out, float* pdf_out, float* params9_out,
+                 int32_t* level_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  const bool brdf = mode == NM_QUERY_EVAL || mode == NM_QUERY_FULL;
+  const bool samp = mode == NM_QUERY_SAMPLE_PDF || mode == NM_QUERY_FULL;
+  if (!brdf && !samp) return fail(NM_ERR_INVALID, "unknown query mode");
+  if (!uv || !lod || !u_rr || !wi || (brdf && (!wo || !rgb_out)) || (samp && (!u3 || !ws_out || !pdf_out)))
+    return fail(NM_ERR_INVALID, "null input");
+  if (brdf && !m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  if (samp && !m->mp.has_sampler) return fail(NM_ERR_INVALID, "material has no sampler decoder");
+  QueryArgs a{};
+  a.n = n; a.uv64 = uv; a.lod64 = lod; a.lod_stride = lod_stride ? 1 : 0; a.urr64 = u_rr;
+  a.wi = wi; a.wo = wo; a.u3 = u3; a.rgb = rgb_out; a.albedo = albedo_out; a.ws = ws_out; a.pdf = pdf_out;
+  a.params9 = params9_out; a.level = level_out;
+  DeviceGuard guard(m->device);
+  const int kmode = mode == NM_QUERY_EVAL ? kModeEval : (mode == NM_QUERY_SAMPLE_PDF ? kModeSamplePdf : kModeQuery);
+  return finish(m, launch_fused(m->mp, kmode, a, (cudaStream_t)stream), "nm_query_f64");
+}
+
+int nm_eval_spp(const nm_material* m, int64_t n, const float* uv, const float* lod, int32_t lod_stride,
+                const float* u_rr, const float* wi, const float* wo, int32_t spp, float* img_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (spp <= 0 || (spp & (spp - 1))) return fail(NM_ERR_INVALID, "spp must be a power of two");
+  if (n % spp) return fail(NM_ERR_INVALID, "the batch must be whole pixels (n a multiple of spp)");
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !wo || !img_out) return fail(NM_ERR_INVALID, "null input");
+  if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  int lg = 0;
+  while ((1 << lg) < spp) ++lg;
+  DeviceGuard guard(m->device);
+  cudaError_t e = cudaMemsetAsync(img_out, 0, (size_t)(n / spp) * 12, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "nm_eval_spp");
+  QueryArgs a{};
+  a.n = n; a.uv = uv; a.lod = lod; a.lod_stride = lod_stride ? 1 : 0; a.u_rr = u_rr;
+  a.wi = wi; a.wo = wo; a.img = img_out; a.spp_log2 = lg;
+  return finish(m, launch_fused(m->mp, kModeEval, a, (cudaStream_t)stream), "nm_eval_spp");
+}
+
 int nm_eval(const nm_material* m, int64_t n, const float* uv, const float* lod,
             int32_t lod_stride, const float* u_rr, const float* wi, const float* wo,
             float* rgb_out, float* albedo_out, int32_t* level_out, void* stream) {

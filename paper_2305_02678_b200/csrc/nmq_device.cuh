@@ -511,6 +511,52 @@ __device__ __forceinline__ void fetch_exact(const MatParams& m, int level, float
   blend64<false>(tex, w, z);
 }
 
+// float64 coordinates (the reference's own dtype: uv, level and u_rr are
+// float64 arrays in latent.py / render.py:369) — every step as numpy does it
+__device__ __forceinline__ int choose_level(const MatParams& m, double lod, double urr) {
+  const double top = (double)(m.n_levels - 1);
+  const double l = fmin(fmax(lod, 0.0), top);
+  const double lo = floor(l);
+  int c = (int)lo + ((urr < __dsub_rn(l, lo)) ? 1 : 0);
+  c = c < 0 ? 0 : c;
+  c = c > m.n_levels - 1 ? m.n_levels - 1 : c;
+  return c;
+}
+__device__ __forceinline__ double frac64d(double u, int32_t w) {  // latent.py:59-64: fl(fl(u*w) - 0.5)
+  const double x = __dsub_rn(__dmul_rn(u, (double)w), 0.5);
+  return __dsub_rn(x, floor(x));
+}
+__device__ __forceinline__ Taps make_taps(const MatParams& m, int level, double u, double v) {
+  const LevelDesc L = m.lv[level];
+  Taps t;
+  const double x = __dsub_rn(__dmul_rn(u, (double)L.w), 0.5);
+  const double y = __dsub_rn(__dmul_rn(v, (double)L.h), 0.5);
+  const double xf = floor(x), yf = floor(y);
+  t.fx = (float)(x - xf);
+  t.fy = (float)(y - yf);
+  t.x0 = (int32_t)wrap_index(xf, L.w);
+  t.y0 = (int32_t)wrap_index(yf, L.h);
+  t.x1 = (t.x0 + 1 == L.w) ? 0 : t.x0 + 1;
+  t.y1 = (t.y0 + 1 == L.h) ? 0 : t.y0 + 1;
+  t.w = L.w;
+  t.base = L.off;
+  return t;
+}
+__device__ __forceinline__ void fetch_exact(const MatParams& m, int level, double u, double v, const Taps& t,
+                                            float (&z)[8]) {
+  double w[4];
+  weights64(frac64d(u, m.lv[level].w), frac64d(v, m.lv[level].h), w);
+  if (m.texel_fp32) {
+    const int64_t idx[4] = {tap_index(t, 0), tap_index(t, 1), tap_index(t, 2), tap_index(t, 3)};
+    blend64_f32(reinterpret_cast<const float4*>(m.latent), idx, w, z);
+    return;
+  }
+  uint4 tex[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) tex[k] = __ldg(m.latent + tap_index(t, k));
+  blend64<false>(tex, w, z);
+}
+
 // fp16 rounding of a pair (the decoder input rounding, mlp.py:205)
 __device__ __forceinline__ uint32_t pack_h2(float a, float b) {
   const __half2 h = __floats2half2_rn(a, b);
@@ -689,6 +735,29 @@ __device__ __forceinline__ void brdf_simt_warp(const MatParams& m, const uint32_
         y[o] = p;
       }
     }
+  }
+}
+
+// Per-pixel sample mean in the eval epilogue (the renderer's spp
+// accumulation, render.py:565): rows q = pixel * spp + s, spp = 2^spp_log2,
+// consecutive rows on consecutive lanes.  The warp sums each aligned segment
+// of min(spp, 32) lanes with shuffles and its first lane adds the segment's
+// share of the mean to img[pixel] (fp32 atomics: 1 per 32 samples at spp >= 32).
+// Warp-collective: every lane calls it (rows past the batch with valid = false).
+__device__ __forceinline__ void spp_accumulate(float* img, int64_t q, V3 f, bool valid, int spp_log2) {
+  const float inv = __int_as_float((127 - spp_log2) << 23);  // 2^-spp_log2, exact
+  float x = valid ? f.x * inv : 0.f, y = valid ? f.y * inv : 0.f, z = valid ? f.z * inv : 0.f;
+  const int seg = spp_log2 < 5 ? (1 << spp_log2) : 32;
+  for (int d = seg >> 1; d > 0; d >>= 1) {
+    x += __shfl_xor_sync(0xffffffffu, x, d);
+    y += __shfl_xor_sync(0xffffffffu, y, d);
+    z += __shfl_xor_sync(0xffffffffu, z, d);
+  }
+  if (valid && ((threadIdx.x & 31) & (seg - 1)) == 0) {
+    float* o = img + 3 * (q >> spp_log2);
+    atomicAdd(o, x);
+    atomicAdd(o + 1, y);
+    atomicAdd(o + 2, z);
   }
 }
 

@@ -86,9 +86,10 @@ constexpr float kLk = 0.98019802570343017578f;  // fp32(99/101)
 
 // Exact-rounding queue of one launch: CTA b owns entries [b * cap, (b+1) * cap)
 // of `ent` (kQueueWords x 16 B each: {row, x16[0..2]}, {x16[3..5], z16[0]},
-// {z16[1..3], wi.x}, {wi.y, wi.z, wo.x, wo.y}, {wo.z, frames to resolve, 0, 0}) and writes how
+// {z16[1..3], wi.x}, {wi.y, wi.z, wo.x, wo.y}, {wo.z, frames to resolve, 0, 0},
+// {fast rgb (spp-mean launches only), 0}) and writes how
 // many it used to cnt[b] when it exits.
-constexpr int kQueueWords = 5;
+constexpr int kQueueWords = 6;
 struct ResolveQ {
   uint4* ent;
   uint32_t* cnt;
@@ -417,6 +418,7 @@ struct SlotSt {
   V3 wi, u3;        // the row's directions (registers: the buffer is refilled early)
   bool up;          // wi.z > 0 && wo.z > 0
   TexPrefetch nx;   // texels of the slot's next tile
+  int32_t qslot;    // spp-mean launches: this row's resolve-queue entry (-1: none)
 };
 
 // Follow-up of a BRDF-mode launch: blocks (b, *) resolve the rows CTA b
@@ -446,7 +448,7 @@ __device__ __forceinline__ void load_row8(const MatParams& mp, uint32_t off, int
   }
 }
 
-template <int BW, int BNH>
+template <int BW, int BNH, bool RED = false>
 __device__ __forceinline__ void resolve_entries(const MatParams& mp, const QueryArgs& a, const uint4* ent,
                                                 uint32_t n, uint32_t first, uint32_t step, uint32_t tid) {
   const int lane = tid & 31;
@@ -549,7 +551,14 @@ __device__ __forceinline__ void resolve_entries(const MatParams& mp, const Query
         for (int d = 16; d > 0; d >>= 1) p += __shfl_xor_sync(0xffffffffu, p, d);
         y[o] = p + mp.ob[o];
       }
-      if (lane == src) {
+      if (RED && lane == src) {  // replace the fast value's share of its pixel's mean
+        const uint4 e5 = __ldg(ent + kQueueWords * (size_t)i + 5);
+        const float inv = __int_as_float((127 - a.spp_log2) << 23);
+        float* o = a.img + 3 * ((int64_t)row >> a.spp_log2);
+        atomicAdd(o, (brdf_output(y[0]) - __uint_as_float(e5.x)) * inv);
+        atomicAdd(o + 1, (brdf_output(y[1]) - __uint_as_float(e5.y)) * inv);
+        atomicAdd(o + 2, (brdf_output(y[2]) - __uint_as_float(e5.z)) * inv);
+      } else if (lane == src) {
         const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + row) : (int64_t)row;
         // queued rows are above the horizon (below it the output is 0 either way)
         stg3(a.rgb, q, v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])));
@@ -568,7 +577,8 @@ resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Que
                            blockIdx.y * kResolveThreads, kResolveThreads * gridDim.y, threadIdx.x);
 }
 
-template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG, bool DBG = false>
+template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG, bool DBG = false,
+          bool RED = false>
 __global__ void __launch_bounds__(G * 128, 1)
 fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
             const __grid_constant__ FastConsts fc) {
@@ -801,13 +811,16 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             const bool flag = valid && S.up && (near_f0 | near_f1) != 0u;
             // queue the tile's flagged rows (one shared atomic per warp)
             const uint32_t wmask = __ballot_sync(0xffffffffu, flag);
+            if constexpr (RED) S.qslot = -1;
             if (wmask) {
               const int lead = __ffs(wmask) - 1;
               uint32_t wbase = 0;
               if ((r & 31) == lead) wbase = atomicAdd(&q_cnt, __popc(wmask));
               wbase = __shfl_sync(0xffffffffu, wbase, lead);
               if (flag) {
-                uint4* e = fc.q.ent + kQueueWords * ((size_t)blockIdx.x * fc.q.cap + wbase + __popc(wmask & lanemask_lt()));
+                const uint32_t slot = wbase + __popc(wmask & lanemask_lt());
+                if constexpr (RED) S.qslot = (int32_t)slot;
+                uint4* e = fc.q.ent + kQueueWords * ((size_t)blockIdx.x * fc.q.cap + slot);
                 e[0] = make_uint4((uint32_t)(seg_base + q_in), x[0], x[1], x[2]);
                 e[1] = make_uint4(x[3], x[4], x[5], S.zp[0]);
                 e[2] = make_uint4(S.zp[1], S.zp[2], S.zp[3], __float_as_uint(S.wi.x));
@@ -845,7 +858,15 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           mma_wait(S.bar, S.ph);
           float y[6];
           out_layer_simt<BW>(S.dl, mp, fc.inv_brdf, mp.albedo != 0, y);
-          if (valid) {
+          if constexpr (RED) {
+            // per-pixel spp mean straight from the epilogue: per-sample rgb
+            // never reaches HBM; a queued row keeps its fast value in its entry
+            const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
+            spp_accumulate(a.img, q_in, f, valid, a.spp_log2);
+            if (S.qslot >= 0)
+              fc.q.ent[kQueueWords * ((size_t)blockIdx.x * fc.q.cap + S.qslot) + 5] =
+                  make_uint4(__float_as_uint(f.x), __float_as_uint(f.y), __float_as_uint(f.z), 0u);
+          } else if (valid) {
             const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
             const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                               : v3(0.f, 0.f, 0.f);
@@ -921,8 +942,8 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     if (NMQ_RESOLVE_FUSED) {
       // every queued row's output is stored (the barrier above): the CTA
       // resolves its own rows while other SMs are still on their tiles
-      resolve_entries<BW, BNH>(mp, a, fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap, q_cnt, 0,
-                               G * 128, tid);
+      resolve_entries<BW, BNH, RED>(mp, a, fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap, q_cnt, 0,
+                                    G * 128, tid);
     } else if (tid == 0) {
       fc.q.cnt[blockIdx.x] = q_cnt;
     }
@@ -1059,14 +1080,17 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
       if (a.params9) c.params9 = a.params9 + 9 * c0;
       if (a.level) c.level = a.level + c0;
       if (a.dbg) c.dbg = a.dbg + 14 * c0;
+      if (a.img) c.img = a.img + 3 * (c0 >> a.spp_log2);  // chunks are whole pixels (2^24 rows)
       const cudaError_t e = launch_fast_t<MODE, BW, BNH, SW, SNH, G, NS, TS>(mp, c, s);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
   }
+  if (a.img && (MODE != kModeEval || seg || !NMQ_RESOLVE_FUSED)) return cudaErrorNotSupported;
   auto kern = seg ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, true>
-                  : (a.dbg && MODE == kModeEval) ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false, true>
-                                                 : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
+              : (a.dbg && MODE == kModeEval) ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false, true>
+              : (a.img && MODE == kModeEval) ? fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false, false, true>
+                                             : fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>;
   const int smem = (int)(((mp.wblob_bytes + 127) & ~127u) + G * NS * 2 * sizeof(InBuf<MODE>) +
                          (TS ? G * NS * kTile * 64 : 0));
   const int max_dyn = std::min(max_dynamic_smem((const void*)fast_kernel<MODE, BW, BNH, SW, SNH, G, NS, TS, false>),
@@ -1119,7 +1143,7 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 // Returns cudaErrorNotSupported when the fast path does not apply (caller
 // then uses the generic kernel).
 cudaError_t launch_fast(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s) {
-  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx) return cudaErrorNotSupported;
+  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx || a.uv64) return cudaErrorNotSupported;
   if (mode != kModeEval && mode != kModeSamplePdf && mode != kModeQuery)
     return cudaErrorNotSupported;
   if (!aligned16(a.uv) || !aligned16(a.u_rr) || !aligned16(a.wi) ||

@@ -92,6 +92,9 @@ struct QueryArgs {
   const float* lod;
   int32_t lod_stride;
   const float* u_rr;
+  const double* uv64;   // optional float64 coordinates (generic kernels): uv, lod, u_rr
+  const double* lod64;
+  const double* urr64;
   const float* z;
   const float* wi;
   const float* wo;
@@ -113,6 +116,8 @@ struct QueryArgs {
   int32_t* level;
   int32_t* taps;
   float* wts;
+  int32_t spp_log2;   // eval with img: per-pixel mean over 2^spp_log2 consecutive rows (in-kernel)
+  float* img;          // (n >> spp_log2, 3), accumulated (zeroed by the caller)
   int32_t trilinear;  // fetch: deterministic trilinear filtering instead of the roulette pick
   float* dbg;  // fast kernel calibration dump: fp32 T.wi, T.wo and frame conditioning (14 floats/row)
 };

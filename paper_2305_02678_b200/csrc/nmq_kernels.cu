@@ -353,26 +353,45 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
         if constexpr (MODE == kModeEvalZ) wo = ldg3(a.wo, q);
       }
     } else {
-      float u = 0.f, v = 0.f, lod = 0.f, urr = 0.f;
-      if (valid) {
-        const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + q);
-        u = uv.x;
-        v = uv.y;
-        lod = __ldg(a.lod + (a.lod_stride ? q : 0));
-        urr = __ldg(a.u_rr + q);
-        wi = ldg3(a.wi, q);
-        if constexpr (MODE != kModeSamplePdf) wo = ldg3(a.wo, q);
+      if (a.uv64) {  // float64 coordinates, as the reference computes them
+        double u = 0.0, v = 0.0, lod = 0.0, urr = 0.0;
+        if (valid) {
+          u = __ldg(a.uv64 + 2 * q);
+          v = __ldg(a.uv64 + 2 * q + 1);
+          lod = __ldg(a.lod64 + (a.lod_stride ? q : 0));
+          urr = __ldg(a.urr64 + q);
+          wi = ldg3(a.wi, q);
+          if constexpr (MODE != kModeSamplePdf) wo = ldg3(a.wo, q);
+        }
+        const int level = choose_level(mp, lod, urr);
+        fetch_exact(mp, level, u, v, make_taps(mp, level, u, v), z);
+        if (valid && a.level) a.level[oq] = level;
+      } else {
+        float u = 0.f, v = 0.f, lod = 0.f, urr = 0.f;
+        if (valid) {
+          const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + q);
+          u = uv.x;
+          v = uv.y;
+          lod = __ldg(a.lod + (a.lod_stride ? q : 0));
+          urr = __ldg(a.u_rr + q);
+          wi = ldg3(a.wi, q);
+          if constexpr (MODE != kModeSamplePdf) wo = ldg3(a.wo, q);
+        }
+        const int level = choose_level(mp, lod, urr);
+        const Taps t = make_taps(mp, level, u, v);
+        fetch_exact(mp, level, u, v, t, z);
+        if (valid && a.level) a.level[oq] = level;
       }
-      const int level = choose_level(mp, lod, urr);
-      const Taps t = make_taps(mp, level, u, v);
-      fetch_exact(mp, level, u, v, t, z);
-      if (valid && a.level) a.level[oq] = level;
     }
 
     if constexpr (MODE == kModeEval || MODE == kModeEvalZ || MODE == kModeQuery) {
       float y[16];
       brdf_decode(mp, g, z, wi, wo, y);
-      if (valid) {
+      if (MODE == kModeEval && a.img) {  // per-pixel spp mean (warp-collective)
+        const bool up = (wi.z > 0.f) && (wo.z > 0.f);
+        const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
+        spp_accumulate(a.img, i, f, valid, a.spp_log2);
+      } else if (valid) {
         const bool up = (wi.z > 0.f) && (wo.z > 0.f);
         const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                         : v3(0.f, 0.f, 0.f);
@@ -545,6 +564,31 @@ __global__ void __launch_bounds__(256) fetch_kernel(const __grid_constant__ MatP
                                                     const __grid_constant__ QueryArgs a) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < a.n;
        i += (int64_t)gridDim.x * blockDim.x) {
+    if (a.uv64) {  // float64 coordinates
+      const double u = __ldg(a.uv64 + 2 * i), v = __ldg(a.uv64 + 2 * i + 1);
+      const int level = choose_level(mp, __ldg(a.lod64 + (a.lod_stride ? i : 0)), __ldg(a.urr64 + i));
+      const Taps t = make_taps(mp, level, u, v);
+      float z[8];
+      fetch_exact(mp, level, u, v, t, z);
+      if (a.z_out) {
+        float4* o = reinterpret_cast<float4*>(a.z_out + 8 * i);
+        o[0] = make_float4(z[0], z[1], z[2], z[3]);
+        o[1] = make_float4(z[4], z[5], z[6], z[7]);
+      }
+      if (a.level) a.level[i] = level;
+      if (a.taps) {
+        int32_t* p = a.taps + 8 * i;
+        p[0] = t.x0; p[1] = t.y0; p[2] = t.x1; p[3] = t.y0;
+        p[4] = t.x0; p[5] = t.y1; p[6] = t.x1; p[7] = t.y1;
+      }
+      if (a.wts) {
+        double w[4];
+        weights64(frac64d(u, mp.lv[level].w), frac64d(v, mp.lv[level].h), w);
+        float* o = a.wts + 4 * i;
+        o[0] = (float)w[0]; o[1] = (float)w[1]; o[2] = (float)w[2]; o[3] = (float)w[3];
+      }
+      continue;
+    }
     const float2 uv = __ldg(reinterpret_cast<const float2*>(a.uv) + i);
     const float lod = __ldg(a.lod + (a.lod_stride ? i : 0));
     if (a.trilinear) {

@@ -128,18 +128,21 @@ class LatentPyramid:
         np_mode = _io.is_numpy_like(uv)
         h = self.device_material(None if np_mode else uv.device)
         dev = h.device
-        uv_t = _io.as_rows(uv, 2, dev, "uv", exact=True)
+        # float64 coordinates fp32 cannot hold exactly stay float64 (nm_fetch_f64)
+        f64 = any(_io.inexact_f64(x) for x in (uv, level, u_rr))
+        rows, vec = (_io.as_rows64, _io.as_vec64) if f64 else (_io.as_rows, _io.as_vec)
+        uv_t = rows(uv, 2, dev, "uv")
         n = uv_t.shape[0]
-        lod_t, lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
-        urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
+        lod_t, lod_stride = vec(level, n, dev, "level")
+        urr_t, _ = vec(u_rr, n, dev, "u_rr")
         z = _io.empty(n, 8, dev)
         lv = _io.empty(n, 1, dev, torch.int32)
         taps = _io.empty(n, 8, dev, torch.int32) if return_taps else None
         wts = _io.empty(n, 4, dev) if return_taps else None
         lib = _lib.load()
-        _lib.check(lib.nm_fetch(h.ptr, n, uv_t.data_ptr(), lod_t.data_ptr(), lod_stride,
-                                urr_t.data_ptr(), z.data_ptr(), lv.data_ptr(), _io.ptr(taps),
-                                _io.ptr(wts), _io.stream_ptr(dev)), "nm_fetch")
+        fn = lib.nm_fetch_f64 if f64 else lib.nm_fetch
+        _lib.check(fn(h.ptr, n, uv_t.data_ptr(), lod_t.data_ptr(), lod_stride, urr_t.data_ptr(), z.data_ptr(),
+                      lv.data_ptr(), _io.ptr(taps), _io.ptr(wts), _io.stream_ptr(dev)), fn.__name__)
         res = (_io.out(z, np_mode, np.float32), _io.out(lv, np_mode, np.int64))
         if return_taps:
             t = taps.reshape(n, 4, 2)

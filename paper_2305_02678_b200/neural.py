@@ -249,10 +249,18 @@ class _QueryInputs:
         self.np_mode = _io.is_numpy_like(uv)
         self.h = mat.device_material(None if self.np_mode else uv.device, precise=not fp16)
         dev = self.dev = self.h.device
-        self.uv = _io.as_rows(uv, 2, dev, "uv", exact=True)
-        n = self.n = self.uv.shape[0]
-        self.lod, self.lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
-        self.urr, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
+        # float64 coordinates fp32 cannot hold exactly keep float64 (nm_query_f64)
+        self.f64 = any(_io.inexact_f64(x) for x in (uv, level, u_rr))
+        if self.f64:
+            self.uv = _io.as_rows64(uv, 2, dev, "uv")
+            n = self.n = self.uv.shape[0]
+            self.lod, self.lod_stride = _io.as_vec64(level, n, dev, "level")
+            self.urr, _ = _io.as_vec64(u_rr, n, dev, "u_rr")
+        else:
+            self.uv = _io.as_rows(uv, 2, dev, "uv")
+            n = self.n = self.uv.shape[0]
+            self.lod, self.lod_stride = _io.as_vec(level, n, dev, "level")
+            self.urr, _ = _io.as_vec(u_rr, n, dev, "u_rr")
         for k in need:
             t = _io.as_rows(dirs[k], 3, dev, k)
             if t.shape[0] != n:
@@ -270,9 +278,8 @@ def _host_eval(mat, uv, level, wi, wo, u_rr, out, return_level):
     n = np.shape(uv)[0] if np.ndim(uv) == 2 else 0
     if n == 0:
         return None
-    for x, name in ((uv, "uv"), (level, "level"), (u_rr, "u_rr")):
-        if not isinstance(x, (int, float)):
-            _io.check_exact_f32(x, name)
+    if any(_io.inexact_f64(x) for x in (uv, level, u_rr)):
+        return None  # float64 coordinates: the device path's nm_query_f64
     h_uv, h_wi, h_wo = _io.host_rows(uv, 2, "uv"), _io.host_rows(wi, 3, "wi"), _io.host_rows(wo, 3, "wo")
     h_lod = np.ascontiguousarray(np.asarray(level, dtype=np.float32)).reshape(-1)
     h_urr = np.ascontiguousarray(np.asarray(u_rr, dtype=np.float32)).reshape(-1)
@@ -311,9 +318,14 @@ def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, o
     alb = _io.empty(q.n, 3, q.dev) if mat.cfg.albedo_head else None
     lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
     lib = _lib.load()
-    _launch(lib.nm_eval, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
-            q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), f.data_ptr(), _io.ptr(alb),
-            _io.ptr(lv), _io.stream_ptr(q.dev))
+    if q.f64:
+        _launch(lib.nm_query_f64, q.h.ptr, _lib.NM_QUERY_EVAL, q.n, q.uv.data_ptr(), q.lod.data_ptr(),
+                q.lod_stride, q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), None, f.data_ptr(),
+                _io.ptr(alb), None, None, None, _io.ptr(lv), _io.stream_ptr(q.dev))
+    else:
+        _launch(lib.nm_eval, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
+                q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), f.data_ptr(), _io.ptr(alb),
+                _io.ptr(lv), _io.stream_ptr(q.dev))
     if out is not None and not on_dev:  # host buffer (numpy or pinned CPU tensor)
         (torch.from_numpy(out) if isinstance(out, np.ndarray) else out).copy_(f)
         f_res = out
@@ -321,6 +333,24 @@ def eval_material(mat, uv, level, wi, wo, u_rr, fp16=False, return_level=True, o
         f_res = _io.out(f, q.np_mode)
     return (f_res, None if alb is None else _io.out(alb, q.np_mode),
             None if lv is None else _io.out(lv, q.np_mode, np.int64))
+
+
+def eval_material_spp(mat, uv, level, wi, wo, u_rr, spp, fp16=True, out=None):
+    """eval_material reduced to the per-pixel mean over `spp` consecutive
+    samples inside the kernel (the renderer's accumulation, render.py:565):
+    rows are pixel * spp + s; returns the (B / spp, 3) image (fp32 tensor for
+    torch callers, float64 numpy otherwise)."""
+    _require_fp16(fp16)
+    for x, name in ((uv, "uv"), (level, "level"), (u_rr, "u_rr")):
+        _io.check_exact_f32(x, name)
+    q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), fp16=fp16, wi=wi, wo=wo)
+    if spp <= 0 or spp & (spp - 1) or q.n % spp:
+        raise ValueError("spp must be a power of two dividing the batch")
+    img = out if isinstance(out, torch.Tensor) and out.is_cuda else _io.empty(q.n // spp, 3, q.dev)
+    lib = _lib.load()
+    _launch(lib.nm_eval_spp, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride, q.urr.data_ptr(),
+            q.wi.data_ptr(), q.wo.data_ptr(), int(spp), img.data_ptr(), _io.stream_ptr(q.dev))
+    return _io.out(img, q.np_mode)
 
 
 def infer_proxy(mat, z, wi, fp16=False):
@@ -350,9 +380,14 @@ def sample_pdf(mat, uv, level, u_rr, wi, u, fp16=True, return_params=False, retu
     p9 = _io.empty(q.n, 9, q.dev) if return_params else None
     lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
     lib = _lib.load()
-    _launch(lib.nm_sample_pdf, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
-            q.urr.data_ptr(), q.wi.data_ptr(), q.u.data_ptr(), ws.data_ptr(), p.data_ptr(),
-            _io.ptr(p9), _io.ptr(lv), _io.stream_ptr(q.dev))
+    if q.f64:
+        _launch(lib.nm_query_f64, q.h.ptr, _lib.NM_QUERY_SAMPLE_PDF, q.n, q.uv.data_ptr(), q.lod.data_ptr(),
+                q.lod_stride, q.urr.data_ptr(), q.wi.data_ptr(), None, q.u.data_ptr(), None, None,
+                ws.data_ptr(), p.data_ptr(), _io.ptr(p9), _io.ptr(lv), _io.stream_ptr(q.dev))
+    else:
+        _launch(lib.nm_sample_pdf, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
+                q.urr.data_ptr(), q.wi.data_ptr(), q.u.data_ptr(), ws.data_ptr(), p.data_ptr(),
+                _io.ptr(p9), _io.ptr(lv), _io.stream_ptr(q.dev))
     res = (_io.out(ws, q.np_mode), _io.out(p, q.np_mode))
     if return_params:
         res = res + (ProxyParams.from_block(p9, q.np_mode),)
@@ -370,9 +405,14 @@ def query(mat, uv, level, u_rr, wi, wo, u, fp16=True, return_level=False):
     p = _io.empty(q.n, 1, q.dev)
     lv = _io.empty(q.n, 1, q.dev, torch.int32) if return_level else None
     lib = _lib.load()
-    _launch(lib.nm_query, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
-            q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), q.u.data_ptr(), f.data_ptr(),
-            ws.data_ptr(), p.data_ptr(), _io.ptr(lv), _io.stream_ptr(q.dev))
+    if q.f64:
+        _launch(lib.nm_query_f64, q.h.ptr, _lib.NM_QUERY_FULL, q.n, q.uv.data_ptr(), q.lod.data_ptr(),
+                q.lod_stride, q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), q.u.data_ptr(), f.data_ptr(),
+                None, ws.data_ptr(), p.data_ptr(), None, _io.ptr(lv), _io.stream_ptr(q.dev))
+    else:
+        _launch(lib.nm_query, q.h.ptr, q.n, q.uv.data_ptr(), q.lod.data_ptr(), q.lod_stride,
+                q.urr.data_ptr(), q.wi.data_ptr(), q.wo.data_ptr(), q.u.data_ptr(), f.data_ptr(),
+                ws.data_ptr(), p.data_ptr(), _io.ptr(lv), _io.stream_ptr(q.dev))
     res = (_io.out(f, q.np_mode), _io.out(ws, q.np_mode), _io.out(p, q.np_mode))
     if return_level:
         res = res + (_io.out(lv, q.np_mode, np.int64),)

@@ -114,5 +114,5 @@ def test_training_and_host_entry_points_validate_before_launch(lib):
     assert lib.nm_kl_target_dir(4, 1, 2, *([None] * 6)) == inv
     assert lib.nm_kl_grad(4, 0, *([None] * 8)) == inv
     assert lib.nm_kl_grad(0, 0, *([None] * 8)) == ok
-    assert lib.nm_eval_host(None, 10, None, None, 1, None, None, None, None, 0, None) == inv
+    assert lib.nm_eval_host(None, 10, None, None, 1, None, None, None, None, None, None, 0, None) == inv
     assert lib.nm_mlp_backward(None, 4, None, None, None, None, None) == inv

@@ -290,7 +290,46 @@ def test_trilinear_is_the_roulette_expectation():
     pyr = LatentPyramid(O.random_pyramid(rng, 16, 16).levels)
     uv = np.array([0.37, 0.81], np.float32)
     n = 100_000
-    z, _ = pyr.fetch(np.tile(uv, (n, 1)), 1.3, rng.random(n))
-    zt = pyr.fetch_trilinear(uv[None, :], 1.3)[0].astype(np.float64)
+    z, _ = pyr.fetch(np.tile(uv, (n, 1)), np.float32(1.3), rng.random(n).astype(np.float32))
+    zt = pyr.fetch_trilinear(uv[None, :], np.float32(1.3))[0].astype(np.float64)
     z = z.astype(np.float64)
     assert np.all(np.abs(z.mean(0) - zt) <= 3.0 * z.std(0) / np.sqrt(n) + 1e-7)
+
+
+
+# --- float64 coordinates (the reference's dtype): levels, taps and z bit-exact
+# for inputs fp32 cannot represent (latent.py:59-82) ---------------------------
+
+def test_float64_coordinates_bit_exact_at_boundaries():
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+    from test_gpu_parity import _oracle_from
+    rng = np.random.default_rng(41)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 24, 40).levels)  # npot levels
+    n = 20000
+    w0, h0 = 24, 40
+    # texel-boundary coordinates: u*w - 0.5 within ~1e-13 of an integer, and
+    # u_rr within 1e-13 of the level fraction (the float32 rounding of either
+    # would flip the tap or the level)
+    k = rng.integers(-40, 80, size=(n, 2)).astype(np.float64)
+    uv = (k + 0.5) / np.array([w0, h0]) + rng.choice([-1e-13, 1e-13, 0.0], size=(n, 2))
+    lod = rng.random(n) * (mat.latent.n_levels - 1)
+    urr = (lod - np.floor(lod)) + rng.choice([-1e-13, 1e-13], size=n)
+    pyr = O.Pyramid(mat.latent.levels)
+    z_ref, ch_ref = pyr.fetch(uv, lod, urr)
+    z, ch = mat.latent.fetch(uv, lod, urr)
+    assert np.array_equal(ch, ch_ref) and np.array_equal(z, z_ref)
+    zh, chh, xs, ys, _ = mat.half()["latent"].fetch(uv, lod, urr, return_taps=True)
+    hz, hch = O.Pyramid(mat.half()["latent"].levels).fetch(uv, lod, urr)
+    assert np.array_equal(chh, hch) and np.array_equal(zh, hz)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    f_ref, _, ch2 = O.eval_material(_oracle_from(mat), uv, lod, wi.astype(np.float32), wo.astype(np.float32),
+                                    urr, fp16=True)
+    f, _, ch3 = neural.eval_material(mat, uv, lod, wi.astype(np.float32), wo.astype(np.float32), urr, fp16=True)
+    assert np.array_equal(ch3, ch2)
+    check_rel(f, f_ref, what="float64 coordinates")
+    # float32-narrowed, the same inputs would pick other levels / taps on some rows
+    _, ch32 = pyr.fetch(uv.astype(np.float32), lod.astype(np.float32), urr.astype(np.float32))
+    assert not np.array_equal(ch32, ch_ref)

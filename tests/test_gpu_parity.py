@@ -551,3 +551,34 @@ def test_empty_batches_are_no_ops():
     z, lv = mat.latent.fetch(e2, e1, e1)
     assert z.shape == (0, 8)
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("spp", [1, 4, 64])
+def test_eval_spp_mean_in_kernel(spp, kernel_path):
+    """nm_eval_spp: the per-pixel mean over spp consecutive rows computed in
+    the eval epilogue equals the mean of the per-sample results (up to fp32
+    summation order) and the oracle's; forced exact resolution of every row
+    changes nothing beyond that order."""
+    import torch
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import _lib, neural, shard, synth
+
+    dev = torch.device("cuda", 0)
+    mat = synth.material("2x32", 128, 128, seed=5, device=dev)
+    n = 64 * 1000 + 64 * 3  # several tiles + a partial one
+    q = synth.queries(n, mat.latent.n_levels, seed=8, device=dev, need=("uv", "lod", "u_rr", "wi", "wo"))
+    f = neural.eval_material(mat, q["uv"], q["lod"], q["wi"], q["wo"], q["u_rr"], fp16=True)[0]
+    img = neural.eval_material_spp(mat, q["uv"], q["lod"], q["wi"], q["wo"], q["u_rr"], spp)
+    assert _last_path() == kernel_path
+    ref = shard.reduce_spp(f, spp)
+    np.testing.assert_allclose(img.cpu().numpy(), ref.cpu().numpy(), rtol=2e-6, atol=1e-7)
+    lib = _lib.load()
+    try:
+        lib.nm_set_tw_margin(1e30)
+        img2 = neural.eval_material_spp(mat, q["uv"], q["lod"], q["wi"], q["wo"], q["u_rr"], spp)
+    finally:
+        lib.nm_set_tw_margin(0.0)
+    np.testing.assert_allclose(img2.cpu().numpy(), ref.cpu().numpy(), rtol=2e-6, atol=1e-7)
+    with pytest.raises(ValueError):
+        neural.eval_material_spp(mat, q["uv"][:100], q["lod"][:100], q["wi"][:100], q["wo"][:100],
+                                 q["u_rr"][:100], 64)
