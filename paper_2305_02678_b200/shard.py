@@ -40,6 +40,8 @@ def gather_bands(band, height, width, dst=0, group=None):
     the (height, width, C) image on `dst`, None elsewhere."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    if dist.get_backend(group) == "gloo" and band.is_cuda:  # gloo gathers host tensors
+        band = band.cpu()
     c = band.shape[-1]
     max_rows = row_band(0, world, height)[1]  # rank 0 holds the largest band
     buf = band.new_zeros((max_rows, width, c))
