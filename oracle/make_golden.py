@@ -197,6 +197,27 @@ def make_train_case(name="train", seed=41):
             d[f"{tag}_dw{i}"] = grads[i][0]
             d[f"{tag}_db{i}"] = grads[i][1]
         d[f"{tag}_x"], d[f"{tag}_g"], d[f"{tag}_out"], d[f"{tag}_dx"] = x, g, out, dx
+    # the 3x64 BRDF decoder's shape (the width-64 kernel instances) and a
+    # 13-layer width-64 net whose padded / float64 weight copies exceed the
+    # 200 KB SMEM budget (the unpadded forward and float-weight backward
+    # fallbacks); own generator, so the cases above stay as they were
+    wrng = np.random.default_rng(seed + 1)
+    for tag, sizes in (("wide", (20, 64, 64, 64, 3)), ("deep", (20,) + (64,) * 12 + (3,))):
+        net = mlp.Mlp.create(sizes, wrng)
+        for l in net.layers:
+            l.b[:] = wrng.normal(0, 0.1, l.b.shape).astype(np.float32)
+        x = _f32(wrng.normal(0, 1, (2051, sizes[0])))
+        g = _f32(wrng.normal(0, 1, (2051, sizes[-1])))
+        out, cache = net.forward_cached(x)
+        grads, dx = net.backward(cache, g)
+        d[f"{tag}_n"] = np.int64(len(net.layers))
+        for i, l in enumerate(net.layers):
+            d[f"{tag}_w{i}"] = l.w
+            d[f"{tag}_b{i}"] = l.b
+            d[f"{tag}_a{i}"] = np.int64(0 if l.act == "linear" else 1)
+            d[f"{tag}_dw{i}"] = grads[i][0]
+            d[f"{tag}_db{i}"] = grads[i][1]
+        d[f"{tag}_x"], d[f"{tag}_g"], d[f"{tag}_out"], d[f"{tag}_dx"] = x, g, out, dx
     pyr = latent.LatentPyramid.zeros(32, 16)
     for lvl in pyr.levels:
         lvl[:] = rng.standard_normal(lvl.shape).astype(np.float32)
@@ -268,13 +289,14 @@ def make_vertex_case(name="vertex", n=3000, seed=51):
 def make_kl_case(name="kl", b=2048, seed=61):
     """KL sampler loss (training.py:219-273) from the reference:
     loss and sampler-decoder gradients with fixed uniforms, for the default
-    material (2 frames), one frame, no frames (vanilla), isotropic sampler
-    and the albedo head (6 decoder outputs)."""
+    material (2 frames), one frame, no frames (vanilla), isotropic sampler,
+    the albedo head (6 decoder outputs) and the 3x64 BRDF decoder."""
     geom, latent, neural, proxy = _ref()
     from neuralmat import training
     d = {}
     variants = (("std", {}), ("oneframe", {"n_frames": 1}), ("vanilla", {"use_frames": False}),
-                ("iso", {"sampler_isotropic": True}), ("albedo", {"albedo_head": True}))
+                ("iso", {"sampler_isotropic": True}), ("albedo", {"albedo_head": True}),
+                ("wide", {"brdf_hidden": "3x64"}))
     for k, (tag, kw) in enumerate(variants):
         cfg = neural.NeuralMaterialConfig(**kw)
         mat = neural.NeuralMaterial.create(cfg, np.random.default_rng(seed + k))

@@ -515,6 +515,8 @@ const void* nm_material_latent_ptr(const nm_material* m) { return m ? m->latent 
 
 static int finish(const nm_material* m, cudaError_t e, const char* what) {
   (void)m;
+  if (e == cudaErrorNotSupported)
+    return fail(NM_ERR_UNSUPPORTED, std::string(what) + ": shape outside what the kernels implement");
   if (e != cudaSuccess) return cuda_fail(e, what);
   return NM_OK;
 }

@@ -485,7 +485,8 @@ cudaError_t launch_mlp_forward(const int32_t* fi, const int32_t* fo, const int32
   auto kern = wide ? (pad ? mlp_forward_kernel<64, true> : mlp_forward_kernel<64, false>)
                    : (pad ? mlp_forward_kernel<32, true> : mlp_forward_kernel<32, false>);
   const int lim = max_dynamic_smem((const void*)kern);
-  if (lim < 0 || (int)smem > lim) return cudaErrorInvalidValue;
+  if (lim < 0) return cudaErrorInvalidValue;
+  if ((int)smem > lim) return cudaErrorNotSupported;  // weights larger than shared memory
   cudaError_t e;
   int64_t blocks = (B + 127) / 128;
   if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;
@@ -514,7 +515,8 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
   auto kern = wide ? (w64 ? mlp_backward_kernel<64, double> : mlp_backward_kernel<64, float>)
                    : (w64 ? mlp_backward_kernel<32, double> : mlp_backward_kernel<32, float>);
   const int lim = max_dynamic_smem((const void*)kern);
-  if (lim < 0 || (int)smem > lim) return cudaErrorInvalidValue;
+  if (lim < 0) return cudaErrorInvalidValue;
+  if ((int)smem > lim) return cudaErrorNotSupported;  // weights larger than shared memory
   cudaError_t e;
   int64_t blocks = (B + 127) / 128;
   if (blocks > (int64_t)sm_count() * 8) blocks = (int64_t)sm_count() * 8;

@@ -11,7 +11,7 @@ from conftest import load_golden
 
 pytestmark = pytest.mark.gpu
 
-TAGS = ("std", "oneframe", "vanilla", "iso", "albedo")
+TAGS = ("std", "oneframe", "vanilla", "iso", "albedo", "wide")
 
 
 def _mat(g, tag):

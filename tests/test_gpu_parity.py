@@ -441,7 +441,7 @@ def _train_net(g, tag):
                               "linear" if int(g[f"{tag}_a{i}"]) == 0 else "leaky_relu") for i in range(n)])
 
 
-@pytest.mark.parametrize("tag", ["brdf", "samp"])
+@pytest.mark.parametrize("tag", ["brdf", "samp", "wide", "deep"])
 def test_mlp_forward_cached_backward_vs_reference(tag):
     """Mlp.forward_cached / backward on the GPU against the reference's own
     outputs (tests/golden/train.npz): fp32 forward to float32 rounding-order

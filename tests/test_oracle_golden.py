@@ -110,7 +110,7 @@ def test_training_side_oracle_matches_reference():
     """forward_cached / backward / accumulate_texel_grads restatements
     against the reference's own outputs (tests/golden/train.npz)."""
     g = load_golden("train")
-    for tag in ("brdf", "samp"):
+    for tag in ("brdf", "samp", "wide", "deep"):
         n = int(g[f"{tag}_n"])
         net = O.Net([(g[f"{tag}_w{i}"], g[f"{tag}_b{i}"], "linear" if int(g[f"{tag}_a{i}"]) == 0 else "leaky_relu")
                      for i in range(n)])
@@ -132,7 +132,7 @@ def test_training_side_oracle_matches_reference():
         assert np.array_equal(l, g[f"tg_grad{i}"])
 
 
-@pytest.mark.parametrize("tag", ["std", "oneframe", "vanilla", "iso", "albedo"])
+@pytest.mark.parametrize("tag", ["std", "oneframe", "vanilla", "iso", "albedo", "wide"])
 def test_kl_sampler_loss_oracle_matches_reference(tag):
     """oracle.sampler_loss_and_grads against the reference's own
     training.sampler_loss_and_grads (tests/golden/kl.npz)."""
