@@ -11,8 +11,15 @@
  *    material's device, fp32 (or int32), C-contiguous, batch-first:
  *    uv (n,2), lod (n,) or scalar, u_rr (n,), wi/wo (n,3), u3 (n,3),
  *    z (n,8), params9 (n,9), rgb/albedo/ws (n,3), pdf (n,), level (n,).
- *  - `stream` is a cudaStream_t passed as void*.  Launches are asynchronous
- *    and never allocate; many streams may launch on one material at once.
+ *  - `stream` is a cudaStream_t passed as void*.  Launches are asynchronous;
+ *    many streams may launch on one material at once.  Allocation: the
+ *    device-pointer entry points allocate nothing per call, except one
+ *    grow-only scratch buffer per (device, stream) — the fp16 fast path's
+ *    exact-rounding queue (stream-ordered cudaMallocAsync, reused by every
+ *    later call on that stream).  nm_eval_host keeps one grow-only device
+ *    staging buffer per device (cudaMalloc when a call needs more; calls on
+ *    one device serialize on it).
+ *    Nothing is freed before nm_destroy / process exit.
  *  - Optional outputs may be NULL.  `lod_stride` is 1 for a per-query array
  *    and 0 to broadcast lod[0] (the reference's scalar level, latent.py:91).
  *  - Return value: 0 = ok, < 0 = error; nm_last_error() returns a

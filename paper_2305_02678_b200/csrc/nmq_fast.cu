@@ -78,6 +78,9 @@ using namespace dev;
 #ifndef NMQ_PDL
 #define NMQ_PDL 1  // programmatic dependent launch (prologue overlaps the previous kernel's tail): C2 +4 %
 #endif
+#ifndef NMQ_TW_INLINE
+#define NMQ_TW_INLINE 0  // 1: every row's direction inputs in float64 inline (no queue)
+#endif
 #ifndef NMQ_FAST_NS
 #define NMQ_FAST_NS 1  // tiles in flight per group (2 = ping-pong; slower: fewer warps)
 #endif
@@ -792,6 +795,20 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             float raw[12];
 #pragma unroll
             for (int j = 0; j < 12; ++j) raw[j] = __uint_as_float(fr[j]);
+#if NMQ_TW_INLINE
+            {
+              (void)raw;
+              uint32_t x6[6];
+              tw_exact(mp, S.zp, S.wi, wo, x6);
+              const uint32_t x[8] = {x6[0], x6[1], x6[2], x6[3], x6[4], x6[5], 0u, 0u};
+              tc::tmem_st8(S.al + 8, x);
+              if constexpr (RED) S.qslot = -1;
+              mma_issue<BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, refill);
+            }
+            if (false) {
+#else
+            {
+#endif
             float ti[6], to[6];
             const float2 kappa = frames2_transform(raw, S.wi, wo, ti, to);
             const uint32_t x[8] = {pack2(ti[0], ti[1]), pack2(ti[2], ti[3]), pack2(ti[4], ti[5]),
@@ -836,6 +853,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
               for (int j = 0; j < 6; ++j) { o[j] = ti[j]; o[6 + j] = to[j]; }
               o[12] = kappa.x;
               o[13] = kappa.y;
+            }
             }
           } else {
             // sample+pdf: sampler layer 1 D -> layer 2

@@ -90,21 +90,32 @@ __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mat
 // material from warp-aggregated SHARED atomics, ONE global atomic per
 // material per CTA reserves the chunk's contiguous range of each segment
 // (one global atomic per distinct id per warp — 5 x 65k atomics on 5
-// counters for C4 — serialised at L2: 115 us per 2.07M queries), and the
-// chunk is permuted through SMEM so every segment range is written with
-// coalesced stores.  Ids outside [0, n_mats) are skipped (bin_count_kernel
-// flags them).
-constexpr int kScatterItems = 4;
+// counters for C4 — serialised at L2: 115 us per 2.07M queries).  The
+// chunk's inputs are staged into SMEM in input order with coalesced 16-byte
+// loads (every array of a chunk is one contiguous range), and written out in
+// segment order — position p of the chunk's sorted order reads its source
+// row from SMEM — so every segment range is written with coalesced stores.
+// Ids outside [0, n_mats) are skipped (bin_count_kernel flags them).
+constexpr int kScatterItems = 2;  // 512 rows: 18..32 KB SMEM, full occupancy
 constexpr int kScatterRows = 256 * kScatterItems;
-struct ScatterSmem {
-  float uv[2 * kScatterRows];
-  float lod[kScatterRows];
-  float urr[kScatterRows];
-  float wi[3 * kScatterRows];
-  float wo[3 * kScatterRows];
-  float u3[3 * kScatterRows];
-  int32_t row[kScatterRows];
-};
+// SMEM of one chunk: uv[2R] urr[R] src[R] wi[3R] | lod[R] | wo[3R] | u3[3R]
+// (the optional arrays only when present)
+__host__ __device__ constexpr size_t scatter_smem_bytes(bool lod_arr, bool has_wo, bool has_u3) {
+  return (size_t)kScatterRows * 4 * (7 + (lod_arr ? 1 : 0) + (has_wo ? 3 : 0) + (has_u3 ? 3 : 0));
+}
+
+// count floats from src into SMEM dst with 16-byte loads when both ends allow
+__device__ __forceinline__ void stage_floats(float* dst, const float* __restrict__ src, int count) {
+  if ((((uintptr_t)src) & 15u) == 0 && (count & 3) == 0) {
+    const float4* s4 = reinterpret_cast<const float4*>(src);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < count / 4; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  } else {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = __ldg(src + i);
+  }
+}
+
 __global__ void __launch_bounds__(256) bin_scatter_kernel(
     int64_t n, int32_t n_mats, const int32_t* __restrict__ mat_id, const int32_t* __restrict__ counts,
     int32_t* __restrict__ seg, int32_t* __restrict__ cursor,
@@ -113,8 +124,21 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     const float* __restrict__ wo, const float* __restrict__ u3, float* __restrict__ p_uv,
     float* __restrict__ p_lod, float* __restrict__ p_urr, float* __restrict__ p_wi, float* __restrict__ p_wo,
     float* __restrict__ p_u3) {
-  extern __shared__ __align__(16) uint8_t sm_raw[];
-  ScatterSmem& S = *reinterpret_cast<ScatterSmem*>(sm_raw);
+  extern __shared__ __align__(16) float sm_f[];
+  struct {
+    float *uv, *urr, *wi, *lod, *wo, *u3;
+    int32_t* src;
+  } S;
+  {
+    float* q = sm_f;
+    S.uv = q; q += 2 * kScatterRows;
+    S.urr = q; q += kScatterRows;
+    S.src = reinterpret_cast<int32_t*>(q); q += kScatterRows;
+    S.wi = q; q += 3 * kScatterRows;
+    S.lod = q; if (lod_stride) q += kScatterRows;
+    S.wo = q; if (wo) q += 3 * kScatterRows;
+    S.u3 = q;
+  }
   __shared__ int32_t cnt[kMaxMats], loc[kMaxMats + 1], base[kMaxMats], off[kMaxMats];
   for (int i = threadIdx.x; i < n_mats; i += blockDim.x) cnt[i] = 0;
   if (threadIdx.x == 0) {
@@ -132,14 +156,26 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
       acc += (c + 3) & ~3;
     }
   }
-  __syncthreads();
   const int64_t c0 = (int64_t)blockIdx.x * kScatterRows;
+  const int rows = (int)(n - c0 < kScatterRows ? n - c0 : kScatterRows);
   int mi[kScatterItems];
+#pragma unroll
+  for (int k = 0; k < kScatterItems; ++k) {
+    const int r = k * 256 + threadIdx.x;
+    mi[k] = r < rows ? __ldg(mat_id + c0 + r) : -1;
+  }
+  // the chunk's inputs, input order (in flight together with the ids)
+  stage_floats(S.uv, uv + 2 * c0, 2 * rows);
+  if (lod_stride) stage_floats(S.lod, lod + c0, rows);
+  stage_floats(S.urr, urr + c0, rows);
+  stage_floats(S.wi, wi + 3 * c0, 3 * rows);
+  if (wo) stage_floats(S.wo, wo + 3 * c0, 3 * rows);
+  if (u3) stage_floats(S.u3, u3 + 3 * c0, 3 * rows);
+  __syncthreads();
   int32_t rk[kScatterItems];
 #pragma unroll
   for (int k = 0; k < kScatterItems; ++k) {
-    const int64_t i = c0 + k * 256 + threadIdx.x;
-    int m = i < n ? __ldg(mat_id + i) : -1;
+    int m = mi[k];
     if (m >= n_mats) m = -1;
     mi[k] = m;
     rk[k] = 0;
@@ -165,25 +201,9 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
   for (int i = threadIdx.x; i < n_mats; i += blockDim.x)
     base[i] = off[i] + (cnt[i] ? atomicAdd(cursor + i, cnt[i]) : 0);
   __syncthreads();
-  // gather (coalesced reads) into chunk-local sorted order in SMEM
 #pragma unroll
-  for (int k = 0; k < kScatterItems; ++k) {
-    if (mi[k] < 0) continue;
-    const int64_t i = c0 + k * 256 + threadIdx.x;
-    const int p = loc[mi[k]] + rk[k];
-    const float2 u = __ldg(reinterpret_cast<const float2*>(uv) + i);
-    S.uv[2 * p] = u.x;
-    S.uv[2 * p + 1] = u.y;
-    S.lod[p] = __ldg(lod + (lod_stride ? i : 0));
-    S.urr[p] = __ldg(urr + i);
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      S.wi[3 * p + j] = __ldg(wi + 3 * i + j);
-      if (wo) S.wo[3 * p + j] = __ldg(wo + 3 * i + j);
-      if (u3) S.u3[3 * p + j] = __ldg(u3 + 3 * i + j);
-    }
-    S.row[p] = (int32_t)i;
-  }
+  for (int k = 0; k < kScatterItems; ++k)
+    if (mi[k] >= 0) S.src[loc[mi[k]] + rk[k]] = k * 256 + threadIdx.x;
   __syncthreads();
   // write each segment range contiguously: position p -> slot base[m] + p - loc[m]
   const int tot = loc[n_mats];
@@ -192,19 +212,24 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     while (p >= loc[m + 1]) ++m;  // n_mats <= 64, typically a handful
     return (int64_t)base[m] + (p - loc[m]);
   };
+  const float lod0 = lod_stride ? 0.f : __ldg(lod);
   for (int p = threadIdx.x; p < tot; p += blockDim.x) {
     const int64_t sl = slot_of(p);
-    order[sl] = S.row[p];
-    p_lod[sl] = S.lod[p];
-    p_urr[sl] = S.urr[p];
-    reinterpret_cast<float2*>(p_uv)[sl] = make_float2(S.uv[2 * p], S.uv[2 * p + 1]);
-  }
-  for (int f = threadIdx.x; f < 3 * tot; f += blockDim.x) {
-    const int p = f / 3, j = f - 3 * p;
-    const int64_t sl = slot_of(p);
-    p_wi[3 * sl + j] = S.wi[f];
-    if (wo) p_wo[3 * sl + j] = S.wo[f];
-    if (u3) p_u3[3 * sl + j] = S.u3[f];
+    const int r = S.src[p];
+    order[sl] = (int32_t)(c0 + r);
+    p_lod[sl] = lod_stride ? S.lod[r] : lod0;
+    p_urr[sl] = S.urr[r];
+    reinterpret_cast<float2*>(p_uv)[sl] = make_float2(S.uv[2 * r], S.uv[2 * r + 1]);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) p_wi[3 * sl + j] = S.wi[3 * r + j];
+    if (wo) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) p_wo[3 * sl + j] = S.wo[3 * r + j];
+    }
+    if (u3) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) p_u3[3 * sl + j] = S.u3[3 * r + j];
+    }
   }
 }
 
@@ -338,8 +363,9 @@ cudaError_t multi_binned(const MatParams* const* mps, int32_t n_mats, int mode, 
     const int nb = grid256(a.n), cap = 4 * num_sms_multi();
     bin_count_kernel<<<nb < cap ? nb : cap, 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
   }
-  if (max_dynamic_smem((const void*)bin_scatter_kernel) < (int)sizeof(ScatterSmem)) return cudaErrorInvalidValue;
-  bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sizeof(ScatterSmem), s>>>(
+  const size_t sm_bytes = scatter_smem_bytes(a.lod_stride != 0, a.wo != nullptr, a.u3 != nullptr);
+  if (max_dynamic_smem((const void*)bin_scatter_kernel) < (int)sm_bytes) return cudaErrorInvalidValue;
+  bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sm_bytes, s>>>(
       a.n, n_mats, mat_id, w.counts, w.seg, w.cursor, w.order, a.uv, a.lod, a.lod_stride, a.u_rr, a.wi,
       a.wo, a.u3, w.uv, w.lod, w.urr, w.wi, w.wo, w.u3);
   g_launches += 2;

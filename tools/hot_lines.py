@@ -14,21 +14,47 @@ import sys
 import tempfile
 
 
+# NMQ_HL_OUTER=<file>: attribute inlined code to its call site when the
+# innermost line is not in <file> (one inlining level, nvdisasm -gi)
+OUTER = os.environ.get("NMQ_HL_OUTER")
+
+
+def _short(loc):
+    loc = re.sub(r'^"/root/repo/paper_2305_02678_b200/csrc/', "", loc).replace('", line ', ":")
+    return re.sub(r'^".*/include/', "", loc)
+
+
 def line_table(lib, key):
+    """SASS offset -> source line.  With OUTER set, nvdisasm -gi prints the
+    inlining chain (innermost first); the innermost frame matching OUTER is
+    used, suffixed with its nearest nmq_fast.cu caller."""
     tmp = tempfile.mkdtemp()
     subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
     table = {}
     for f in os.listdir(tmp):
-        dis = subprocess.run(["nvdisasm", "-g", os.path.join(tmp, f)], capture_output=True, text=True).stdout
-        fn, loc = None, None
+        dis = subprocess.run(["nvdisasm", "-gi" if OUTER else "-g", os.path.join(tmp, f)],
+                             capture_output=True, text=True).stdout
+        fn, loc, chain, fresh = None, None, [], False
         for l in dis.split("\n"):
             m = re.match(r"\s*\.text\.(\S+):", l)
             if m:
                 fn = m.group(1)
             if "//## File" in l:
-                loc = l.split("//## File")[1].strip()
-                loc = re.sub(r'^"/root/repo/paper_2305_02678_b200/csrc/', "", loc).replace('", line ', ":")
-                loc = re.sub(r'^".*/include/', "", loc)
+                if not fresh:
+                    chain, fresh = [], True
+                chain.append(_short(l.split("//## File")[1].strip().split(" inlined at ")[0]))
+                continue
+            if fresh:
+                fresh = False
+                if OUTER:
+                    hit = [i for i, c in enumerate(chain) if re.search(OUTER, c)]
+                    i = hit[0] if hit else len(chain) - 1
+                    loc = chain[i]
+                    up = [c for c in chain[i + 1:] if c.startswith("nmq_fast.cu") and c != loc]
+                    if up and not loc.startswith("nmq_fast.cu"):
+                        loc += " < " + up[0]
+                else:
+                    loc = chain[-1]
             m = re.match(r"\s*/\*([0-9a-f]{4,})\*/", l)
             if m and fn and key in fn:
                 table[int(m.group(1), 16)] = loc
