@@ -634,7 +634,8 @@ def run_kl(args):
         }))
 
 
-def measure(args, lib, h, workload, sets, steps, warmup, stream, world, local, clocks=None):
+def measure(args, lib, h, workload, sets, steps, warmup, stream, world, local, clocks=None, tag=None,
+            kernel=None):
     """Device-timed throughput of one workload: `steps` back-to-back launches
     of the C-ABI call with inputs resident in HBM (rotating over `sets`),
     CUDA events on the launching stream, max over ranks.  Returns a dict."""
@@ -673,7 +674,7 @@ def measure(args, lib, h, workload, sets, steps, warmup, stream, world, local, c
     kernel_s = ms / steps / 1e3
     ach = bpq * n / kernel_s / 1e9
     traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{workload}.json")
+    tp = os.path.join(ROOT, "profiles", f"traffic_{tag or workload}.json")  # ncu capture of THIS kernel
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
     return {
@@ -684,7 +685,7 @@ def measure(args, lib, h, workload, sets, steps, warmup, stream, world, local, c
                      "texel_bytes_per_query": texel_b,
                      "tensor_tflops_achieved": fpq * n / kernel_s / 1e12,
                      "tensor_frac": fpq * n / kernel_s / 1e12 / tflops,
-                     "kernel": "fast_kernel<%s> (csrc/nmq_fast.cu; exact-rounding resolve in its epilogue)" % {
+                     "kernel": kernel or "fast_kernel<%s> (csrc/nmq_fast.cu; exact-rounding resolve in its epilogue)" % {
                          "c2": "kModeEval", "c3": "kModeSamplePdf", "full": "kModeQuery"}[workload]},
     }
 
@@ -765,7 +766,7 @@ def run_ours(args):
         mat1, q1 = c1_case()
         h1 = mat1.device_material(device)
         t1 = [{k: torch.from_numpy(v).to(device) for k, v in q1.items()}]
-        c1 = measure(args, lib, h1, "full", t1, max(50, args.steps // 2), 5, stream, world, local)
+        c1 = measure(args, lib, h1, "full", t1, max(50, args.steps // 2), 5, stream, world, local, tag="c1")
         c1["config"] = "C1: 512^2 pyramid, 65,536 full queries (inputs fit L2)"
         subs["c1_full_query"] = c1
         # the reference's default fp16=False path: fp32 master weights and pyramid
@@ -778,7 +779,9 @@ def run_ours(args):
             m32 = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), np.random.default_rng(0))
             m32.latent = LatentPyramid(lv)
             h32 = m32.device_material(device, precise=True)
-            f32 = measure(args, lib, h32, "c2", sets[:1], max(10, args.steps // 20), 3, stream, world, local)
+            f32 = measure(args, lib, h32, "c2", sets[:1], max(10, args.steps // 20), 3, stream, world, local,
+                          tag="fp32_path", kernel="fused_kernel<kModeEval> (csrc/nmq_kernels.cu, generic "
+                          "tcgen05 kernel, 3 products per layer on hi/lo pairs)")
             f32["config"] = ("fp16=False (the reference default): fp32 master weights as fp16 hi/lo pairs, "
                              "fp32 4096^2 pyramid, 1920x1080 eval, generic tcgen05 kernel")
             subs["fp32_path_eval"] = f32

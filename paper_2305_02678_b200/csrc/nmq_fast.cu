@@ -39,15 +39,18 @@
 // tensor-core frame layer and the fp32 frames here are within a small,
 // conditioning-scaled bound of those values; a row whose fast value lies
 // within that bound of an fp16 rounding midpoint is queued (input row, fp16
-// latent code, fast fp16 inputs) in a per-CTA region of a global queue.  A
-// follow-up kernel (resolve_kernel, same stream, programmatic dependent
-// launch) recomputes each queued row's inputs in the reference's own
-// arithmetic (frame_raw_seq + frame_tw64); where an fp16 value differs, the
-// warp re-evaluates the BRDF decoder for that row on the CUDA cores (fp32)
-// and overwrites its output.  Nothing of it sits in the pipelined loop: a
-// call there constrains its register allocation (the prefetched texels
-// spill) and an SMEM ring takes the L1 the coarse pyramid levels live in
-// (both measured: -40 % / -8 % on C2).
+// latent code, fast fp16 inputs) in a per-CTA region of a global queue.
+// After its last tile each CTA resolves its own entries (resolve_entries, in
+// the kernel's epilogue; NMQ_RESOLVE_FUSED=0 runs resolve_kernel as a
+// follow-up launch instead, measured slower): it recomputes each queued
+// row's inputs in the reference's own arithmetic (frame_raw_seq +
+// frame_tw64); where an fp16 value differs, the warp re-evaluates the BRDF
+// decoder for that row on the CUDA cores (fp32) and overwrites its output.
+// Nothing of it sits in the pipelined loop: a call there constrains its
+// register allocation (the prefetched texels spill) and an SMEM ring takes
+// the L1 the coarse pyramid levels live in (both measured: -40 % / -8 % on
+// C2).  NMQ_TW_INLINE=1 computes every row's inputs in float64 inline
+// instead (no queue): measured equal on C2 (22.3 G q/s either way).
 #include <cstdio>
 #include <cmath>
 #include <cstdlib>

@@ -11,6 +11,8 @@ Tolerances (stated in DESIGN.md §5, from the north star / SURVEY §8c4):
     direction) rel max <= 1e-2, mean <= 1e-3.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -47,6 +49,8 @@ def check_rel(a, b, max_tol=1e-2, mean_tol=1e-3, what=""):
         f"{what}: {int(np.count_nonzero(r > max_tol))} values above {max_tol}; max rel {r.max():.3e} at "
         f"{i}: got {np.ravel(a)[i]!r} want {np.ravel(b)[i]!r}, mean {r.mean():.2e}")
     assert r.mean() <= mean_tol, f"{what}: mean rel {r.mean():.3e}"
+    if os.environ.get("NMQ_PARITY_REPORT"):  # -s: the measured margins (profiles/r02_parity_report.txt)
+        print(f"\nPARITY {what}: n {r.size} max rel {r.max():.3e} mean rel {r.mean():.3e}")
     return r
 
 
@@ -75,6 +79,8 @@ def check_dirs(ws, ws_ref, u3, p_ref, wi, tol=1e-3, band=1e-3):
     assert bad.size == 0, (f"{bad.size} directions off, worst {dw[bad].max():.3e} at {bad[0]}: "
                            f"diffuse={diff[bad[0]]} |g|={glen[bad[0]]:.3e} u={u3[bad[0]]} "
                            f"got {ws[bad[0]]} want {ws_ref[bad[0]]}")
+    if os.environ.get("NMQ_PARITY_REPORT"):
+        print(f"\nPARITY directions: n {int(ok.sum())} max |dw| {dw[ok].max():.3e}")
     return int(np.count_nonzero(band_rows & (dw > tol)))
 
 

@@ -22,6 +22,14 @@ neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=True)
 neural.sample_pdf(mat, uv, lod, urr, wi, u3)
 neural.query(mat, uv, lod, urr, wi, wo, u3)
 neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=False)
+# float64 coordinates (nm_fetch_f64 / nm_query_f64), trilinear, in-kernel spp mean
+uv64 = rng.random((n, 2)); lod64 = rng.random(n) * 5; urr64 = rng.random(n)
+neural.eval_material(mat, uv64, lod64, wi, wo, urr64, fp16=True)
+neural.sample_pdf(mat, uv64, lod64, urr64, wi, u3)
+neural.query(mat, uv64, lod64, urr64, wi, wo, u3)
+mat.latent.fetch(uv64, lod64, urr64)
+mat.latent.fetch_trilinear(uv, lod)
+neural.eval_material_spp(mat, uv[:1024], lod[:1024], wi[:1024], wo[:1024], urr[:1024], 16)
 z, _ = mat.latent.fetch(uv, lod, urr)
 neural.eval_brdf(mat, z, wi, wo, fp16=True)
 neural.infer_proxy(mat, z, wi, fp16=True)
@@ -30,6 +38,9 @@ mats[1].latent = LatentPyramid(O.random_pyramid(rng, 32, 32).levels)
 ids = rng.integers(0, 2, n).astype(np.int32)
 for mode in ("binned", "binned_async", "divergent"):
     neural.eval_material_multi(mats, ids, uv, lod, wi, wo, urr, mode=mode)
+for mode in ("binned", "binned_async"):
+    neural.sample_pdf_multi(mats, ids, uv, lod, urr, wi, u3, mode=mode)
+    neural.query_multi(mats, ids, uv, lod, urr, wi, wo, u3, mode=mode)
 render.cone_level(rng.random(n).astype(np.float32), rng.random(n).astype(np.float32),
                   rng.random(n).astype(np.float32), rng.random(n).astype(np.float32), 100.0, 6)
 net = mlp.Mlp.create((20, 32, 32, 3), rng)
@@ -59,7 +70,7 @@ rgb_pg = np.empty((n, 3), np.float32)
 for src, dst in ((pin, rgb_pin.data_ptr()), ({"uv": uv, "lod": lod, "urr": urr, "wi": wi, "wo": wo}, rgb_pg.ctypes.data)):
     ptr = {k: (v.data_ptr() if isinstance(v, torch.Tensor) else v.ctypes.data) for k, v in src.items()}
     _lib.check(lib.nm_eval_host(h.ptr, n, ptr["uv"], ptr["lod"], 1, ptr["urr"], ptr["wi"], ptr["wo"], dst,
-                                256, _io.stream_ptr(h.device)))
+                                None, None, 256, _io.stream_ptr(h.device)))
 assert np.array_equal(rgb_pin.numpy(), rgb_pg)
 torch.cuda.synchronize()
 print("sanitize_run ok")
