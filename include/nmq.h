@@ -136,13 +136,16 @@ int nm_fetch(const nm_material* mat, int64_t n, const float* uv, const float* lo
  * (latent.py:59-82 computes in float64; render.py:369 passes float64): level
  * pick, taps and weights exactly as numpy does them, so levels / taps / z stay
  * bit-exact for any float64 input (the fp32 entry points are exact for
- * fp32-representable inputs).  Directions stay fp32.  Runs on the generic
- * kernels. */
+ * fp32-representable inputs).  nm_query_f64 also takes the directions in
+ * float64 (wi, wo (n,3); wo unused by NM_QUERY_SAMPLE_PDF): the decoder's
+ * T.wi / T.wo are formed from them in float64 as the reference does
+ * (neural.py:280-287); the sampler input and the proxy use them narrowed to
+ * fp32 (neural.py:358 `astype(np.float32)`).  Runs on the generic kernels. */
 int nm_fetch_f64(const nm_material* m, int64_t n, const double* uv, const double* lod, int32_t lod_stride,
                  const double* u_rr, float* z_out, int32_t* level_out, int32_t* taps_out, float* wts_out,
                  void* stream);
 int nm_query_f64(const nm_material* m, int32_t mode, int64_t n, const double* uv, const double* lod,
-                 int32_t lod_stride, const double* u_rr, const float* wi, const float* wo, const float* u3,
+                 int32_t lod_stride, const double* u_rr, const double* wi, const double* wo, const float* u3,
                  float* rgb_out, float* albedo_out, float* ws_out, float* pdf_out, float* params9_out,
                  int32_t* level_out, void* stream);
 /* Eval reduced to the per-pixel sample mean in the kernel epilogue (the
@@ -166,6 +169,19 @@ int nm_eval(const nm_material* mat, int64_t n, const float* uv, const float* lod
 /* --- eval_brdf (neural.py:273-300), fp16 path, from given latent codes -- */
 int nm_eval_z(const nm_material* mat, int64_t n, const float* z, const float* wi,
               const float* wo, float* rgb_out, float* albedo_out, void* stream);
+/* eval_brdf on the reference's float64 directions (render.py passes float64;
+ * T.wi / T.wo formed from them in float64, neural.py:280-287). */
+int nm_eval_z_f64(const nm_material* m, int64_t n, const float* z, const double* wi, const double* wo,
+                  float* rgb_out, float* albedo_out, void* stream);
+/* Check hook for the exact-rounding contract: the BRDF decoder's direction
+ * inputs exactly as the reference rounds them (neural.py:282-287: frames
+ * from the frame layer's fp32 outputs, T.wi / T.wo in float64 with numpy's
+ * operation order, then fp32, then fp16).  x16_out (n, 12) fp16 bit patterns
+ * [T.wi (3 per frame), T.wo (3 per frame)] (one frame: 6 values, then 0).
+ * z (n, 8) fp32 holding fp16 values; directions fp32 (wi, wo) or float64
+ * (wi64, wo64; then wi / wo may be NULL).  fp16 materials with frames. */
+int nm_decoder_inputs(const nm_material* m, int64_t n, const float* z, const float* wi, const float* wo,
+                      const double* wi64, const double* wo64, uint16_t* x16_out, void* stream);
 
 /* --- infer_proxy (neural.py:353-362) + proxy_from_raw (:317-331) -------- */
 int nm_infer_proxy(const nm_material* mat, int64_t n, const float* z, const float* wi,

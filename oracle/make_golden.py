@@ -234,7 +234,7 @@ def make_train_case(name="train", seed=41):
     print(name)
 
 
-def make_vertex_case(name="vertex", n=3000, seed=51):
+def make_vertex_case(name="vertex", n=3000, seed=51, f64=False):
     """The renderer's per-vertex shading context (render.py:340-420,
     SURVEY §8 f2) on a two-material scene: material "alpha" (2x32) bound
     fp16, "beta" (2x16) bound fp32, objects [beta, alpha, beta]; records
@@ -266,10 +266,12 @@ def make_vertex_case(name="vertex", n=3000, seed=51):
     scene = SimpleNamespace(objects=objects, materials=materials)
     q = np.random.default_rng(seed + 2)
     obj = q.integers(0, 3, n)
-    uv = _f32(q.uniform(-0.5, 1.5, (n, 2)))
-    level = _f32(q.random(n) * 5.0).astype(np.float64)
+    uv = q.uniform(-0.5, 1.5, (n, 2))
+    level = q.random(n) * 5.0
     wi, wo = geom.sample_half_diff(q, n)
-    wi, wo = _f32(wi).astype(np.float64), _f32(wo).astype(np.float64)
+    if not f64:  # fp32-representable inputs (the original case); f64: the renderer's own values
+        uv, level = _f32(uv), _f32(level).astype(np.float64)
+        wi, wo = _f32(wi).astype(np.float64), _f32(wo).astype(np.float64)
     hits = SimpleNamespace(obj=obj, uv=uv.astype(np.float64))
     out = {}
     for tag, cfg in (("lod", render.RenderConfig(lod=True)),
@@ -318,6 +320,61 @@ def make_kl_case(name="kl", b=2048, seed=61):
     print(name)
 
 
+def make_vertex_f64_case():
+    make_vertex_case("vertex_f64", f64=True)
+
+
+def make_f64_case(name="f64_inputs", n=4096, seed=71):
+    """The reference on genuinely float64 inputs (what its renderer passes,
+    render.py:369): uv / level / u_rr / wi / wo not representable in fp32, a
+    non-power-of-two pyramid.  Records eval_material's f and levels, and the
+    BRDF decoder's fp16 direction inputs (neural.py:282-287:
+    inp.astype(float32) -> fp16 in fused_forward) for the material's own
+    frames and for two hand-set frame layers (all rows on the degenerate
+    fallback tangent; a tangent 1e-8 from the normal)."""
+    geom, latent, neural, proxy = _ref()
+    cfg = neural.NeuralMaterialConfig()
+    mat = neural.NeuralMaterial.create(cfg, np.random.default_rng(seed))
+    lrng = np.random.default_rng(seed + 1)
+    pyr = latent.LatentPyramid.zeros(40, 24)
+    for lvl in pyr.levels:
+        lvl[:] = lrng.standard_normal(lvl.shape).astype(np.float32)
+    mat.latent = pyr
+    q = np.random.default_rng(seed + 2)
+    uv = -1.0 + 3.0 * q.random((n, 2))
+    lod = q.random(n) * (pyr.n_levels - 1)
+    u_rr = q.random(n)
+    wi, wo = geom.sample_half_diff(q, n)
+    assert not np.array_equal(wi.astype(np.float32).astype(np.float64), wi)
+    f, _, chosen = neural.eval_material(mat, uv, lod, wi, wo, u_rr, fp16=True)
+    z, chosen2 = mat.half()["latent"].fetch(uv, lod, u_rr)
+    assert np.array_equal(chosen, chosen2)
+
+    def dec_inputs(m):
+        raw = m.half()["frame"].fused_forward(np.atleast_2d(z).astype(np.float32))
+        fr = neural.frames_from_raw(raw)
+        x = np.concatenate([fr.transform(wi), fr.transform(wo)], axis=-1)
+        return x.astype(np.float32).astype(np.float16).view(np.uint16)
+
+    d = dict(config=np.array(json.dumps(cfg.to_json())), uv=uv, lod=lod, u_rr=u_rr, wi=wi, wo=wo,
+             z=z, chosen=chosen, f=f, x16=dec_inputs(mat))
+    from neuralmat import mlp as rmlp
+    for tag, bias in (("degen", [0.0, 0.0, 1.0, 0.0, 0.0, 1.0] * 2),
+                      ("near", [0.0, 0.0, 1.0, 1.0, 0.0, 0.0, 0.0, 0.0, 1.0, 1e-8, 0.0, 1.0])):
+        m2 = neural.NeuralMaterial.create(cfg, np.random.default_rng(seed))
+        m2.frame_layer = rmlp.Mlp([rmlp.Layer(np.zeros((12, 8), np.float32), np.asarray(bias, np.float32),
+                                              "linear")])
+        d[f"x16_{tag}"] = dec_inputs(m2)
+        d[f"bias_{tag}"] = np.asarray(bias, np.float32)
+    for i, l in enumerate(pyr.levels):
+        d[f"lat{i}"] = l
+    _nets("frame", mat.frame_layer, d)
+    _nets("brdf", mat.brdf_decoder, d)
+    _nets("sampler", mat.sampler_decoder, d)
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
+    print(name, {k: v.shape for k, v in d.items() if hasattr(v, "shape") and v.ndim})
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     make_case("c1_2x32", {}, n=4096, taps=True, fp32_path=True)
@@ -333,8 +390,15 @@ def main():
     make_lod_case()
     make_train_case()
     make_vertex_case()
+    make_vertex_f64_case()
     make_kl_case()
+    make_f64_case()
 
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1:  # regenerate only the named cases, e.g. make_f64_case
+        os.makedirs(OUT, exist_ok=True)
+        for fn in sys.argv[1:]:
+            globals()[fn]()
+    else:
+        main()

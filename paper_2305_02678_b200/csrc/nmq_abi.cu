@@ -563,7 +563,7 @@ int nm_fetch_f64(const nm_material* m, int64_t n, const double* uv, const double
 }
 
 int nm_query_f64(const nm_material* m, int32_t mode, int64_t n, const double* uv, const double* lod,
-                 int32_t lod_stride, const double* u_rr, const float* wi, const float* wo, const float* u3,
+                 int32_t lod_stride, const double* u_rr, const double* wi, const double* wo, const float* u3,
                  float* rgb_out, float* albedo_out, float* ws_out, float* pdf_out, float* params9_out,
                  int32_t* level_out, void* stream) {
   if (!m) return fail(NM_ERR_INVALID, "null material");
@@ -578,8 +578,8 @@ int nm_query_f64(const nm_material* m, int32_t mode, int64_t n, const double* uv
   if (samp && !m->mp.has_sampler) return fail(NM_ERR_INVALID, "material has no sampler decoder");
   QueryArgs a{};
   a.n = n; a.uv64 = uv; a.lod64 = lod; a.lod_stride = lod_stride ? 1 : 0; a.urr64 = u_rr;
-  a.wi = wi; a.wo = wo; a.u3 = u3; a.rgb = rgb_out; a.albedo = albedo_out; a.ws = ws_out; a.pdf = pdf_out;
-  a.params9 = params9_out; a.level = level_out;
+  a.wi64 = wi; a.wo64 = brdf ? wo : nullptr; a.u3 = u3; a.rgb = rgb_out; a.albedo = albedo_out; a.ws = ws_out;
+  a.pdf = pdf_out; a.params9 = params9_out; a.level = level_out;
   DeviceGuard guard(m->device);
   const int kmode = mode == NM_QUERY_EVAL ? kModeEval : (mode == NM_QUERY_SAMPLE_PDF ? kModeSamplePdf : kModeQuery);
   return finish(m, launch_fused(m->mp, kmode, a, (cudaStream_t)stream), "nm_query_f64");
@@ -781,6 +781,31 @@ int nm_eval_z(const nm_material* m, int64_t n, const float* z, const float* wi, 
   DeviceGuard guard(m->device);
   if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
   return finish(m, launch_fused(m->mp, kModeEvalZ, a, (cudaStream_t)stream), "nm_eval_z");
+}
+
+int nm_eval_z_f64(const nm_material* m, int64_t n, const float* z, const double* wi, const double* wo,
+                  float* rgb_out, float* albedo_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!z || !wi || !wo || !rgb_out) return fail(NM_ERR_INVALID, "null input");
+  QueryArgs a{};
+  a.n = n; a.z = z; a.wi64 = wi; a.wo64 = wo; a.rgb = rgb_out; a.albedo = albedo_out;
+  DeviceGuard guard(m->device);
+  if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  return finish(m, launch_fused(m->mp, kModeEvalZ, a, (cudaStream_t)stream), "nm_eval_z_f64");
+}
+
+int nm_decoder_inputs(const nm_material* m, int64_t n, const float* z, const float* wi, const float* wo,
+                      const double* wi64, const double* wo64, uint16_t* x16_out, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!z || !x16_out || !((wi && wo) || (wi64 && wo64))) return fail(NM_ERR_INVALID, "null input");
+  if (!m->mp.use_frames || m->mp.precise) return fail(NM_ERR_INVALID, "needs an fp16 material with learned frames");
+  DeviceGuard guard(m->device);
+  return finish(m, launch_decoder_inputs(m->mp, n, z, wi64 ? nullptr : wi, wo, wi64, wo64, (uint32_t*)x16_out,
+                                         (cudaStream_t)stream), "nm_decoder_inputs");
 }
 
 int nm_infer_proxy(const nm_material* m, int64_t n, const float* z, const float* wi,

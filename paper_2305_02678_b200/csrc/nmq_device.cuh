@@ -593,52 +593,51 @@ __device__ __forceinline__ void frame_raw_seq(const MatParams& m, const uint32_t
 struct D3 {
   double x, y, z;
 };
-// 1/sqrt(x) for normal x > 0 to ~1 ulp: the hardware approximation refined by
-// two Newton steps (no library call; only a 1e-16 relative error matters here)
-__device__ __forceinline__ double drsqrt(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = 0.5 * x;
-  y = y * fma(-h * y, y, 1.5);
-  y = y * fma(-h * y, y, 1.5);
-  return y;
+__device__ __forceinline__ D3 d3(V3 v) { return {v.x, v.y, v.z}; }
+// numpy's float64 operations, operation for operation (every product and sum
+// rounded separately — the _rn intrinsics are never contracted into DFMA):
+//   np.sum(a * b, axis=-1) over 3 values: (p0 + p1) + p2
+//   np.linalg.norm(v, axis=-1) = sqrt(add.reduce(v * v))
+//   np.cross(a, b)[0] = a1*b2 - a2*b1, [1] = a2*b0 - a0*b2, [2] = a0*b1 - a1*b0
+//   v / s: IEEE division
+__device__ __forceinline__ double np_dot(D3 a, D3 b) {
+  return __dadd_rn(__dadd_rn(__dmul_rn(a.x, b.x), __dmul_rn(a.y, b.y)), __dmul_rn(a.z, b.z));
 }
-__device__ __forceinline__ double ddot(D3 a, D3 b) { return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x)); }
-__device__ __forceinline__ D3 dcross(D3 a, D3 b) {
-  return {fma(a.y, b.z, -a.z * b.y), fma(a.z, b.x, -a.x * b.z), fma(a.x, b.y, -a.y * b.x)};
+__device__ __forceinline__ double np_norm(D3 v) { return __dsqrt_rn(np_dot(v, v)); }
+__device__ __forceinline__ D3 np_cross(D3 a, D3 b) {
+  return {__dsub_rn(__dmul_rn(a.y, b.z), __dmul_rn(a.z, b.y)), __dsub_rn(__dmul_rn(a.z, b.x), __dmul_rn(a.x, b.z)),
+          __dsub_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x))};
 }
-__device__ __forceinline__ D3 dscale(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ D3 np_div(D3 v, double s) { return {__ddiv_rn(v.x, s), __ddiv_rn(v.y, s), __ddiv_rn(v.z, s)}; }
 
-// One learned frame in float64 (neural.py:207-233, geom.py:82-89) and the
-// transform of wi / wo (neural.py:185-196), rounded to fp32 as the
-// reference's `inp.astype(np.float32)` does (neural.py:287).  The float64
-// arithmetic differs from numpy's by ~1e-16 relative, far below the fp32
-// rounding that follows.
-__device__ __forceinline__ void frame_tw64(const float* raw, V3 wi, V3 wo, float (&ti)[3], float (&to)[3]) {
+// One learned frame in float64 and the transform of wi / wo, bit for bit as
+// numpy computes them (frames_from_raw, neural.py:207-233; fallback_tangent,
+// geom.py:82-89; FrameSet.transform, neural.py:185-196), rounded to fp32 as
+// the reference's `inp.astype(np.float32)` does (neural.py:287).
+__device__ __forceinline__ void frame_tw64(const float* raw, D3 di, D3 dout, float (&ti)[3], float (&to)[3]) {
   const D3 rn = {raw[0], raw[1], raw[2]};
   D3 rt = {raw[3], raw[4], raw[5]};
-  const D3 n = dscale(rn, drsqrt(fmax(ddot(rn, rn), 1e-24)));
-  D3 c = dcross(n, rt);
-  double c2 = ddot(c, c);
-  if (c2 < 1e-16) {  // |c| < 1e-8: fallback tangent n x e_argmin|n| (first index on ties)
+  const D3 n = np_div(rn, fmax(np_norm(rn), 1e-12));
+  D3 c = np_cross(n, rt);
+  double c_len = np_norm(c);
+  if (c_len < 1e-8) {  // degenerate: tangent n x e, e the axis of the smallest |n_k| (first on ties)
     const double ax = fabs(n.x), ay = fabs(n.y), az = fabs(n.z);
     const D3 e = (ax <= ay && ax <= az) ? D3{1.0, 0.0, 0.0} : (ay <= az ? D3{0.0, 1.0, 0.0} : D3{0.0, 0.0, 1.0});
-    const D3 f = dcross(n, e);
-    rt = dscale(f, drsqrt(ddot(f, f)));
-    c = dcross(n, rt);
-    c2 = ddot(c, c);
+    const D3 f = np_cross(n, e);
+    rt = np_div(f, np_norm(f));
+    c = np_cross(n, rt);
+    c_len = np_norm(c);
   }
-  const D3 b = dscale(c, drsqrt(fmax(c2, 1e-24)));
-  const D3 t = dcross(b, n);
-  const D3 di = {wi.x, wi.y, wi.z}, dout = {wo.x, wo.y, wo.z};
-  ti[0] = (float)ddot(t, di); ti[1] = (float)ddot(b, di); ti[2] = (float)ddot(n, di);
-  to[0] = (float)ddot(t, dout); to[1] = (float)ddot(b, dout); to[2] = (float)ddot(n, dout);
+  const D3 b = np_div(c, fmax(c_len, 1e-12));
+  const D3 t = np_cross(b, n);
+  ti[0] = (float)np_dot(t, di); ti[1] = (float)np_dot(b, di); ti[2] = (float)np_dot(n, di);
+  to[0] = (float)np_dot(t, dout); to[1] = (float)np_dot(b, dout); to[2] = (float)np_dot(n, dout);
 }
 
 // The decoder's direction inputs, exactly as the reference rounds them:
 // x16 = fp16 pairs of [T.wi (3 per frame), T.wo (3 per frame)] for n_frames
 // frames, from the latent code's fp16 pairs.
-__device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
+__device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh)[4], D3 wi, D3 wo,
                                          uint32_t (&x16)[6], uint32_t frames = 3u) {
   float raw[12];
   frame_raw_seq(m, zh, raw);
@@ -665,6 +664,10 @@ __device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh
     x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], to[0]); x16[2] = pack_h2(to[1], to[2]);
     x16[3] = x16[4] = x16[5] = 0u;
   }
+}
+__device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
+                                         uint32_t (&x16)[6], uint32_t frames = 3u) {
+  tw_exact(m, zh, d3(wi), d3(wo), x16, frames);
 }
 
 // fp16 halves of the 2-frame decoder direction words that belong to frame 0

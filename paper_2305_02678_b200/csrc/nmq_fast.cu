@@ -1164,7 +1164,7 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 // Returns cudaErrorNotSupported when the fast path does not apply (caller
 // then uses the generic kernel).
 cudaError_t launch_fast(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s) {
-  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx || a.uv64) return cudaErrorNotSupported;
+  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx || a.uv64 || a.wi64) return cudaErrorNotSupported;
   if (mode != kModeEval && mode != kModeSamplePdf && mode != kModeQuery)
     return cudaErrorNotSupported;
   if (!aligned16(a.uv) || !aligned16(a.u_rr) || !aligned16(a.wi) ||

@@ -98,6 +98,8 @@ struct QueryArgs {
   const float* z;
   const float* wi;
   const float* wo;
+  const double* wi64;   // optional float64 directions (generic kernels; wi / wo then unused)
+  const double* wo64;
   const float* u3;
   const int32_t* idx;   // optional indirection (generic kernel): query = idx[i]
   const int32_t* out_idx;  // optional output rows: results of row i go to row out_idx[i]
@@ -130,6 +132,10 @@ constexpr double kLeakyScale = 1.0 + 0.98019802570343017578;
 // launchers (nmq_kernels.cu); return cudaError_t of the launch
 cudaError_t launch_fused(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s,
                          int groups_override = 0);
+// the decoder's fp16 direction inputs in the reference's arithmetic (tw_exact), one row per thread
+cudaError_t launch_decoder_inputs(const MatParams& mp, int64_t n, const float* z, const float* wi,
+                                  const float* wo, const double* wi64, const double* wo64, uint32_t* x16,
+                                  cudaStream_t s);
 cudaError_t launch_fetch(const MatParams& mp, const QueryArgs& a, cudaStream_t s);
 cudaError_t launch_sample(int64_t n, const float* p9, const float* wi, const float* u3,
                           float* wo, cudaStream_t s);

@@ -194,8 +194,10 @@ __device__ __forceinline__ void load_z(const float* z, int64_t q, float (&out)[8
 }
 
 // BRDF decode of one query given z; returns raw decoder outputs in y.
+// d64: the query's float64 directions [wi, wo] when the caller passed them
+// (warp-uniform), else null — the reference transforms its float64 arrays.
 __device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const float (&z)[8],
-                                            V3 wi, V3 wo, float (&y)[16]) {
+                                            V3 wi, V3 wo, float (&y)[16], const D3* d64 = nullptr) {
   float x[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) x[k] = 0.f;
@@ -208,7 +210,10 @@ __device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const
     uint32_t zh[4], x16[6];
 #pragma unroll
     for (int c = 0; c < 4; ++c) zh[c] = pack_h2(z[2 * c], z[2 * c + 1]);
-    tw_exact(mp, zh, wi, wo, x16);
+    if (d64)
+      tw_exact(mp, zh, d64[0], d64[1], x16);
+    else
+      tw_exact(mp, zh, wi, wo, x16);
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       const float2 f = unpack_h2(x16[c]);
@@ -342,6 +347,20 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
     const int64_t oq = valid ? (a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + i) : q) : 0;  // output row
 
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
+    D3 d64[2] = {{0.0, 0.0, 1.0}, {0.0, 0.0, 1.0}};  // float64 directions (a.wi64)
+    auto load_dirs = [&](bool with_wo) {
+      if (a.wi64) {  // narrowed copies for the fp32 consumers (sampler input, proxy)
+        d64[0] = {__ldg(a.wi64 + 3 * q), __ldg(a.wi64 + 3 * q + 1), __ldg(a.wi64 + 3 * q + 2)};
+        wi = v3((float)d64[0].x, (float)d64[0].y, (float)d64[0].z);
+        if (with_wo) {
+          d64[1] = {__ldg(a.wo64 + 3 * q), __ldg(a.wo64 + 3 * q + 1), __ldg(a.wo64 + 3 * q + 2)};
+          wo = v3((float)d64[1].x, (float)d64[1].y, (float)d64[1].z);
+        }
+      } else {
+        wi = ldg3(a.wi, q);
+        if (with_wo) wo = ldg3(a.wo, q);
+      }
+    };
     float z[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) z[k] = 0.f;
@@ -349,8 +368,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
     if constexpr (MODE == kModeEvalZ || MODE == kModeProxyZ) {
       if (valid) {
         load_z(a.z, q, z);
-        wi = ldg3(a.wi, q);
-        if constexpr (MODE == kModeEvalZ) wo = ldg3(a.wo, q);
+        load_dirs(MODE == kModeEvalZ);
       }
     } else {
       if (a.uv64) {  // float64 coordinates, as the reference computes them
@@ -360,8 +378,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
           v = __ldg(a.uv64 + 2 * q + 1);
           lod = __ldg(a.lod64 + (a.lod_stride ? q : 0));
           urr = __ldg(a.urr64 + q);
-          wi = ldg3(a.wi, q);
-          if constexpr (MODE != kModeSamplePdf) wo = ldg3(a.wo, q);
+          load_dirs(MODE != kModeSamplePdf);
         }
         const int level = choose_level(mp, lod, urr);
         fetch_exact(mp, level, u, v, make_taps(mp, level, u, v), z);
@@ -374,8 +391,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
           v = uv.y;
           lod = __ldg(a.lod + (a.lod_stride ? q : 0));
           urr = __ldg(a.u_rr + q);
-          wi = ldg3(a.wi, q);
-          if constexpr (MODE != kModeSamplePdf) wo = ldg3(a.wo, q);
+          load_dirs(MODE != kModeSamplePdf);
         }
         const int level = choose_level(mp, lod, urr);
         const Taps t = make_taps(mp, level, u, v);
@@ -386,13 +402,13 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
 
     if constexpr (MODE == kModeEval || MODE == kModeEvalZ || MODE == kModeQuery) {
       float y[16];
-      brdf_decode(mp, g, z, wi, wo, y);
+      brdf_decode(mp, g, z, wi, wo, y, a.wi64 ? d64 : nullptr);
+      // horizon mask on the caller's values (a float64 z below 2^-149 narrows to 0)
+      const bool up = a.wi64 ? (d64[0].z > 0.0 && d64[1].z > 0.0) : (wi.z > 0.f && wo.z > 0.f);
       if (MODE == kModeEval && a.img) {  // per-pixel spp mean (warp-collective)
-        const bool up = (wi.z > 0.f) && (wo.z > 0.f);
         const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
         spp_accumulate(a.img, i, f, valid, a.spp_log2);
       } else if (valid) {
-        const bool up = (wi.z > 0.f) && (wo.z > 0.f);
         const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2]))
                         : v3(0.f, 0.f, 0.f);
         stg3(a.rgb, oq, f);
@@ -507,6 +523,20 @@ divergent_eval_kernel(const MatParams* __restrict__ mps_g, int32_t n_mats,
     const bool valid = m0 >= 0 && m0 < n_mats;  // out-of-range ids are skipped
     const int m = valid ? m0 : -1;
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
+    D3 d64[2] = {{0.0, 0.0, 1.0}, {0.0, 0.0, 1.0}};  // float64 directions (a.wi64)
+    auto load_dirs = [&](bool with_wo) {
+      if (a.wi64) {  // narrowed copies for the fp32 consumers (sampler input, proxy)
+        d64[0] = {__ldg(a.wi64 + 3 * q), __ldg(a.wi64 + 3 * q + 1), __ldg(a.wi64 + 3 * q + 2)};
+        wi = v3((float)d64[0].x, (float)d64[0].y, (float)d64[0].z);
+        if (with_wo) {
+          d64[1] = {__ldg(a.wo64 + 3 * q), __ldg(a.wo64 + 3 * q + 1), __ldg(a.wo64 + 3 * q + 2)};
+          wo = v3((float)d64[1].x, (float)d64[1].y, (float)d64[1].z);
+        }
+      } else {
+        wi = ldg3(a.wi, q);
+        if (with_wo) wo = ldg3(a.wo, q);
+      }
+    };
     float z[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) z[k] = 0.f;
@@ -702,6 +732,31 @@ cudaError_t launch_mode(const MatParams& mp, const QueryArgs& a, cudaStream_t s,
   return cudaGetLastError();
 }
 
+// The decoder's fp16 direction inputs, one row per thread, in the
+// reference's arithmetic (the check hook behind nm_decoder_inputs).
+__global__ void __launch_bounds__(256) decoder_inputs_kernel(const __grid_constant__ MatParams mp, int64_t n,
+                                                             const float* __restrict__ z,
+                                                             const float* __restrict__ wi,
+                                                             const float* __restrict__ wo,
+                                                             const double* __restrict__ wi64,
+                                                             const double* __restrict__ wo64,
+                                                             uint32_t* __restrict__ x16) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    float zz[8];
+    load_z(z, i, zz);
+    uint32_t zh[4], x[6];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) zh[c] = pack_h2(zz[2 * c], zz[2 * c + 1]);
+    if (wi64)
+      tw_exact(mp, zh, D3{wi64[3 * i], wi64[3 * i + 1], wi64[3 * i + 2]},
+               D3{wo64[3 * i], wo64[3 * i + 1], wo64[3 * i + 2]}, x);
+    else
+      tw_exact(mp, zh, ldg3(wi, i), ldg3(wo, i), x);
+#pragma unroll
+    for (int c = 0; c < 6; ++c) x16[6 * i + c] = x[c];
+  }
+}
+
 }  // namespace
 
 int smem_bytes_for(const MatParams& mp) { return (int)((mp.wblob_bytes + 127) / 128 * 128); }
@@ -771,6 +826,16 @@ cudaError_t launch_pdf(int64_t n, const float* p9, const float* wi, const float*
                        cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   pdf_kernel<<<grid_for(n, 256), 256, 0, s>>>(n, p9, wi, wo, pdf);
+  ++g_launches;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_decoder_inputs(const MatParams& mp, int64_t n, const float* z, const float* wi,
+                                  const float* wo, const double* wi64, const double* wo64, uint32_t* x16,
+                                  cudaStream_t s) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  decoder_inputs_kernel<<<(unsigned)blocks, 256, 0, s>>>(mp, n, z, wi, wo, wi64, wo64, x16);
   ++g_launches;
   return cudaGetLastError();
 }

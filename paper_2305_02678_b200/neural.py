@@ -232,15 +232,19 @@ def eval_brdf(mat, z, wi, wo, fp16=False):
     dev = h.device
     z_t = _io.as_rows(z, LATENT_CHANNELS, dev, "z")
     n = z_t.shape[0]
-    wi_t = _io.as_rows(wi, 3, dev, "wi")
-    wo_t = _io.as_rows(wo, 3, dev, "wo")
+    # float64 directions fp32 cannot hold exactly stay float64: the reference
+    # forms T.wi / T.wo from its float64 arrays (neural.py:280-287)
+    d64 = _io.inexact_f64(wi) or _io.inexact_f64(wo)
+    rows = _io.as_rows64 if d64 else _io.as_rows
+    wi_t = rows(wi, 3, dev, "wi")
+    wo_t = rows(wo, 3, dev, "wo")
     if wi_t.shape[0] != n or wo_t.shape[0] != n:
         raise ValueError("z, wi and wo must share the batch size")
     f = _io.empty(n, 3, dev)
     alb = _io.empty(n, 3, dev) if mat.cfg.albedo_head else None
     lib = _lib.load()
-    _launch(lib.nm_eval_z, h.ptr, n, z_t.data_ptr(), wi_t.data_ptr(), wo_t.data_ptr(),
-            f.data_ptr(), _io.ptr(alb), _io.stream_ptr(dev))
+    _launch(lib.nm_eval_z_f64 if d64 else lib.nm_eval_z, h.ptr, n, z_t.data_ptr(), wi_t.data_ptr(),
+            wo_t.data_ptr(), f.data_ptr(), _io.ptr(alb), _io.stream_ptr(dev))
     return _io.out(f, np_mode), (None if alb is None else _io.out(alb, np_mode))
 
 
@@ -249,8 +253,10 @@ class _QueryInputs:
         self.np_mode = _io.is_numpy_like(uv)
         self.h = mat.device_material(None if self.np_mode else uv.device, precise=not fp16)
         dev = self.dev = self.h.device
-        # float64 coordinates fp32 cannot hold exactly keep float64 (nm_query_f64)
-        self.f64 = any(_io.inexact_f64(x) for x in (uv, level, u_rr))
+        # float64 coordinates or directions fp32 cannot hold exactly keep
+        # float64 (nm_query_f64: levels / taps / T.w as the reference forms them)
+        self.f64 = any(_io.inexact_f64(x) for x in (uv, level, u_rr)) or \
+            any(_io.inexact_f64(dirs[k]) for k in need if k in ("wi", "wo"))
         if self.f64:
             self.uv = _io.as_rows64(uv, 2, dev, "uv")
             n = self.n = self.uv.shape[0]
@@ -262,7 +268,7 @@ class _QueryInputs:
             self.lod, self.lod_stride = _io.as_vec(level, n, dev, "level")
             self.urr, _ = _io.as_vec(u_rr, n, dev, "u_rr")
         for k in need:
-            t = _io.as_rows(dirs[k], 3, dev, k)
+            t = (_io.as_rows64 if self.f64 and k in ("wi", "wo") else _io.as_rows)(dirs[k], 3, dev, k)
             if t.shape[0] != n:
                 raise ValueError(f"{k}: batch {t.shape[0]} != {n}")
             setattr(self, k, t)
@@ -278,8 +284,8 @@ def _host_eval(mat, uv, level, wi, wo, u_rr, out, return_level):
     n = np.shape(uv)[0] if np.ndim(uv) == 2 else 0
     if n == 0:
         return None
-    if any(_io.inexact_f64(x) for x in (uv, level, u_rr)):
-        return None  # float64 coordinates: the device path's nm_query_f64
+    if any(_io.inexact_f64(x) for x in (uv, level, u_rr, wi, wo)):
+        return None  # float64 coordinates / directions: the device path's nm_query_f64
     h_uv, h_wi, h_wo = _io.host_rows(uv, 2, "uv"), _io.host_rows(wi, 3, "wi"), _io.host_rows(wo, 3, "wo")
     h_lod = np.ascontiguousarray(np.asarray(level, dtype=np.float32)).reshape(-1)
     h_urr = np.ascontiguousarray(np.asarray(u_rr, dtype=np.float32)).reshape(-1)
@@ -341,8 +347,8 @@ def eval_material_spp(mat, uv, level, wi, wo, u_rr, spp, fp16=True, out=None):
     rows are pixel * spp + s; returns the (B / spp, 3) image (fp32 tensor for
     torch callers, float64 numpy otherwise)."""
     _require_fp16(fp16)
-    for x, name in ((uv, "uv"), (level, "level"), (u_rr, "u_rr")):
-        _io.check_exact_f32(x, name)
+    for x, name in ((uv, "uv"), (level, "level"), (u_rr, "u_rr"), (wi, "wi"), (wo, "wo")):
+        _io.check_exact_f32(x, name)  # no float64 spp entry point
     q = _QueryInputs(mat, uv, level, u_rr, ("wi", "wo"), fp16=fp16, wi=wi, wo=wo)
     if spp <= 0 or spp & (spp - 1) or q.n % spp:
         raise ValueError("spp must be a power of two dividing the batch")
@@ -478,7 +484,7 @@ def _multi_inputs(mats, mat_id, uv, level, u_rr, dirs):
     n = uv_t.shape[0]
     lod_t, lod_stride = _io.as_vec(level, n, dev, "level", exact=True)
     urr_t, _ = _io.as_vec(u_rr, n, dev, "u_rr", exact=True)
-    d = {k: _io.as_rows(v, 3, dev, k) for k, v in dirs.items()}
+    d = {k: _io.as_rows(v, 3, dev, k, exact=k in ("wi", "wo")) for k, v in dirs.items()}
     if isinstance(mat_id, torch.Tensor):
         ids = mat_id.to(device=dev, dtype=torch.int32).reshape(-1).contiguous()
     else:

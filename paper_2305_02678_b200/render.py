@@ -110,12 +110,18 @@ class VertexShading:
         self.np_mode = _io.is_numpy_like(wo_local)
         self.dev = _io.cuda_device(None if self.np_mode else wo_local.device)
         self.wo = _io.as_rows(wo_local, 3, self.dev, "wo_local")
+        # numpy callers pass float64 (the reference renderer does): levels, taps
+        # and T.wo are formed from the float64 values (nm_fetch_f64, eval_brdf's
+        # float64 route); the fp32 copy feeds the sampler and proxy as the
+        # reference narrows them (neural.py:358)
+        self.wo64 = _io.as_rows64(wo_local, 3, self.dev, "wo_local") if self.np_mode else None
         self.n = self.wo.shape[0]
         obj = np.asarray(hits.obj if _io.is_numpy_like(hits.obj) else hits.obj.cpu().numpy())
         names = [scene.objects[int(i)].material for i in obj]
         if len(names) != self.n:
             raise ValueError("hits and wo_local must share the batch size")
-        uv = _io.as_rows(hits.uv, 2, self.dev, "uv")
+        uv = (_io.as_rows64 if self.np_mode else _io.as_rows)(hits.uv, 2, self.dev, "uv")
+        ftype = torch.float64 if self.np_mode else torch.float32
         lv_all = None
         if cfg.lod and cfg.force_level is None:
             lv_all = level if isinstance(level, torch.Tensor) else np.asarray(level, np.float64)
@@ -132,39 +138,42 @@ class VertexShading:
             ns = sel.size
             idx = torch.from_numpy(sel).to(self.dev)
             if cfg.force_level is not None:
-                lod = torch.full((ns,), float(cfg.force_level), device=self.dev)
+                lod = torch.full((ns,), float(cfg.force_level), device=self.dev, dtype=ftype)
             elif lv_all is None:
-                lod = torch.zeros((ns,), device=self.dev)
+                lod = torch.zeros((ns,), device=self.dev, dtype=ftype)
             elif isinstance(lv_all, torch.Tensor):
-                lod = lv_all.to(self.dev, torch.float32).reshape(-1)[idx].contiguous()
+                lod = lv_all.to(self.dev, ftype).reshape(-1)[idx].contiguous()
             else:
-                lod = torch.from_numpy(lv_all.reshape(-1)[sel].astype(np.float32)).to(self.dev)
+                lod = torch.from_numpy(lv_all.reshape(-1)[sel].astype(np.float64)).to(self.dev, ftype)
             fp16 = bool(cfg.fp16 or binding.fp16)
             mat = binding.mat
             h = mat.device_material(self.dev, precise=not fp16)
-            u_rr = torch.from_numpy(np.asarray(rng.random(ns), np.float32)).to(self.dev)
+            u_rr = torch.from_numpy(np.asarray(rng.random(ns), np.float64)).to(self.dev, ftype)
             uv_g = uv[idx].contiguous()
             z = torch.empty((ns, neural.LATENT_CHANNELS), device=self.dev)
             chosen = torch.empty((ns,), device=self.dev, dtype=torch.int32)
             if ns:
-                _lib.check(lib.nm_fetch(h.ptr, ns, uv_g.data_ptr(), lod.data_ptr(), 1, u_rr.data_ptr(),
-                                        z.data_ptr(), chosen.data_ptr(), None, None, stream), "nm_fetch")
+                fetch = lib.nm_fetch_f64 if self.np_mode else lib.nm_fetch
+                _lib.check(fetch(h.ptr, ns, uv_g.data_ptr(), lod.data_ptr(), 1, u_rr.data_ptr(),
+                                 z.data_ptr(), chosen.data_ptr(), None, None, stream), "nm_fetch")
             wo_g = self.wo[idx].contiguous()
             pp = neural.infer_proxy(mat, z, wo_g, fp16=fp16) if ns else None
-            self.groups.append((binding, idx, fp16, z, pp, wo_g))
+            wo_e = self.wo64[idx].contiguous() if self.wo64 is not None else wo_g  # for eval
+            self.groups.append((binding, idx, fp16, z, pp, wo_g, wo_e))
 
     def _result(self, t):
         return _io.out(t, self.np_mode)
 
     def eval(self, wi_local):
         """BRDF values at (wi_local, wo_local) per vertex (render.py:377-389)."""
-        wi = _io.as_rows(wi_local, 3, self.dev, "wi_local")
+        rows = _io.as_rows64 if self.np_mode else _io.as_rows
+        wi = rows(wi_local, 3, self.dev, "wi_local")
         if wi.shape[0] != self.n:
             raise ValueError("wi_local must have one row per vertex")
         out = torch.zeros((self.n, 3), device=self.dev)
-        for binding, idx, fp16, z, _, wo_g in self.groups:
+        for binding, idx, fp16, z, _, _, wo_e in self.groups:
             if idx.numel():
-                f, _ = neural.eval_brdf(binding.mat, z, wi[idx].contiguous(), wo_g, fp16=fp16)
+                f, _ = neural.eval_brdf(binding.mat, z, wi[idx].contiguous(), wo_e, fp16=fp16)
                 out[idx] = f
         return self._result(out)
 
@@ -173,7 +182,7 @@ class VertexShading:
         the reference's order, and their mixture pdf (render.py:391-409)."""
         wi = torch.zeros((self.n, 3), device=self.dev)
         pdf = torch.zeros((self.n,), device=self.dev)
-        for _, idx, _, _, pp, wo_g in self.groups:
+        for _, idx, _, _, pp, wo_g, _ in self.groups:
             ns = idx.numel()
             u = torch.from_numpy(np.asarray(rng.random((ns, 3)), np.float32)).to(self.dev)
             if not ns:
@@ -193,7 +202,7 @@ class VertexShading:
         if wi.shape[0] != self.n:
             raise ValueError("wi_local must have one row per vertex")
         out = torch.zeros((self.n,), device=self.dev)
-        for _, idx, _, _, pp, wo_g in self.groups:
+        for _, idx, _, _, pp, wo_g, _ in self.groups:
             if idx.numel():
                 out[idx] = proxy.pdf(pp, wo_g, wi[idx].contiguous()).reshape(-1)
         return self._result(out)

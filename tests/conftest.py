@@ -33,7 +33,8 @@ def pytest_collection_modifyitems(config, items):
             it.add_marker(skip)
 
 
-def golden_cases(pattern="*.npz", exclude=("proxy_kat", "lod", "train", "vertex", "kl")):
+def golden_cases(pattern="*.npz", exclude=("proxy_kat", "lod", "train", "vertex", "vertex_f64", "kl",
+                                            "f64_inputs")):
     names = sorted(os.path.splitext(os.path.basename(p))[0]
                    for p in glob.glob(os.path.join(GOLDEN, pattern)))
     return [n for n in names if n not in exclude]

@@ -1,0 +1,105 @@
+"""The reference's own float64 inputs (its renderer passes float64 uv,
+level, u_rr and directions, render.py:369) and the exact fp16 rounding of
+the BRDF decoder's direction inputs (neural.py:282-287).
+
+Goldens: tests/golden/f64_inputs.npz and vertex_f64.npz, written by the
+reference itself (oracle/make_golden.py make_f64_case / make_vertex_f64_case).
+The decoder inputs are compared as fp16 bit patterns: bit-exact.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from test_gpu_parity import _oracle_from, check_rel, our_material
+from test_oracle_golden import oracle_decoder_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+def _decoder_inputs(mat, z, wi, wo):
+    """nm_decoder_inputs: (n, 12) uint16 fp16 bit patterns; float64 numpy
+    directions go in as float64, fp32 ones as fp32."""
+    from paper_2305_02678_b200 import _io, _lib
+    lib = _lib.load()
+    h = mat.device_material(None)
+    dev = h.device
+    n = z.shape[0]
+    z_t = torch.from_numpy(np.ascontiguousarray(z, np.float32)).to(dev)
+    out = torch.empty((n, 12), dtype=torch.int16, device=dev)
+    if np.asarray(wi).dtype == np.float64:
+        wi_t = torch.from_numpy(np.ascontiguousarray(wi)).to(dev)
+        wo_t = torch.from_numpy(np.ascontiguousarray(wo)).to(dev)
+        args = (None, None, wi_t.data_ptr(), wo_t.data_ptr())
+    else:
+        wi_t = torch.from_numpy(np.ascontiguousarray(wi, np.float32)).to(dev)
+        wo_t = torch.from_numpy(np.ascontiguousarray(wo, np.float32)).to(dev)
+        args = (wi_t.data_ptr(), wo_t.data_ptr(), None, None)
+    _lib.check(lib.nm_decoder_inputs(h.ptr, n, z_t.data_ptr(), *args, out.data_ptr(), _io.stream_ptr(dev)))
+    return out.cpu().numpy().view(np.uint16)
+
+
+def _with_frame_bias(g, bias):
+    from paper_2305_02678_b200 import mlp
+    mat = our_material(g)
+    mat.frame_layer = mlp.Mlp([mlp.Layer(np.zeros((12, 8), np.float32), np.asarray(bias, np.float32),
+                                         mlp.ACT_LINEAR)])
+    return mat
+
+
+def test_decoder_inputs_bit_exact_vs_reference_golden():
+    """The reference's own fp16 decoder inputs on float64 directions: the
+    material's frames, the degenerate fallback tangent on every row, a
+    tangent 1e-8 from the normal."""
+    g = load_golden("f64_inputs")
+    assert np.array_equal(_decoder_inputs(our_material(g), g["z"], g["wi"], g["wo"]), g["x16"])
+    for tag in ("degen", "near"):
+        mat = _with_frame_bias(g, g[f"bias_{tag}"])
+        assert np.array_equal(_decoder_inputs(mat, g["z"], g["wi"], g["wo"]), g[f"x16_{tag}"]), tag
+
+
+@pytest.mark.parametrize("f64", [False, True])
+def test_decoder_inputs_bit_exact_at_scale(f64):
+    """524,288 rows (random fp16 codes, half/difference direction pairs in
+    float64 or fp32) against the oracle's numpy frames (pinned bit-exactly
+    to the reference above): every fp16 bit pattern equal."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    rng = np.random.default_rng(81 + int(f64))
+    from paper_2305_02678_b200.latent import LatentPyramid
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 8, 8).levels)  # unused by this entry point
+    n = 1 << 19
+    z = rng.standard_normal((n, 8)).astype(np.float16).astype(np.float32)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    if not f64:
+        wi, wo = wi.astype(np.float32), wo.astype(np.float32)
+    om = _oracle_from(mat)
+    ref = oracle_decoder_inputs(om, z, np.asarray(wi, np.float64), np.asarray(wo, np.float64))
+    got = _decoder_inputs(mat, z, wi, wo)
+    bad = np.flatnonzero(np.any(got != ref, axis=1))
+    assert bad.size == 0, f"{bad.size} rows differ, first {bad[0]}: {got[bad[0]]} vs {ref[bad[0]]}"
+    if f64:  # the float64 route is not vacuous: narrowing the directions first changes rows
+        narrowed = _decoder_inputs(mat, z, wi.astype(np.float32), wo.astype(np.float32))
+        assert np.any(narrowed != ref)
+
+
+def test_eval_material_float64_inputs_vs_reference_golden():
+    """eval_material on the reference's float64 arrays: levels bit-exact,
+    colours strict (every value <= 1e-2 rel, mean <= 1e-3)."""
+    from paper_2305_02678_b200 import neural
+    g = load_golden("f64_inputs")
+    mat = our_material(g)
+    f, _, ch = neural.eval_material(mat, g["uv"], g["lod"], g["wi"], g["wo"], g["u_rr"], fp16=True)
+    assert ch.dtype == np.int64 and np.array_equal(ch, g["chosen"])
+    check_rel(f, g["f"], what="float64 eval_material")
+    z, ch2 = mat.half()["latent"].fetch(g["uv"], g["lod"], g["u_rr"])
+    assert np.array_equal(ch2, g["chosen"]) and np.array_equal(z, g["z"])
+    # eval_brdf from the codes on the float64 directions (nm_eval_z_f64)
+    f2, _ = neural.eval_brdf(mat, g["z"], g["wi"], g["wo"], fp16=True)
+    check_rel(f2, g["f"], what="float64 eval_brdf")
+    # the full query's eval part on the same float64 inputs (nm_query_f64)
+    u3 = np.random.default_rng(3).random((g["uv"].shape[0], 3))
+    f3, _, _ = neural.query(mat, g["uv"], g["lod"], g["u_rr"], g["wi"], g["wo"], u3)
+    check_rel(f3, g["f"], what="float64 query rgb")

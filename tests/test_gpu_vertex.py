@@ -46,11 +46,14 @@ def _scene(g):
     return SimpleNamespace(objects=objects, materials=materials)
 
 
+@pytest.mark.parametrize("golden", ["vertex", "vertex_f64"])
 @pytest.mark.parametrize("tag", sorted(CFGS))
-def test_vertex_shading_vs_reference(tag):
+def test_vertex_shading_vs_reference(tag, golden):
+    """vertex: fp32-representable inputs; vertex_f64: the renderer's own
+    float64 uv / level / directions / roulette numbers."""
     from paper_2305_02678_b200 import render
 
-    g = load_golden("vertex")
+    g = load_golden(golden)
     scene = _scene(g)
     cfg = SimpleNamespace(assert_pdf_consistency=True, **CFGS[tag])
     hits = SimpleNamespace(obj=g["obj"], uv=g["uv"])

@@ -208,3 +208,32 @@ def test_oracle_chi2_harness_matches_reference():
     ok_r, p_r, s_r, d_r = run(RC.chi_square_test)
     ok_o, p_o, s_o, d_o = run(O.chi_square_test)
     assert (ok_r, d_r) == (ok_o, d_o) and s_r == pytest.approx(s_o, rel=1e-12) and p_r == pytest.approx(p_o, rel=1e-9)
+
+
+def oracle_decoder_inputs(mat, z, wi, wo):
+    """The BRDF decoder's fp16 direction inputs as the reference forms them
+    (neural.py:282-287), from the oracle's frames: fp16 bit patterns."""
+    raw = mat.half()["frame"].forward(np.atleast_2d(z).astype(np.float32))
+    fr = O.frames_from_raw(raw)
+    x = np.concatenate([O.frame_transform(fr, wi), O.frame_transform(fr, wo)], axis=-1)
+    return x.astype(np.float32).astype(np.float16).view(np.uint16)
+
+
+def test_oracle_float64_inputs_bit_exact():
+    """Genuinely float64 uv / level / u_rr / wi / wo (the reference renderer's
+    dtype): levels and z bit-exact, the decoder's fp16 direction inputs
+    bit-exact (own frames, the degenerate fallback, a near-degenerate
+    tangent), colours to 1e-12."""
+    g = load_golden("f64_inputs")
+    mat = oracle_material(g)
+    f, _, chosen = O.eval_material(mat, g["uv"], g["lod"], g["wi"], g["wo"], g["u_rr"], fp16=True)
+    assert np.array_equal(chosen, g["chosen"])
+    np.testing.assert_allclose(f, g["f"], rtol=1e-12, atol=1e-12)
+    z, _ = mat.half()["latent"].fetch(g["uv"], g["lod"], g["u_rr"])
+    assert np.array_equal(z, g["z"])
+    assert np.array_equal(oracle_decoder_inputs(mat, z, g["wi"], g["wo"]), g["x16"])
+    for tag in ("degen", "near"):
+        m2 = oracle_material(g)
+        m2.frame = O.Net([(np.zeros((12, 8), np.float32), g[f"bias_{tag}"], "linear")])
+        m2._half = None
+        assert np.array_equal(oracle_decoder_inputs(m2, z, g["wi"], g["wo"]), g[f"x16_{tag}"]), tag
