@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from conftest import load_golden
-from test_gpu_parity import check_rel
+from test_gpu_parity import check_dirs, check_rel
 
 pytestmark = pytest.mark.gpu
 
@@ -46,6 +46,30 @@ def _scene(g):
     return SimpleNamespace(objects=objects, materials=materials)
 
 
+def _replay_u3_and_params(ctx, g, n):
+    """The (n, 3) uniforms ctx.sample drew per vertex (the constructor draws
+    rng.random(ns) per material group in sorted order, sample then
+    rng.random((ns, 3)) per group, render.py:352-409) and every vertex's
+    9-float proxy block."""
+    rng = np.random.default_rng(int(g["rng_seed"]))
+    for _, idx, *_ in ctx.groups:
+        rng.random(idx.numel())
+    u3 = np.zeros((n, 3))
+    p9 = np.zeros((n, 9))
+    for _, idx, _, _, pp, _, _ in ctx.groups:
+        rows = idx.cpu().numpy()
+        u3[rows] = rng.random((rows.size, 3))
+        if rows.size:
+            a = pp.as_array()
+            p9[rows] = a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+    return u3, p9
+
+
+def _oracle_proxy(p9):
+    from oracle import nm_oracle as O
+    return O.Proxy(p9[:, 0], p9[:, 1], p9[:, 2:4], p9[:, 4:6], p9[:, 6], p9[:, 7:9])
+
+
 @pytest.mark.parametrize("golden", ["vertex", "vertex_f64"])
 @pytest.mark.parametrize("tag", sorted(CFGS))
 def test_vertex_shading_vs_reference(tag, golden):
@@ -66,8 +90,12 @@ def test_vertex_shading_vs_reference(tag, golden):
     ws, pdf_s = ctx.sample(rng)  # same random stream as the reference
     ws_ref = g[f"{tag}_ws"]
     dw = np.abs(ws - ws_ref).max(axis=1)
-    # lobe-pick ties and ill-conditioned specular maps are rare
-    assert np.mean(dw > 1e-3) < 5e-3, (np.mean(dw > 1e-3), dw.max())
+    # every sampled direction within 1e-3 outside the lobe-pick guard band and
+    # where the sampling map is well conditioned (check_dirs, no outlier
+    # budget): replay the context's random stream for the per-vertex u and
+    # take each vertex's proxy from its group's cached parameters
+    u3, p9 = _replay_u3_and_params(ctx, g, len(ws))
+    check_dirs(ws, ws_ref, u3, _oracle_proxy(p9), g["wo"])
     # the specular pdf carries 1/|wo.h| (proxy.py:119-126): where the sampled
     # direction is nearly opposite the conditioning one, h = (wo+ws)/|wo+ws|
     # is ill-conditioned, so rows with |ws.h| < 1e-2 are excluded (as in
