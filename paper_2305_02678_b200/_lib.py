@@ -161,6 +161,8 @@ def load():
             "(the query path has no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("NMQ_LIB") and not hasattr(lib, name):
+            continue  # an experimental / older build (NMQ_LIB) may lack newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

@@ -634,6 +634,17 @@ __device__ __forceinline__ void frame_tw64(const float* raw, D3 di, D3 dout, flo
   to[0] = (float)np_dot(t, dout); to[1] = (float)np_dot(b, dout); to[2] = (float)np_dot(n, dout);
 }
 
+__device__ __forceinline__ void pack_tw(const MatParams& m, const float (&ti)[6], const float (&to)[6],
+                                        uint32_t (&x16)[6]) {
+  if (m.n_frames == 2) {
+    x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], ti[3]); x16[2] = pack_h2(ti[4], ti[5]);
+    x16[3] = pack_h2(to[0], to[1]); x16[4] = pack_h2(to[2], to[3]); x16[5] = pack_h2(to[4], to[5]);
+  } else {  // [T.wi(3), T.wo(3)]
+    x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], to[0]); x16[2] = pack_h2(to[1], to[2]);
+    x16[3] = x16[4] = x16[5] = 0u;
+  }
+}
+
 // The decoder's direction inputs, exactly as the reference rounds them:
 // x16 = fp16 pairs of [T.wi (3 per frame), T.wo (3 per frame)] for n_frames
 // frames, from the latent code's fp16 pairs.
@@ -657,17 +668,74 @@ __device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh
       for (int k = 0; k < 3; ++k) ti[3 * f + k] = to[3 * f + k] = 0.f;
     }
   }
-  if (m.n_frames == 2) {
-    x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], ti[3]); x16[2] = pack_h2(ti[4], ti[5]);
-    x16[3] = pack_h2(to[0], to[1]); x16[4] = pack_h2(to[2], to[3]); x16[5] = pack_h2(to[4], to[5]);
-  } else {  // [T.wi(3), T.wo(3)]
-    x16[0] = pack_h2(ti[0], ti[1]); x16[1] = pack_h2(ti[2], to[0]); x16[2] = pack_h2(to[1], to[2]);
-    x16[3] = x16[4] = x16[5] = 0u;
-  }
+  pack_tw(m, ti, to, x16);
 }
 __device__ __forceinline__ void tw_exact(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
                                          uint32_t (&x16)[6], uint32_t frames = 3u) {
   tw_exact(m, zh, d3(wi), d3(wo), x16, frames);
+}
+
+// ---- the fast kernel's resolve ------------------------------------------------
+// The same frame and transform in float64 by reciprocal square roots and
+// FMA-contracted products (the form the fast kernel's epilogue resolve
+// uses: numpy's IEEE divisions and square roots cost it 5 % of C2 through
+// register pressure in the shared kernel — measured).  Its float64 values
+// are within ~20 kappa ulp of numpy's (kappa = 1 + |r_t|_1 / |n x r_t|):
+// the fp16 result can differ from numpy's only when a value lies that close
+// to an fp32 rounding midpoint which also decides its fp16 rounding (~1e-13
+// per value); tests/test_gpu_scale.py checks whole C2 batches row by row.
+__device__ __forceinline__ double drsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+__device__ __forceinline__ double fdot(D3 a, D3 b) { return fma(a.z, b.z, fma(a.y, b.y, a.x * b.x)); }
+__device__ __forceinline__ D3 fcross(D3 a, D3 b) {
+  return {fma(a.y, b.z, -a.z * b.y), fma(a.z, b.x, -a.x * b.z), fma(a.x, b.y, -a.y * b.x)};
+}
+__device__ __forceinline__ D3 fscale(D3 a, double s) { return {a.x * s, a.y * s, a.z * s}; }
+__device__ __forceinline__ void frame_tw64_rsq(const float* raw, D3 di, D3 dout, float (&ti)[3], float (&to)[3]) {
+  const D3 rn = {raw[0], raw[1], raw[2]};
+  D3 rt = {raw[3], raw[4], raw[5]};
+  const D3 n = fscale(rn, drsqrt(fmax(fdot(rn, rn), 1e-24)));
+  D3 c = fcross(n, rt);
+  double c2 = fdot(c, c);
+  if (c2 < 1e-16) {  // |c| < 1e-8: fallback tangent n x e_argmin|n| (first index on ties)
+    const double ax = fabs(n.x), ay = fabs(n.y), az = fabs(n.z);
+    const D3 e = (ax <= ay && ax <= az) ? D3{1.0, 0.0, 0.0} : (ay <= az ? D3{0.0, 1.0, 0.0} : D3{0.0, 0.0, 1.0});
+    const D3 f = fcross(n, e);
+    rt = fscale(f, drsqrt(fdot(f, f)));
+    c = fcross(n, rt);
+    c2 = fdot(c, c);
+  }
+  const D3 b = fscale(c, drsqrt(fmax(c2, 1e-24)));
+  const D3 t = fcross(b, n);
+  ti[0] = (float)fdot(t, di); ti[1] = (float)fdot(b, di); ti[2] = (float)fdot(n, di);
+  to[0] = (float)fdot(t, dout); to[1] = (float)fdot(b, dout); to[2] = (float)fdot(n, dout);
+}
+__device__ __forceinline__ void tw_resolve(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
+                                           uint32_t (&x16)[6], uint32_t frames) {
+  float raw[12];
+  frame_raw_seq(m, zh, raw);
+  float ti[6], to[6];
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    if (f < m.n_frames && ((frames >> f) & 1u)) {
+      float a[3], b[3];
+      frame_tw64_rsq(raw + 6 * f, d3(wi), d3(wo), a, b);
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        ti[3 * f + k] = a[k];
+        to[3 * f + k] = b[k];
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) ti[3 * f + k] = to[3 * f + k] = 0.f;
+    }
+  }
+  pack_tw(m, ti, to, x16);
 }
 
 // fp16 halves of the 2-frame decoder direction words that belong to frame 0

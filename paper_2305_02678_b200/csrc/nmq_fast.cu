@@ -313,12 +313,15 @@ __device__ __forceinline__ void out_layer_simt(uint32_t dl, const MatParams& mp,
 }
 
 // Stage one tile's inputs into `ib`: TMA bulk copies for full tiles (issued
-// by one thread), direct per-row copies for the partial last tile.
-template <int MODE>
+// by one thread), direct per-row copies for the partial last tile and for
+// gathered rows (a.idx: binned multi-material segments read the caller's
+// arrays through the segment's row list instead of a permuted copy).  A
+// thread reads only its own row of `ib`, so per-row copies need no barrier.
+template <int MODE, bool GATHER>
 __device__ __forceinline__ void stage_inputs(const QueryArgs& a, int64_t base, int64_t n, int tile,
                                              InBuf<MODE>& ib, uint64_t* bar, int r, bool issuer) {
   const int64_t q0 = base + (int64_t)tile * kTile;
-  if ((int64_t)tile * kTile + kTile <= n) {
+  if ((!GATHER || !a.idx) && (int64_t)tile * kTile + kTile <= n) {
     if (issuer) {
       uint32_t bytes = kTile * (8 + 4 + 12);
       if (a.lod_stride) bytes += kTile * 4;
@@ -336,8 +339,23 @@ __device__ __forceinline__ void stage_inputs(const QueryArgs& a, int64_t base, i
     }
     return;
   }
-  const int64_t q = q0 + r;
   const bool v = (int64_t)tile * kTile + r < n;
+  if (GATHER && a.idx && v) {  // gathered row: asynchronous 4-byte copies, awaited in wait_in
+    const int64_t q = __ldg(a.idx + q0 + r);
+    tc::cp_async4(tc::smem_u32(&ib.uv[2 * r]), a.uv + 2 * q);
+    tc::cp_async4(tc::smem_u32(&ib.uv[2 * r + 1]), a.uv + 2 * q + 1);
+    if (a.lod_stride) tc::cp_async4(tc::smem_u32(&ib.lod[r]), a.lod + q);
+    tc::cp_async4(tc::smem_u32(&ib.urr[r]), a.u_rr + q);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      tc::cp_async4(tc::smem_u32(&ib.wi[3 * r + k]), a.wi + 3 * q + k);
+      if constexpr (Need<MODE>::wo) tc::cp_async4(tc::smem_u32(&ib.wo[3 * r + k]), a.wo + 3 * q + k);
+      if constexpr (Need<MODE>::u3) tc::cp_async4(tc::smem_u32(&ib.u3[3 * r + k]), a.u3 + 3 * q + k);
+    }
+    tc::cp_async_commit();
+    return;
+  }
+  const int64_t q = q0 + r;
   ib.uv[2 * r] = v ? a.uv[2 * q] : 0.f;
   ib.uv[2 * r + 1] = v ? a.uv[2 * q + 1] : 0.f;
   if (a.lod_stride) ib.lod[r] = v ? a.lod[q] : 0.f;
@@ -474,7 +492,7 @@ __device__ __forceinline__ void resolve_entries(const MatParams& mp, const Query
       // only frames with a value near a rounding midpoint need the float64 path
       // (warp-uniform choice: a per-lane one would serialize both paths anyway)
       const uint32_t fm = __reduce_or_sync(__activemask(), e4.y);
-      tw_exact(mp, zh, wi, wo, xe, fm);
+      tw_resolve(mp, zh, wi, wo, xe, fm);
       const uint32_t xf[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
@@ -683,7 +701,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
   const int64_t n_rows = SEG && a.seg ? (int64_t)__ldg(a.seg + 1) : a.n;
   const bool seg_out = SEG && a.out_idx;
   const int ntiles = (int)((n_rows + kTile - 1) / kTile);  // host guarantees < 2^31
-  const int last_full = (int)(n_rows / kTile);                // tiles [0, last_full) are full
+  const int last_full = SEG && a.idx ? 0 : (int)(n_rows / kTile);  // tiles [0, last_full) staged by TMA
   const int stride = gridDim.x * G;                        // between a group's tiles
   const int sstride = stride * NS;                         // between a slot's tiles
   const bool want_level = a.level != nullptr;
@@ -711,6 +729,8 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     if (tile < last_full) {
       tc::mbar_wait(&in_bar[gi][s][b], (S.ph_bits >> b) & 1u);
       S.ph_bits ^= 1u << b;
+    } else if (SEG && a.idx) {
+      tc::cp_async_wait<0>();  // this thread's gathered row (and any older copies)
     }
   };
   // First MMA of a tile: input chunk 0 = [z, wi, 1] -> frame layer (eval /
@@ -734,9 +754,9 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
     constexpr int s = decltype(sc)::value;
     SlotSt& S = sl[s];
     if (S.t < ntiles) {
-      stage_inputs<MODE>(a, seg_base, n_rows, S.t, buf(s, 0), &in_bar[gi][s][0], r, r == 64);
+      stage_inputs<MODE, SEG>(a, seg_base, n_rows, S.t, buf(s, 0), &in_bar[gi][s][0], r, r == 64);
       if (S.t + sstride < ntiles)
-        stage_inputs<MODE>(a, seg_base, n_rows, S.t + sstride, buf(s, 1), &in_bar[gi][s][1], r, r == 64);
+        stage_inputs<MODE, SEG>(a, seg_base, n_rows, S.t + sstride, buf(s, 1), &in_bar[gi][s][1], r, r == 64);
       wait_in(S, s, 0, S.t);
       TexPrefetch p0;
       prefetch_texels<MODE>(mp, a, buf(s, 0), r, lod0, p0);
@@ -784,9 +804,9 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
           auto refill = [&]() {  // after the barrier: every row of buffer b was read
             if (t2 < last_full) {
               if (r == 32 * ((LW + 2) % 4))
-                stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
+                stage_inputs<MODE, SEG>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, true);
             } else if (t2 < ntiles) {
-              stage_inputs<MODE>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, false);  // own row
+              stage_inputs<MODE, SEG>(a, seg_base, n_rows, t2, buf(s, b), &in_bar[gi][s][b], r, false);  // own row
             }
           };
           mma_wait(S.bar, S.ph);
@@ -802,7 +822,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             {
               (void)raw;
               uint32_t x6[6];
-              tw_exact(mp, S.zp, S.wi, wo, x6);
+              tw_resolve(mp, S.zp, S.wi, wo, x6, 3u);
               const uint32_t x[8] = {x6[0], x6[1], x6[2], x6[3], x6[4], x6[5], 0u, 0u};
               tc::tmem_st8(S.al + 8, x);
               if constexpr (RED) S.qslot = -1;
@@ -1082,7 +1102,7 @@ cudaError_t launch_fast_t(const MatParams& mp, const QueryArgs& a, cudaStream_t 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const bool seg = a.seg || a.out_idx;
+  const bool seg = a.seg || a.out_idx || a.idx;  // segment instantiation (gathers rows when a.idx)
   constexpr bool kBrdf = Need<MODE>::brdf;
   if (kBrdf && !seg && a.n > kChunkRows) {
     for (int64_t c0 = 0; c0 < a.n; c0 += kChunkRows) {
@@ -1164,7 +1184,7 @@ bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 // Returns cudaErrorNotSupported when the fast path does not apply (caller
 // then uses the generic kernel).
 cudaError_t launch_fast(const MatParams& mp, int mode, const QueryArgs& a, cudaStream_t s) {
-  if (mp.fast_arch < 0 || mp.texel_fp32 || a.idx || a.uv64 || a.wi64) return cudaErrorNotSupported;
+  if (mp.fast_arch < 0 || mp.texel_fp32 || a.uv64 || a.wi64) return cudaErrorNotSupported;
   if (mode != kModeEval && mode != kModeSamplePdf && mode != kModeQuery)
     return cudaErrorNotSupported;
   if (!aligned16(a.uv) || !aligned16(a.u_rr) || !aligned16(a.wi) ||

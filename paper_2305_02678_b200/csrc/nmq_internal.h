@@ -101,7 +101,8 @@ struct QueryArgs {
   const double* wi64;   // optional float64 directions (generic kernels; wi / wo then unused)
   const double* wo64;
   const float* u3;
-  const int32_t* idx;   // optional indirection (generic kernel): query = idx[i]
+  const int32_t* idx;   // optional input-row gather: row i of the launch reads query idx[i]
+                        // (i counted from the segment base, like out_idx)
   const int32_t* out_idx;  // optional output rows: results of row i go to row out_idx[i]
                            // (binned multi-material writes straight to query order)
   const int32_t* seg;      // optional device {base, count}: the launch covers input rows

@@ -343,7 +343,7 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
        tile += (int64_t)gridDim.x * G) {
     const int64_t i = tile * kTile + r;
     const bool valid = i < n_rows;
-    const int64_t q = valid ? (a.idx ? (int64_t)__ldg(a.idx + i) : seg_base + i) : 0;
+    const int64_t q = valid ? (a.idx ? (int64_t)__ldg(a.idx + seg_base + i) : seg_base + i) : 0;
     const int64_t oq = valid ? (a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + i) : q) : 0;  // output row
 
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);

@@ -98,10 +98,11 @@ __global__ void __launch_bounds__(256) bin_count_kernel(int64_t n, int32_t n_mat
 // Ids outside [0, n_mats) are skipped (bin_count_kernel flags them).
 constexpr int kScatterItems = 2;  // 512 rows: 18..32 KB SMEM, full occupancy
 constexpr int kScatterRows = 256 * kScatterItems;
-// SMEM of one chunk: uv[2R] urr[R] src[R] wi[3R] | lod[R] | wo[3R] | u3[3R]
-// (the optional arrays only when present)
-__host__ __device__ constexpr size_t scatter_smem_bytes(bool lod_arr, bool has_wo, bool has_u3) {
-  return (size_t)kScatterRows * 4 * (7 + (lod_arr ? 1 : 0) + (has_wo ? 3 : 0) + (has_u3 ? 3 : 0));
+// SMEM of one chunk: src[R] | uv[2R] urr[R] wi[3R] | lod[R] | wo[3R] | u3[3R]
+// (the optional arrays only when present; gather mode: src only)
+__host__ __device__ constexpr size_t scatter_smem_bytes(bool gather, bool lod_arr, bool has_wo, bool has_u3) {
+  return gather ? (size_t)kScatterRows * 4
+                : (size_t)kScatterRows * 4 * (7 + (lod_arr ? 1 : 0) + (has_wo ? 3 : 0) + (has_u3 ? 3 : 0));
 }
 
 // count floats from src into SMEM dst with 16-byte loads when both ends allow
@@ -131,9 +132,9 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
   } S;
   {
     float* q = sm_f;
+    S.src = reinterpret_cast<int32_t*>(q); q += kScatterRows;
     S.uv = q; q += 2 * kScatterRows;
     S.urr = q; q += kScatterRows;
-    S.src = reinterpret_cast<int32_t*>(q); q += kScatterRows;
     S.wi = q; q += 3 * kScatterRows;
     S.lod = q; if (lod_stride) q += kScatterRows;
     S.wo = q; if (wo) q += 3 * kScatterRows;
@@ -164,13 +165,15 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     const int r = k * 256 + threadIdx.x;
     mi[k] = r < rows ? __ldg(mat_id + c0 + r) : -1;
   }
-  // the chunk's inputs, input order (in flight together with the ids)
-  stage_floats(S.uv, uv + 2 * c0, 2 * rows);
-  if (lod_stride) stage_floats(S.lod, lod + c0, rows);
-  stage_floats(S.urr, urr + c0, rows);
-  stage_floats(S.wi, wi + 3 * c0, 3 * rows);
-  if (wo) stage_floats(S.wo, wo + 3 * c0, 3 * rows);
-  if (u3) stage_floats(S.u3, u3 + 3 * c0, 3 * rows);
+  const bool gather = p_uv == nullptr;  // only the row order (segments gather their inputs)
+  if (!gather) {  // the chunk's inputs, input order (in flight together with the ids)
+    stage_floats(S.uv, uv + 2 * c0, 2 * rows);
+    if (lod_stride) stage_floats(S.lod, lod + c0, rows);
+    stage_floats(S.urr, urr + c0, rows);
+    stage_floats(S.wi, wi + 3 * c0, 3 * rows);
+    if (wo) stage_floats(S.wo, wo + 3 * c0, 3 * rows);
+    if (u3) stage_floats(S.u3, u3 + 3 * c0, 3 * rows);
+  }
   __syncthreads();
   int32_t rk[kScatterItems];
 #pragma unroll
@@ -212,6 +215,10 @@ __global__ void __launch_bounds__(256) bin_scatter_kernel(
     while (p >= loc[m + 1]) ++m;  // n_mats <= 64, typically a handful
     return (int64_t)base[m] + (p - loc[m]);
   };
+  if (gather) {
+    for (int p = threadIdx.x; p < tot; p += blockDim.x) order[slot_of(p)] = (int32_t)(c0 + S.src[p]);
+    return;
+  }
   const float lod0 = lod_stride ? 0.f : __ldg(lod);
   for (int p = threadIdx.x; p < tot; p += blockDim.x) {
     const int64_t sl = slot_of(p);
@@ -327,8 +334,26 @@ static MultiWs carve(void* ws, int64_t n_rows, int32_t n_mats) {
 
 // Per-segment launch arguments: the permuted inputs at row offset `off`,
 // outputs straight to query order through `order` (mode-dependent outputs).
+// Segments read the caller's arrays through the row order (gather, default)
+// or a permuted copy made by the scatter (NMQ_MULTI_GATHER=0).
+bool multi_gather() {
+  static const bool g = [] {
+    const char* e = getenv("NMQ_MULTI_GATHER");
+    return !(e && e[0] == '0');
+  }();
+  return g;
+}
+
 static QueryArgs segment_args(const QueryArgs& a, const MultiWs& w, int64_t off) {
   QueryArgs sa{};
+  if (multi_gather()) {
+    sa = a;
+    sa.idx = w.order + off;
+    sa.out_idx = w.order + off;
+    sa.seg = nullptr;
+    sa.max_ctas = 0;
+    return sa;
+  }
   sa.uv = w.uv + 2 * off;
   sa.lod = w.lod + off;
   sa.lod_stride = 1;
@@ -363,11 +388,12 @@ cudaError_t multi_binned(const MatParams* const* mps, int32_t n_mats, int mode, 
     const int nb = grid256(a.n), cap = 4 * num_sms_multi();
     bin_count_kernel<<<nb < cap ? nb : cap, 256, 0, s>>>(a.n, n_mats, mat_id, w.counts, w.bad);
   }
-  const size_t sm_bytes = scatter_smem_bytes(a.lod_stride != 0, a.wo != nullptr, a.u3 != nullptr);
+  const bool gather = multi_gather();
+  const size_t sm_bytes = scatter_smem_bytes(gather, a.lod_stride != 0, a.wo != nullptr, a.u3 != nullptr);
   if (max_dynamic_smem((const void*)bin_scatter_kernel) < (int)sm_bytes) return cudaErrorInvalidValue;
   bin_scatter_kernel<<<(unsigned)((a.n + kScatterRows - 1) / kScatterRows), 256, sm_bytes, s>>>(
       a.n, n_mats, mat_id, w.counts, w.seg, w.cursor, w.order, a.uv, a.lod, a.lod_stride, a.u_rr, a.wi,
-      a.wo, a.u3, w.uv, w.lod, w.urr, w.wi, w.wo, w.u3);
+      a.wo, a.u3, gather ? nullptr : w.uv, w.lod, w.urr, w.wi, w.wo, w.u3);
   g_launches += 2;
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   if (!checked) {
