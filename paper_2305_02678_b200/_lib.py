@@ -107,6 +107,8 @@ SIGNATURES = {
                              ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]),
     "nm_query_f64": (c_i32, [ctypes.c_void_p, c_i32, c_i64] + [ctypes.c_void_p] * 14),
     "nm_eval_z_f64": (c_i32, [ctypes.c_void_p, c_i64] + [ctypes.c_void_p] * 6),
+    "nm_eval_host_ref": (c_i32, [ctypes.c_void_p, c_i64, ctypes.c_void_p, ctypes.c_void_p, c_i32]
+                         + [ctypes.c_void_p] * 6 + [c_i64, ctypes.c_void_p]),
     "nm_decoder_inputs": (c_i32, [ctypes.c_void_p, c_i64] + [ctypes.c_void_p] * 7),
     "nm_eval_spp": (c_i32, [ctypes.c_void_p, c_i64, c_float_p, c_float_p, c_i32, c_float_p, c_float_p,
                             c_float_p, c_i32, c_float_p, ctypes.c_void_p]),

@@ -1,7 +1,11 @@
 // nmq_abi.cu — C ABI (include/nmq.h): material creation (re-tiling the
 // reference's packed fp16 weights into the UMMA B-operand layout, latent
 // upload) and the query entry points.
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstdio>
 #include <mutex>
 #include <cstdlib>
@@ -660,6 +664,242 @@ struct HostStage {
   cudaEvent_t ev_in[NMQ_HOST_SLOTS] = {}, ev_k[NMQ_HOST_SLOTS] = {}, ev_out[NMQ_HOST_SLOTS] = {};
 };
 HostStage g_stage[16];
+
+// ---- pageable host buffers: pinned bounce pipeline ---------------------------
+// Pageable memory cannot be read by DMA; the driver's own staging copies it
+// through small pinned buffers on the calling thread (~12 GB/s for the C2
+// inputs).  Here a pool of host threads copies each chunk into a pinned
+// slot (and the results out of one), the copy engines move pinned slots at
+// PCIe speed, and the chunks pipeline over NMQ_HOST_SLOTS slots: copy-in of
+// chunk i, DMA + kernel of i-1..i-3 and copy-out of i-3 overlap.  The
+// reference-dtype variant widens rgb / albedo to float64 and levels to int64
+// on the device (neural.py:303 returns them so), so the host never converts.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // never destroyed: workers idle at exit
+    return *p;
+  }
+  // f(i) for i in [0, tasks), on the pool and the calling thread; returns when done
+  void run(int tasks, const std::function<void(int)>& f) {
+    if (tasks <= 0) return;
+    if (workers_.empty() || tasks == 1) {
+      for (int i = 0; i < tasks; ++i) f(i);
+      return;
+    }
+    std::lock_guard<std::mutex> serial(run_mu_);
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      job_ = &f;
+      ntask_ = tasks;
+      next_.store(0);
+      pending_ = (int)workers_.size() + 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> l(mu_);
+    done_cv_.wait(l, [&] { return pending_ == 0; });
+  }
+
+ private:
+  HostPool() {
+    int n = (int)std::thread::hardware_concurrency();
+    if (const char* v = getenv("NMQ_HOST_THREADS")) n = atoi(v);
+    n = n < 1 ? 1 : (n > 32 ? 32 : n);
+    for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  void work() {
+    for (;;) {
+      const int i = next_.fetch_add(1);
+      if (i >= ntask_) break;
+      (*job_)(i);
+    }
+    std::lock_guard<std::mutex> l(mu_);
+    if (--pending_ == 0) done_cv_.notify_all();
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int ntask_ = 0, pending_ = 0;
+  std::atomic<int> next_{0};
+  uint64_t gen_ = 0;
+};
+
+struct CopyJob {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+// memcpy a list of (possibly large) ranges on the pool in ~1 MiB pieces
+void parallel_copy(const std::vector<CopyJob>& jobs) {
+  constexpr size_t kPiece = size_t(1) << 20;
+  std::vector<CopyJob> pieces;
+  for (const CopyJob& j : jobs)
+    for (size_t o = 0; o < j.bytes; o += kPiece)
+      pieces.push_back({(char*)j.dst + o, (const char*)j.src + o, j.bytes - o < kPiece ? j.bytes - o : kPiece});
+  HostPool::get().run((int)pieces.size(), [&](int i) { memcpy(pieces[i].dst, pieces[i].src, pieces[i].bytes); });
+}
+
+__global__ void widen_kernel(int64_t c, const float* __restrict__ rgb, const float* __restrict__ alb,
+                             const int32_t* __restrict__ lv, double* __restrict__ rgb64,
+                             double* __restrict__ alb64, int64_t* __restrict__ lv64) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * c; i += stride) {
+    rgb64[i] = rgb[i];
+    if (alb) alb64[i] = alb[i];
+    if (lv && i < c) lv64[i] = lv[i];
+  }
+}
+
+struct HostIo {
+  const float *uv, *lod;
+  int32_t lod_stride;
+  const float *u_rr, *wi, *wo;
+  void *rgb, *albedo, *level;  // float / int32, or double / int64 when wide
+  bool wide;
+};
+
+struct BounceStage {
+  std::mutex mu;
+  char* pin = nullptr;  // pinned: per slot inputs (40 B/row) | outputs (56 B/row)
+  char* dev = nullptr;  // device: per slot inputs | fp32 outputs (28 B/row) | wide outputs (56 B/row)
+  int64_t chunk = 0;
+  cudaStream_t h2d = nullptr, run = nullptr, d2h = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  cudaEvent_t ev_in[NMQ_HOST_SLOTS] = {}, ev_k[NMQ_HOST_SLOTS] = {}, ev_out[NMQ_HOST_SLOTS] = {};
+};
+BounceStage g_bounce[16];
+constexpr size_t kInRow = 8 + 4 + 4 + 12 + 12, kOutRow = 24 + 24 + 8, kDevOutRow = 12 + 12 + 4;
+
+int host_eval_bounce(const nm_material* m, int64_t n, const HostIo& io, int64_t chunk, void* stream) {
+  BounceStage& B = g_bounce[m->device & 15];
+  std::lock_guard<std::mutex> lock(B.mu);
+  cudaError_t e;
+  if (B.chunk < chunk) {
+    if (B.pin) cudaFreeHost(B.pin);
+    if (B.dev) cudaFree(B.dev);
+    B.pin = B.dev = nullptr;
+    B.chunk = 0;
+    if ((e = cudaHostAlloc((void**)&B.pin, NMQ_HOST_SLOTS * (size_t)chunk * (kInRow + kOutRow), 0)) != cudaSuccess)
+      return cuda_fail(e, "host-eval pinned staging");
+    if ((e = cudaMalloc(&B.dev, NMQ_HOST_SLOTS * (size_t)chunk * (kInRow + kDevOutRow + kOutRow))) != cudaSuccess)
+      return cuda_fail(e, "host-eval device staging");
+    B.chunk = chunk;
+  }
+  if (!B.h2d) {
+    for (cudaStream_t* st : {&B.h2d, &B.run, &B.d2h}) cudaStreamCreateWithFlags(st, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&B.ev_start, cudaEventDisableTiming);
+    for (int i = 0; i < NMQ_HOST_SLOTS; ++i) {
+      cudaEventCreateWithFlags(&B.ev_in[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&B.ev_k[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&B.ev_out[i], cudaEventDisableTiming);
+    }
+  }
+  const int64_t ck = B.chunk;
+  cudaEventRecord(B.ev_start, (cudaStream_t)stream);  // after prior work on the caller's stream
+  for (cudaStream_t st : {B.h2d, B.run, B.d2h}) cudaStreamWaitEvent(st, B.ev_start, 0);
+  const size_t ob = io.wide ? 8 : 4;  // output element bytes
+  struct Slot {
+    char *pin_in, *pin_out, *dev_in, *dev_out, *dev_wide;
+  };
+  auto slot = [&](int s) {
+    Slot q;
+    q.pin_in = B.pin + (size_t)s * ck * kInRow;
+    q.pin_out = B.pin + (size_t)NMQ_HOST_SLOTS * ck * kInRow + (size_t)s * ck * kOutRow;
+    q.dev_in = B.dev + (size_t)s * ck * kInRow;
+    q.dev_out = B.dev + (size_t)NMQ_HOST_SLOTS * ck * kInRow + (size_t)s * ck * kDevOutRow;
+    q.dev_wide = B.dev + (size_t)NMQ_HOST_SLOTS * ck * (kInRow + kDevOutRow) + (size_t)s * ck * kOutRow;
+    return q;
+  };
+  const int64_t nch = (n + ck - 1) / ck;
+  auto drain = [&](int64_t cj) -> int {  // results of chunk cj -> the caller's buffers
+    const int s = (int)(cj % NMQ_HOST_SLOTS);
+    const int64_t c0 = cj * ck, c = n - c0 < ck ? n - c0 : ck;
+    cudaError_t err = cudaEventSynchronize(B.ev_out[s]);
+    if (err != cudaSuccess) return cuda_fail(err, "nm_eval_host");
+    const Slot q = slot(s);
+    std::vector<CopyJob> jobs{{(char*)io.rgb + 3 * c0 * ob, q.pin_out, (size_t)c * 3 * ob}};
+    if (io.albedo) jobs.push_back({(char*)io.albedo + 3 * c0 * ob, q.pin_out + (size_t)ck * 3 * ob, (size_t)c * 3 * ob});
+    if (io.level) jobs.push_back({(char*)io.level + c0 * ob, q.pin_out + (size_t)ck * 6 * ob, (size_t)c * ob});
+    parallel_copy(jobs);
+    return NM_OK;
+  };
+  for (int64_t ci = 0; ci < nch; ++ci) {
+    const int s = (int)(ci % NMQ_HOST_SLOTS);
+    const bool reuse = ci >= NMQ_HOST_SLOTS;
+    const int64_t c0 = ci * ck, c = n - c0 < ck ? n - c0 : ck;
+    const Slot q = slot(s);
+    // inputs: pageable -> pinned slot (host threads) -> device slot (DMA)
+    if (reuse && (e = cudaEventSynchronize(B.ev_in[s])) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
+    float* p_uv = (float*)q.pin_in;
+    float* p_lod = p_uv + 2 * ck;
+    float* p_urr = p_lod + ck;
+    float* p_wi = p_urr + ck;
+    float* p_wo = p_wi + 3 * ck;
+    parallel_copy({{p_uv, io.uv + 2 * c0, (size_t)c * 8},
+                   {p_lod, io.lod_stride ? io.lod + c0 : io.lod, io.lod_stride ? (size_t)c * 4 : 4},
+                   {p_urr, io.u_rr + c0, (size_t)c * 4},
+                   {p_wi, io.wi + 3 * c0, (size_t)c * 12},
+                   {p_wo, io.wo + 3 * c0, (size_t)c * 12}});
+    if (reuse) cudaStreamWaitEvent(B.h2d, B.ev_k[s], 0);  // the older chunk's kernel has read the slot
+    cudaMemcpyAsync(q.dev_in, q.pin_in, (size_t)ck * kInRow, cudaMemcpyHostToDevice, B.h2d);
+    cudaEventRecord(B.ev_in[s], B.h2d);
+    // kernel (+ widening) on the run stream
+    cudaStreamWaitEvent(B.run, B.ev_in[s], 0);
+    if (reuse) cudaStreamWaitEvent(B.run, B.ev_out[s], 0);  // the older chunk's results have left
+    float* d_uv = (float*)q.dev_in;
+    float* d_rgb = (float*)q.dev_out;
+    float* d_alb = d_rgb + 3 * ck;
+    int32_t* d_lv = (int32_t*)(d_alb + 3 * ck);
+    QueryArgs a{};
+    a.n = c; a.uv = d_uv; a.lod = d_uv + 2 * ck; a.lod_stride = io.lod_stride ? 1 : 0; a.u_rr = d_uv + 3 * ck;
+    a.wi = d_uv + 4 * ck; a.wo = d_uv + 7 * ck; a.rgb = d_rgb;
+    a.albedo = io.albedo ? d_alb : nullptr;
+    a.level = io.level ? d_lv : nullptr;
+    if ((e = launch_fused(m->mp, kModeEval, a, B.run)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
+    const char* out_src = q.dev_out;
+    if (io.wide) {
+      double* w = (double*)q.dev_wide;
+      widen_kernel<<<148 * 4, 256, 0, B.run>>>(c, d_rgb, a.albedo, a.level, w, w + 3 * ck, (int64_t*)(w + 6 * ck));
+      ++g_launches;
+      out_src = q.dev_wide;
+    }
+    cudaEventRecord(B.ev_k[s], B.run);
+    // results -> pinned slot (DMA); same layout as the device slot: rgb | albedo | level
+    cudaStreamWaitEvent(B.d2h, B.ev_k[s], 0);
+    cudaMemcpyAsync(q.pin_out, out_src, (size_t)c * 3 * ob, cudaMemcpyDeviceToHost, B.d2h);
+    if (io.albedo)
+      cudaMemcpyAsync(q.pin_out + (size_t)ck * 3 * ob, out_src + (size_t)ck * 3 * ob, (size_t)c * 3 * ob,
+                      cudaMemcpyDeviceToHost, B.d2h);
+    if (io.level)
+      cudaMemcpyAsync(q.pin_out + (size_t)ck * 6 * ob, out_src + (size_t)ck * 6 * ob, (size_t)c * ob,
+                      cudaMemcpyDeviceToHost, B.d2h);
+    cudaEventRecord(B.ev_out[s], B.d2h);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
+    if (ci >= NMQ_HOST_SLOTS - 1) {
+      const int rc = drain(ci - (NMQ_HOST_SLOTS - 1));
+      if (rc != NM_OK) return rc;
+    }
+  }
+  for (int64_t cj = nch > NMQ_HOST_SLOTS - 1 ? nch - (NMQ_HOST_SLOTS - 1) : 0; cj < nch; ++cj) {
+    const int rc = drain(cj);
+    if (rc != NM_OK) return rc;
+  }
+  return NM_OK;
+}
 }  // namespace
 
 int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* lod,
@@ -705,6 +945,16 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
         return cuda_fail(e, "nm_eval_host");
       if ((e = cudaStreamSynchronize((cudaStream_t)stream)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
       return NM_OK;
+    }
+  }
+  {
+    static const int bounce = [] {  // NMQ_HOST_BOUNCE=0: driver-staged pageable copies (A/B)
+      const char* v = getenv("NMQ_HOST_BOUNCE");
+      return v ? atoi(v) : 1;
+    }();
+    if (bounce) {
+      const HostIo io{uv, lod, lod_stride, u_rr, wi, wo, rgb_out, albedo_out, level_out, false};
+      return host_eval_bounce(m, n, io, chunk, stream);
     }
   }
   HostStage& H = g_stage[m->device & 15];
@@ -768,6 +1018,21 @@ int nm_eval_host(const nm_material* m, int64_t n, const float* uv, const float* 
   for (cudaStream_t st : {H.h2d, H.run, H.d2h})
     if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
   return NM_OK;
+}
+
+int nm_eval_host_ref(const nm_material* m, int64_t n, const float* uv, const float* lod, int32_t lod_stride,
+                     const float* u_rr, const float* wi, const float* wo, double* rgb_out, double* albedo_out,
+                     int64_t* level_out, int64_t chunk, void* stream) {
+  if (!m) return fail(NM_ERR_INVALID, "null material");
+  NM_CHECK_N(n);
+  if (n == 0) return NM_OK;
+  if (!uv || !lod || !u_rr || !wi || !wo || !rgb_out) return fail(NM_ERR_INVALID, "null input");
+  if (!m->mp.has_brdf) return fail(NM_ERR_INVALID, "material has no BRDF decoder");
+  if (chunk <= 0) chunk = (int64_t)1 << 18;
+  chunk = (chunk + 127) / 128 * 128;
+  DeviceGuard guard(m->device);
+  const HostIo io{uv, lod, lod_stride, u_rr, wi, wo, rgb_out, albedo_out, level_out, true};
+  return host_eval_bounce(m, n, io, chunk, stream);
 }
 
 int nm_eval_z(const nm_material* m, int64_t n, const float* z, const float* wi, const float* wo,

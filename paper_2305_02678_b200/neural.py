@@ -294,17 +294,27 @@ def _host_eval(mat, uv, level, wi, wo, u_rr, out, return_level):
         return None
     if out is not None and (out.dtype != np.float32 or out.shape != (n, 3) or not out.flags.c_contiguous):
         return None
-    f_host = out if out is not None else np.empty((n, 3), np.float32)
-    alb = np.empty((n, 3), np.float32) if mat.cfg.albedo_head else None
-    lv = np.empty(n, np.int32) if return_level else None
     h = mat.device_material(None)
     lib = _lib.load()
-    _launch(lib.nm_eval_host, h.ptr, n, h_uv.ctypes.data, h_lod.ctypes.data, int(h_lod.shape[0] == n),
-            h_urr.ctypes.data, h_wi.ctypes.data, h_wo.ctypes.data, f_host.ctypes.data,
+    lod_stride = int(h_lod.shape[0] == n)
+    if out is None:
+        # the reference's dtypes straight from the library (widened on the
+        # device; pageable buffers through its pinned bounce pipeline)
+        f = np.empty((n, 3), np.float64)
+        alb = np.empty((n, 3), np.float64) if mat.cfg.albedo_head else None
+        lv = np.empty(n, np.int64) if return_level else None
+        _launch(lib.nm_eval_host_ref, h.ptr, n, h_uv.ctypes.data, h_lod.ctypes.data, lod_stride,
+                h_urr.ctypes.data, h_wi.ctypes.data, h_wo.ctypes.data, f.ctypes.data,
+                None if alb is None else alb.ctypes.data, None if lv is None else lv.ctypes.data,
+                0, _io.stream_ptr(h.device))
+        return f, alb, lv
+    alb = np.empty((n, 3), np.float32) if mat.cfg.albedo_head else None
+    lv = np.empty(n, np.int32) if return_level else None
+    _launch(lib.nm_eval_host, h.ptr, n, h_uv.ctypes.data, h_lod.ctypes.data, lod_stride,
+            h_urr.ctypes.data, h_wi.ctypes.data, h_wo.ctypes.data, out.ctypes.data,
             None if alb is None else alb.ctypes.data, None if lv is None else lv.ctypes.data,
             _io.STREAM_CHUNK, _io.stream_ptr(h.device))
-    f = f_host if out is not None else f_host.astype(np.float64)
-    return (f, None if alb is None else alb.astype(np.float64),
+    return (out, None if alb is None else alb.astype(np.float64),
             None if lv is None else lv.astype(np.int64))
 
 
