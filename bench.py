@@ -12,8 +12,9 @@ data path); `value` = all ranks' queries / max-over-ranks time.
 
 One JSON line on rank 0.  `value` = device-timed throughput with inputs in
 HBM (CUDA events, inputs rotating over 3 sets > L2); `e2e` = the public API
-(`neural.eval_material` on pinned host numpy buffers, H2D + kernel + D2H
-inside the timed region); `roofline` = the fused kernel's algorithmic bytes
+(`neural.eval_material` on pageable host numpy buffers in the reference's
+call shape, H2D + kernel + D2H inside the timed region; `e2e_pinned` the
+zero-copy variant); `roofline` = the fused kernel's algorithmic bytes
 (fp32 I/O + 16 B per unique texel touched) / launch time vs measured HBM
 peak; `cpu_baseline` = the numpy oracle (restatement of the reference,
 oracle/nm_oracle.py) on the host cores for a bounded sample.
@@ -805,11 +806,13 @@ def run_ours(args):
         torch.cuda.synchronize()
         e_ms = max_over_ranks((time.perf_counter() - t0) * 1e3, world)
         e2e = {"value": n * world * args.e2e_steps / (e_ms / 1e3), "unit": "queries/s",
-               "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 16),
+               "h2d_bytes_per_step": int(n * 40), "d2h_bytes_per_step": int(n * 32),
                "steps": args.e2e_steps,
                "api": "paper_2305_02678_b200.neural.eval_material(mat, uv, lod, wi, wo, u_rr, fp16=True) "
                       "-> (f float64, None, chosen int64): pageable numpy in/out, the reference call shape "
-                      "(neural.py:303); H2D, kernels, D2H and the dtype conversions inside the timed region"}
+                      "(neural.py:303) -> nm_eval_host_ref (pinned bounce pipeline, float64/int64 widened "
+                      "on the device and copied back); H2D, kernels, D2H and the result allocation inside "
+                      "the timed region"}
         # pinned host buffers and an fp32 `out`: the zero-copy launch
         pin = []
         for q in sets[:2]:
