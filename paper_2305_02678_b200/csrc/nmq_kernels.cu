@@ -194,26 +194,32 @@ __device__ __forceinline__ void load_z(const float* z, int64_t q, float (&out)[8
 }
 
 // BRDF decode of one query given z; returns raw decoder outputs in y.
-// d64: the query's float64 directions [wi, wo] when the caller passed them
-// (warp-uniform), else null — the reference transforms its float64 arrays.
+// wi64 / wo64: the query's float64 directions when the caller passed them,
+// else null — the reference transforms its float64 arrays.
+// PREC: instantiated for precise (fp32-master) materials only — the fp16
+// path's reference-arithmetic frames (IEEE divisions with slow-path calls)
+// are compiled out of it (their register pressure measured -7 % there).
+template <bool PREC = false>
 __device__ __forceinline__ void brdf_decode(const MatParams& mp, Group& g, const float (&z)[8],
-                                            V3 wi, V3 wo, float (&y)[16], const D3* d64 = nullptr) {
+                                            V3 wi, V3 wo, float (&y)[16], const double* wi64 = nullptr,
+                                            const double* wo64 = nullptr) {
   float x[32];
 #pragma unroll
   for (int k = 0; k < 32; ++k) x[k] = 0.f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) x[k] = z[k];
-  if (mp.use_frames && !mp.precise) {
+  if (!PREC && mp.use_frames && !mp.precise) {
     // fp16 path: the reference's rounding of every decoder input, exactly —
     // frame layer in its sequential-FMA order, frames and transforms in
     // float64, fp32, then fp16 (neural.py:282-287)
     uint32_t zh[4], x16[6];
 #pragma unroll
     for (int c = 0; c < 4; ++c) zh[c] = pack_h2(z[2 * c], z[2 * c + 1]);
-    if (d64)
-      tw_exact(mp, zh, d64[0], d64[1], x16);
-    else
-      tw_exact(mp, zh, wi, wo, x16);
+    // float64 directions are read here, at the point of use (nothing float64
+    // stays live across the fetch); one call site keeps the code single
+    const D3 di = wi64 ? D3{__ldg(wi64), __ldg(wi64 + 1), __ldg(wi64 + 2)} : d3(wi);
+    const D3 dq = wo64 ? D3{__ldg(wo64), __ldg(wo64 + 1), __ldg(wo64 + 2)} : d3(wo);
+    tw_exact(mp, zh, di, dq, x16);
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
       const float2 f = unpack_h2(x16[c]);
@@ -284,7 +290,7 @@ __device__ __forceinline__ Proxy sampler_decode(const MatParams& mp, Group& g,
   return proxy_from_raw(y, mp.isotropic != 0);
 }
 
-template <int MODE>
+template <int MODE, bool PREC>
 __global__ void __launch_bounds__(384, 2)
 fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryArgs a,
              uint32_t tmem_cols, uint32_t group_cols) {
@@ -347,15 +353,11 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
     const int64_t oq = valid ? (a.out_idx ? (int64_t)__ldg(a.out_idx + seg_base + i) : q) : 0;  // output row
 
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
-    D3 d64[2] = {{0.0, 0.0, 1.0}, {0.0, 0.0, 1.0}};  // float64 directions (a.wi64)
     auto load_dirs = [&](bool with_wo) {
       if (a.wi64) {  // narrowed copies for the fp32 consumers (sampler input, proxy)
-        d64[0] = {__ldg(a.wi64 + 3 * q), __ldg(a.wi64 + 3 * q + 1), __ldg(a.wi64 + 3 * q + 2)};
-        wi = v3((float)d64[0].x, (float)d64[0].y, (float)d64[0].z);
-        if (with_wo) {
-          d64[1] = {__ldg(a.wo64 + 3 * q), __ldg(a.wo64 + 3 * q + 1), __ldg(a.wo64 + 3 * q + 2)};
-          wo = v3((float)d64[1].x, (float)d64[1].y, (float)d64[1].z);
-        }
+        wi = v3((float)__ldg(a.wi64 + 3 * q), (float)__ldg(a.wi64 + 3 * q + 1), (float)__ldg(a.wi64 + 3 * q + 2));
+        if (with_wo)
+          wo = v3((float)__ldg(a.wo64 + 3 * q), (float)__ldg(a.wo64 + 3 * q + 1), (float)__ldg(a.wo64 + 3 * q + 2));
       } else {
         wi = ldg3(a.wi, q);
         if (with_wo) wo = ldg3(a.wo, q);
@@ -402,9 +404,11 @@ fused_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Query
 
     if constexpr (MODE == kModeEval || MODE == kModeEvalZ || MODE == kModeQuery) {
       float y[16];
-      brdf_decode(mp, g, z, wi, wo, y, a.wi64 ? d64 : nullptr);
+      const bool d64 = a.wi64 && valid;
+      brdf_decode<PREC>(mp, g, z, wi, wo, y, d64 ? a.wi64 + 3 * q : nullptr, d64 ? a.wo64 + 3 * q : nullptr);
       // horizon mask on the caller's values (a float64 z below 2^-149 narrows to 0)
-      const bool up = a.wi64 ? (d64[0].z > 0.0 && d64[1].z > 0.0) : (wi.z > 0.f && wo.z > 0.f);
+      const bool up = d64 ? (__ldg(a.wi64 + 3 * q + 2) > 0.0 && __ldg(a.wo64 + 3 * q + 2) > 0.0)
+                          : (wi.z > 0.f && wo.z > 0.f);
       if (MODE == kModeEval && a.img) {  // per-pixel spp mean (warp-collective)
         const V3 f = up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
         spp_accumulate(a.img, i, f, valid, a.spp_log2);
@@ -523,15 +527,11 @@ divergent_eval_kernel(const MatParams* __restrict__ mps_g, int32_t n_mats,
     const bool valid = m0 >= 0 && m0 < n_mats;  // out-of-range ids are skipped
     const int m = valid ? m0 : -1;
     V3 wi = v3(0.f, 0.f, 1.f), wo = v3(0.f, 0.f, 1.f);
-    D3 d64[2] = {{0.0, 0.0, 1.0}, {0.0, 0.0, 1.0}};  // float64 directions (a.wi64)
     auto load_dirs = [&](bool with_wo) {
       if (a.wi64) {  // narrowed copies for the fp32 consumers (sampler input, proxy)
-        d64[0] = {__ldg(a.wi64 + 3 * q), __ldg(a.wi64 + 3 * q + 1), __ldg(a.wi64 + 3 * q + 2)};
-        wi = v3((float)d64[0].x, (float)d64[0].y, (float)d64[0].z);
-        if (with_wo) {
-          d64[1] = {__ldg(a.wo64 + 3 * q), __ldg(a.wo64 + 3 * q + 1), __ldg(a.wo64 + 3 * q + 2)};
-          wo = v3((float)d64[1].x, (float)d64[1].y, (float)d64[1].z);
-        }
+        wi = v3((float)__ldg(a.wi64 + 3 * q), (float)__ldg(a.wi64 + 3 * q + 1), (float)__ldg(a.wi64 + 3 * q + 2));
+        if (with_wo)
+          wo = v3((float)__ldg(a.wo64 + 3 * q), (float)__ldg(a.wo64 + 3 * q + 1), (float)__ldg(a.wo64 + 3 * q + 2));
       } else {
         wi = ldg3(a.wi, q);
         if (with_wo) wo = ldg3(a.wo, q);
@@ -717,7 +717,7 @@ cudaError_t launch_mode(const MatParams& mp, const QueryArgs& a, cudaStream_t s,
   if (cols > 512) return cudaErrorInvalidValue;
   const int ctas_per_sm = (int)(512 / cols) < 2 ? (int)(512 / cols) : 2;
   const int smem = smem_bytes_for(mp);
-  auto kern = fused_kernel<MODE>;
+  auto kern = mp.precise ? fused_kernel<MODE, true> : fused_kernel<MODE, false>;
   const int lim = max_dynamic_smem((const void*)kern);
   if (lim < 0) return cudaErrorInvalidValue;
   if (smem > lim) return cudaErrorNotSupported;
