@@ -715,25 +715,34 @@ __device__ __forceinline__ void frame_tw64_rsq(const float* raw, D3 di, D3 dout,
   ti[0] = (float)fdot(t, di); ti[1] = (float)fdot(b, di); ti[2] = (float)fdot(n, di);
   to[0] = (float)fdot(t, dout); to[1] = (float)fdot(b, dout); to[2] = (float)fdot(n, dout);
 }
+// frames: THIS row's frames to compute (bit f = frame f).  The float64
+// frame runs once per pass for all lanes of the warp, each lane on its own
+// next frame — a warp whose rows flag different frames does one pass, not
+// two (rows flag a single frame almost always).  Frames not computed come
+// back as 0 (the caller keeps their fast values).
 __device__ __forceinline__ void tw_resolve(const MatParams& m, const uint32_t (&zh)[4], V3 wi, V3 wo,
                                            uint32_t (&x16)[6], uint32_t frames) {
   float raw[12];
   frame_raw_seq(m, zh, raw);
-  float ti[6], to[6];
+  float ti[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, to[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  uint32_t todo = frames & (m.n_frames == 2 ? 3u : 1u);
+  const uint32_t warp = __activemask();
 #pragma unroll
-  for (int f = 0; f < 2; ++f) {
-    if (f < m.n_frames && ((frames >> f) & 1u)) {
-      float a[3], b[3];
-      frame_tw64_rsq(raw + 6 * f, d3(wi), d3(wo), a, b);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (!__any_sync(warp, todo != 0u)) break;
+    const bool act = todo != 0u;
+    const bool f1 = !(todo & 1u);  // this lane's next frame: 0 first
+    float r6[6];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        ti[3 * f + k] = a[k];
-        to[3 * f + k] = b[k];
-      }
-    } else {
+    for (int k = 0; k < 6; ++k) r6[k] = f1 ? raw[6 + k] : raw[k];
+    float a[3], b[3];
+    frame_tw64_rsq(r6, d3(wi), d3(wo), a, b);
 #pragma unroll
-      for (int k = 0; k < 3; ++k) ti[3 * f + k] = to[3 * f + k] = 0.f;
+    for (int k = 0; k < 3; ++k) {
+      if (act && !f1) { ti[k] = a[k]; to[k] = b[k]; }
+      if (act && f1) { ti[3 + k] = a[k]; to[3 + k] = b[k]; }
     }
+    todo &= f1 ? ~2u : ~1u;
   }
   pack_tw(m, ti, to, x16);
 }

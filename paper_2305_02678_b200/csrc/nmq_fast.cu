@@ -489,9 +489,9 @@ __device__ __forceinline__ void resolve_entries(const MatParams& mp, const Query
       zh[0] = e1.w; zh[1] = e2.x; zh[2] = e2.y; zh[3] = e2.z;
       const V3 wi = v3(__uint_as_float(e2.w), __uint_as_float(e3.x), __uint_as_float(e3.y));
       const V3 wo = v3(__uint_as_float(e3.z), __uint_as_float(e3.w), __uint_as_float(e4.x));
-      // only frames with a value near a rounding midpoint need the float64 path
-      // (warp-uniform choice: a per-lane one would serialize both paths anyway)
-      const uint32_t fm = __reduce_or_sync(__activemask(), e4.y);
+      // only this row's frames with a value near a rounding midpoint need the
+      // float64 path (tw_resolve runs one frame per lane per pass)
+      const uint32_t fm = e4.y;
       tw_resolve(mp, zh, wi, wo, xe, fm);
       const uint32_t xf[6] = {e0.y, e0.z, e0.w, e1.x, e1.y, e1.z};
 #pragma unroll
