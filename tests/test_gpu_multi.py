@@ -177,3 +177,49 @@ def test_multi_material_sample_pdf_and_query(mode):
     assert np.array_equal(ws, ws2) and np.array_equal(pdf, pdf2)  # the same kernels on the same rows
     with pytest.raises(NotImplementedError):
         neural.sample_pdf_multi(mats, ids, uv, lod, urr, wi, u3, mode="divergent")
+
+
+def test_host_buffer_eval_from_threads_and_chunking():
+    """The drop-in call on pageable numpy arrays (nm_eval_host_ref: pinned
+    bounce pipeline, host thread pool, float64 / int64 results widened on
+    the device) from two host threads at once and across many chunks equals
+    the device-pointer call bit for bit."""
+    import threading
+
+    import torch
+
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import _io, _lib, neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(91)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(albedo_head=True), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 64, 64).levels)
+    n = 600_001  # three 256k chunks and a ragged tail
+    uv = rng.random((n, 2)).astype(np.float32)
+    lod = (rng.random(n) * 6).astype(np.float32)
+    urr = rng.random(n).astype(np.float32)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    wi, wo = wi.astype(np.float32), wo.astype(np.float32)
+    # reference result through device pointers
+    t = {k: torch.from_numpy(v).cuda() for k, v in (("uv", uv), ("lod", lod), ("urr", urr), ("wi", wi), ("wo", wo))}
+    f_d, a_d, l_d = neural.eval_material(mat, t["uv"], t["lod"], t["wi"], t["wo"], t["urr"], fp16=True)
+    want = (f_d.cpu().numpy().astype(np.float64), a_d.cpu().numpy().astype(np.float64),
+            l_d.cpu().numpy().astype(np.int64))
+    got = [None, None]
+
+    def run(k):
+        got[k] = neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=True)
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for f, a, lv in got:
+        assert f.dtype == np.float64 and a.dtype == np.float64 and lv.dtype == np.int64
+        assert np.array_equal(f, want[0]) and np.array_equal(a, want[1]) and np.array_equal(lv, want[2])
+    # scalar level (lod_stride 0) through the same pipeline
+    f1, _, lv1 = neural.eval_material(mat, uv[:1000], np.float32(2.5), wi[:1000], wo[:1000], urr[:1000], fp16=True)
+    f2, _, lv2 = neural.eval_material(mat, t["uv"][:1000], torch.tensor([2.5], device="cuda"), t["wi"][:1000],
+                                      t["wo"][:1000], t["urr"][:1000], fp16=True)
+    assert np.array_equal(f1, f2.cpu().numpy().astype(np.float64)) and np.array_equal(lv1, lv2.cpu().numpy())
