@@ -72,5 +72,19 @@ for src, dst in ((pin, rgb_pin.data_ptr()), ({"uv": uv, "lod": lod, "urr": urr, 
     _lib.check(lib.nm_eval_host(h.ptr, n, ptr["uv"], ptr["lod"], 1, ptr["urr"], ptr["wi"], ptr["wo"], dst,
                                 None, None, 256, _io.stream_ptr(h.device)))
 assert np.array_equal(rgb_pin.numpy(), rgb_pg)
+# the drop-in's reference dtypes through the pinned bounce pipeline (several chunks)
+f64o, lv64 = np.empty((n, 3)), np.empty(n, np.int64)
+_lib.check(lib.nm_eval_host_ref(h.ptr, n, uv.ctypes.data, lod.ctypes.data, 1, urr.ctypes.data, wi.ctypes.data,
+                                wo.ctypes.data, f64o.ctypes.data, None, lv64.ctypes.data, 256, _io.stream_ptr(h.device)))
+assert np.array_equal(f64o, rgb_pg.astype(np.float64))
+# float64 directions (nm_query_f64 / nm_eval_z_f64) and the decoder-input hook
+wi64, wo64 = O.draw_direction_pairs(rng, n)
+neural.eval_material(mat, uv64, lod64, wi64, wo64, urr64, fp16=True)
+neural.eval_brdf(mat, z, wi64, wo64, fp16=True)
+x16 = torch.empty((n, 12), dtype=torch.int16, device="cuda")
+zt = torch.from_numpy(np.ascontiguousarray(z, np.float32)).cuda()
+w64 = [torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (wi64, wo64)]
+_lib.check(lib.nm_decoder_inputs(h.ptr, n, zt.data_ptr(), None, None, w64[0].data_ptr(), w64[1].data_ptr(),
+                                 x16.data_ptr(), _io.stream_ptr(h.device)))
 torch.cuda.synchronize()
 print("sanitize_run ok")
