@@ -212,7 +212,12 @@ int nm_query(const nm_material* mat, int64_t n, const float* uv, const float* lo
  *     mat_id (n,) int32 in [0, n_mats).  DIVERGENT decodes mixed tiles
  *     directly; BINNED first bins queries by material with warp-aggregated
  *     counting, then runs the coherent kernel per bin.  workspace must hold
- *     nm_multi_workspace_bytes(n, n_mats) bytes of device memory. --------- */
+ *     nm_multi_workspace_bytes(n, n_mats) bytes of device memory.  Host
+ *     blocking: BINNED waits for the bin counts (one D2H, to validate ids
+ *     and size the per-bin launches); BINNED_ASYNC never waits; DIVERGENT
+ *     waits only on the first call with a given material list (its device
+ *     table of parameter blocks is uploaded once and cached until one of
+ *     the materials is destroyed). --------------------------------------- */
 size_t nm_multi_workspace_bytes(int64_t n, int32_t n_mats);
 int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
                   const int32_t* mat_id, const float* uv, const float* lod,

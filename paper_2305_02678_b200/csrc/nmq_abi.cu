@@ -1,6 +1,7 @@
 // nmq_abi.cu — C ABI (include/nmq.h): material creation (re-tiling the
 // reference's packed fp16 weights into the UMMA B-operand layout, latent
 // upload) and the query entry points.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <condition_variable>
@@ -301,6 +302,55 @@ struct nm_material {
   int brdf_width = 0, sampler_width = 0;
 };
 
+namespace {
+// DIVERGENT's device table of the materials' parameter blocks, uploaded once
+// per material list (handles are immutable) so a call never waits for the
+// stream; entries holding a material are dropped when it is destroyed.
+struct DivTable {
+  int device;
+  std::vector<const nm_material*> mats;
+  nmq::MatParams* dev;
+};
+std::mutex g_div_mu;
+std::vector<DivTable> g_div;
+
+cudaError_t div_table(const std::vector<const nmq::MatParams*>& mps, const nm_material* const* mats, int32_t n_mats,
+                      int device, nmq::MatParams** out) {
+  std::lock_guard<std::mutex> lock(g_div_mu);
+  std::vector<const nm_material*> key(mats, mats + n_mats);
+  for (const DivTable& t : g_div)
+    if (t.device == device && t.mats == key) {
+      *out = t.dev;
+      return cudaSuccess;
+    }
+  std::vector<nmq::MatParams> host(n_mats);
+  for (int k = 0; k < n_mats; ++k) host[k] = *mps[k];
+  nmq::MatParams* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, n_mats * sizeof(nmq::MatParams));
+  if (e != cudaSuccess) return e;
+  if ((e = cudaMemcpy(d, host.data(), n_mats * sizeof(nmq::MatParams), cudaMemcpyHostToDevice)) != cudaSuccess) {
+    cudaFree(d);
+    return e;
+  }
+  g_div.push_back({device, key, d});
+  *out = d;
+  return cudaSuccess;
+}
+
+void div_forget(const nm_material* m) {
+  std::lock_guard<std::mutex> lock(g_div_mu);
+  for (size_t i = 0; i < g_div.size();) {
+    const auto& v = g_div[i].mats;
+    if (std::find(v.begin(), v.end(), m) != v.end()) {
+      cudaFree(g_div[i].dev);
+      g_div.erase(g_div.begin() + i);
+    } else {
+      ++i;
+    }
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char* nm_last_error(void) { return t_err.c_str(); }
@@ -481,6 +531,7 @@ int nm_material_create(const nm_material_desc* d, int device, nm_material** out)
 int nm_material_destroy(nm_material* m) {
   if (!m) return NM_OK;
   DeviceGuard guard(m->device);
+  div_forget(m);
   if (m->latent) cudaFree(m->latent);
   if (m->wblob) cudaFree(m->wblob);
   if (m->w32) cudaFree(m->w32);
@@ -1398,13 +1449,8 @@ int nm_eval_multi(const nm_material* const* mats, int32_t n_mats, int64_t n,
   DeviceGuard guard(dev);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e;
-  std::vector<MatParams> host(n_mats);
-  for (int k = 0; k < n_mats; ++k) host[k] = *mps[k];
-  MatParams* dev_mps = reinterpret_cast<MatParams*>(((uintptr_t)workspace + 255) & ~(uintptr_t)255);
-  if ((e = cudaMemcpyAsync(dev_mps, host.data(), n_mats * sizeof(MatParams), cudaMemcpyHostToDevice,
-                           s)) != cudaSuccess)
-    return cuda_fail(e, "upload material table");
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(e, "upload material table");
+  MatParams* dev_mps = nullptr;
+  if ((e = div_table(mps, mats, n_mats, dev, &dev_mps)) != cudaSuccess) return cuda_fail(e, "material table");
   return finish(nullptr, launch_eval_divergent(mps.data(), dev_mps, n_mats, mat_id, a, s),
                 "nm_eval_multi(divergent)");
 }
