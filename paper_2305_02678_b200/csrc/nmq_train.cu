@@ -21,6 +21,7 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "nmq_device.cuh"
+#include "tc.cuh"
 #include "nmq_internal.h"
 
 namespace nmq {
@@ -418,6 +419,163 @@ __global__ void __launch_bounds__(256) mlp_dparam_kernel(const __grid_constant__
   }
 }
 
+// ---------------------------------------------------------------------------
+// dW / db on the tensor cores (tcgen05.mma kind::tf32), 3xTF32: every operand
+// is split a = hi + lo (hi = a with its low 13 mantissa bits cleared, exact
+// in tf32; lo = a - hi, whose own tf32 truncation keeps ~11 more bits) and
+// D += A_hi B_hi + A_hi B_lo + A_lo B_hi — each product to ~2^-21 relative,
+// fp32 accumulation in TMEM over one CTA's rows, float64 atomics across
+// CTAs.  A = g^T (M = 128 >= fo rows, K = batch: g is cached column-major,
+// so K is contiguous), B = [x | 1] (N = fi + 1 padded to 16, K = batch), both
+// K-major in SMEM in the canonical no-swizzle layout: element (row, k) at
+// (k / 4) * (rows * 16) + row * 16 + (k % 4) * 4 — 8-row x 16-byte core
+// matrices, SBO = 128 B between row groups, LBO = rows * 16 B between k
+// chunks.  The reference's float64 chain is replaced only in this reduction
+// (parity: tests/test_gpu_parity.py::test_mlp_forward_cached_backward_*).
+#ifndef NMQ_TC_KT
+#define NMQ_TC_KT 32
+#endif
+#ifndef NMQ_TC_ROWS
+#define NMQ_TC_ROWS 256
+#endif
+constexpr int kTcM = 128, kTcNMax = 80, kTcKT = NMQ_TC_KT, kTcRows = NMQ_TC_ROWS;  // rows per CTA (split-K)
+constexpr size_t kTcSmem = (size_t)2 * (kTcM + kTcNMax) * kTcKT * 4;
+
+__device__ __forceinline__ void split_tf32(float v, float& hi, float& lo) {
+  hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  lo = v - hi;  // exact
+}
+
+__global__ void __launch_bounds__(128) mlp_dparam_tc_kernel(const __grid_constant__ DparamArgs args, int64_t B) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase_sh;
+  const int l = blockIdx.y;
+  const int fi = args.fi[l], fo = args.fo[l], in_act = args.in_act[l];
+  const float* __restrict__ in_src = args.in_src[l];
+  const double* __restrict__ g = args.g[l];
+  double* __restrict__ dp = args.dp[l];
+  const int np = ((fi + 1) + 15) / 16 * 16;  // N: inputs + the bias column, padded
+  float* a_hi = reinterpret_cast<float*>(sm);
+  float* a_lo = a_hi + kTcM * kTcKT;
+  float* b_hi = a_lo + kTcM * kTcKT;
+  float* b_lo = b_hi + kTcNMax * kTcKT;
+  const int t = threadIdx.x, warp = t / 32;
+  auto off = [](int rows, int row, int k) { return (k >> 2) * (rows * 4) + row * 4 + (k & 3); };  // in floats
+  // padded rows stay zero: A rows >= fo, B rows > fi
+  for (int i = t; i < (int)(kTcSmem / 4); i += 128) reinterpret_cast<float*>(sm)[i] = 0.f;
+  if (t == 0) tc::mbar_init(&bar, 1);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(tc::smem_u32(&tbase_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_mbar_init();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tb = tbase_sh;
+  const int64_t r0 = (int64_t)blockIdx.x * kTcRows;
+  const int64_t r1 = r0 + kTcRows < B ? r0 + kTcRows : B;
+  constexpr uint32_t idesc = tc::idesc_tf32(kTcM, 16);  // N patched below (runtime)
+  const uint32_t id = (idesc & ~(0x3Fu << 17)) | ((uint32_t)(np >> 3) << 17);
+  // the next tile's g and inputs are loaded into registers while the tensor
+  // core runs the current one (consecutive threads take consecutive k of one
+  // row: coalesced)
+  constexpr int kGPer = kMaxW * kTcKT / 128, kXPer = (kMaxW + 1) * kTcKT / 128 + 1;
+  double gr[kGPer];
+  float xr[kXPer];
+  const int ng = fo * kTcKT, nx = (fi + 1) * kTcKT;
+  auto load = [&](int64_t t0) {
+#pragma unroll
+    for (int u = 0; u < kGPer; ++u) {
+      const int i = t + 128 * u;
+      if (i >= ng) break;
+      const int m = i / kTcKT, k = i % kTcKT;
+      gr[u] = t0 + k < r1 ? g[(int64_t)m * B + t0 + k] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kXPer; ++u) {
+      const int i = t + 128 * u;
+      if (i >= nx) break;
+      const int n = i / kTcKT, k = i % kTcKT;
+      float xv = 0.f;
+      if (t0 + k < r1) {
+        if (n == fi) {
+          xv = 1.f;  // bias column: db = sum g
+        } else {
+          xv = in_src[(int64_t)n * B + t0 + k];
+          if (in_act && xv < 0.f) xv *= kLeaky;
+        }
+      }
+      xr[u] = xv;
+    }
+  };
+  load(r0);
+  uint32_t phase = 0;
+  for (int64_t t0 = r0; t0 < r1; t0 += kTcKT) {
+#pragma unroll
+    for (int u = 0; u < kGPer; ++u) {
+      const int i = t + 128 * u;
+      if (i >= ng) break;
+      const int m = i / kTcKT, k = i % kTcKT;
+      const double v = gr[u];
+      const float hi = __uint_as_float(__float_as_uint((float)v) & 0xFFFFE000u);
+      a_hi[off(kTcM, m, k)] = hi;
+      a_lo[off(kTcM, m, k)] = (float)(v - (double)hi);
+    }
+#pragma unroll
+    for (int u = 0; u < kXPer; ++u) {
+      const int i = t + 128 * u;
+      if (i >= nx) break;
+      const int n = i / kTcKT, k = i % kTcKT;
+      float hi, lo;
+      split_tf32(xr[u], hi, lo);
+      b_hi[off(kTcNMax, n, k)] = hi;
+      b_lo[off(kTcNMax, n, k)] = lo;
+    }
+    tc::fence_proxy_async_smem();  // generic-proxy stores -> the tensor core's async proxy
+    tc::tc_fence_before();
+    __syncthreads();
+    if (t == 0) {
+      tc::tc_fence_after();
+      const uint32_t lbo_a = kTcM * 16, lbo_b = kTcNMax * 16;
+#pragma unroll
+      for (int s = 0; s < kTcKT / 8; ++s) {  // K = 8 tf32 = 2 k-chunks per MMA
+        const uint64_t ah = tc::smem_desc(tc::smem_u32(a_hi) + 2 * s * lbo_a, lbo_a, 128);
+        const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo) + 2 * s * lbo_a, lbo_a, 128);
+        const uint64_t bh = tc::smem_desc(tc::smem_u32(b_hi) + 2 * s * lbo_b, lbo_b, 128);
+        const uint64_t bl = tc::smem_desc(tc::smem_u32(b_lo) + 2 * s * lbo_b, lbo_b, 128);
+        tc::mma_ss_tf32(tb, ah, bh, id, (t0 > r0 || s > 0) ? 1u : 0u);
+        tc::mma_ss_tf32(tb, ah, bl, id, 1u);
+        tc::mma_ss_tf32(tb, al, bh, id, 1u);
+      }
+      tc::mma_commit(&bar);
+    }
+    if (t0 + kTcKT < r1) load(t0 + kTcKT);
+    tc::mbar_wait(&bar, phase);  // the MMAs have read the tile before it is overwritten
+    phase ^= 1u;
+    tc::tc_fence_after();
+  }
+  // row m of D (TMEM lane m) -> dW[m][0..fi], db[m] = column fi
+  const int m = t;
+  const uint32_t lane_addr = tb + ((uint32_t)(warp * 32) << 16);
+  for (int c0 = 0; c0 < np; c0 += 16) {
+    uint32_t r[16];
+    tc::tmem_ld16(lane_addr + (uint32_t)c0, r);
+    tc::tmem_ld_wait();
+    if (m < fo) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j <= fi) atomicAdd(dp + (int64_t)m * (fi + 1) + c0 + j, (double)__uint_as_float(r[j]));
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tb) : "memory");
+}
+
 int max_width(const MlpView& v) {
   int w = 0;
   for (int l = 0; l < v.n_layers; ++l) {
@@ -536,6 +694,16 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
     da.g[l] = g_cache + pre_off;
     da.dp[l] = dparams + v.w_off[l];
     pre_off += (int64_t)fo[l] * B;
+  }
+#ifndef NMQ_DPARAM_TC
+#define NMQ_DPARAM_TC 1  // dW / db on the tensor cores (3xTF32); 0: the float64 SIMT reduction
+#endif
+  if (NMQ_DPARAM_TC) {
+    if (max_dynamic_smem((const void*)mlp_dparam_tc_kernel) < (int)kTcSmem) return cudaErrorNotSupported;
+    const dim3 gtc((unsigned)((B + kTcRows - 1) / kTcRows), (unsigned)n_layers);
+    mlp_dparam_tc_kernel<<<gtc, 128, kTcSmem, s>>>(da, B);
+    ++g_launches;
+    return cudaGetLastError();
   }
   const dim3 grid((unsigned)((B + kRowsPerCta - 1) / kRowsPerCta), (unsigned)n_layers);
   if (wide)

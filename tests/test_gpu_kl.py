@@ -52,7 +52,7 @@ def test_sampler_loss_and_grads_vs_reference(tag):
     assert isinstance(loss, float)
     want = float(g[f"{tag}_loss"])
     assert abs(loss - want) <= 1e-10 * max(1.0, abs(want)), (loss, want)  # measured ~1e-14
-    _grads_close(grads, g, tag, rtol=2e-5)  # measured <= 1.5e-6 of the largest entry
+    _grads_close(grads, g, tag, rtol=2e-5)  # measured <= 5.1e-6 of the largest entry (3xTF32 dW)
 
 
 def test_sampler_loss_custom_target_and_rng():
