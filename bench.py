@@ -935,7 +935,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["c2", "c3", "full", "c4", "c5", "train", "kl"], default="c2")
     ap.add_argument("--sets", type=int, default=3)
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=50)
     ap.add_argument("--cpu-sample", type=int, default=C2_N)
     ap.add_argument("--ref-sample", type=int, default=262144)
     ap.add_argument("--no-cpu-baseline", action="store_true")

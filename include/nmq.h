@@ -256,10 +256,11 @@ int nm_eval_host(const nm_material* mat, int64_t n, const float* uv, const float
  * reference's output dtypes — colours (n,3) and albedo float64, levels
  * int64 — widened on the device, so the host never converts.  Pageable
  * buffers stream through a pinned bounce pipeline: a pool of host threads
- * (NMQ_HOST_THREADS, default the hardware threads) copies each chunk of
+ * (NMQ_HOST_THREADS, default min(8, hardware threads)) copies each chunk of
  * inputs into a pinned slot and each chunk of results out of one, the copy
  * engines move the pinned slots, chunks of `chunk` queries (0 = 256k)
- * overlap over 4 slots.  Blocking.  nm_eval_host's pageable path uses the
+ * overlap over 4 slots; page-locked result buffers receive the DMA
+ * directly.  Blocking.  nm_eval_host's pageable path uses the
  * same pipeline (NMQ_HOST_BOUNCE=0: the driver's own staging). */
 int nm_eval_host_ref(const nm_material* m, int64_t n, const float* uv, const float* lod, int32_t lod_stride,
                      const float* u_rr, const float* wi, const float* wo, double* rgb_out, double* albedo_out,

@@ -134,6 +134,7 @@ def out(t, numpy_mode, np_dtype=np.float64):
 # internal streams, overlapped).  Host buffers should be pinned for full overlap.
 
 STREAM_CHUNK = int(os.environ.get("NMQ_STREAM_CHUNK", 1 << 19))  # queries per chunk
+REF_CHUNK = int(os.environ.get("NMQ_REF_CHUNK", 0))  # nm_eval_host_ref chunk (0 = the library's default)
 
 
 def host_rows(x, cols, name):
@@ -143,3 +144,20 @@ def host_rows(x, cols, name):
     if a.ndim != 2 or a.shape[1] != cols:
         return None
     return np.ascontiguousarray(a, dtype=np.float32)
+
+
+# Result arrays of the host-buffer calls: numpy arrays backed by page-locked
+# memory from torch's caching host allocator (a block returns to its cache
+# when the caller drops the array and is reused by a later call), so the
+# results are DMA'd straight into them — no fresh-page faults, no host copy.
+# Small results stay ordinary numpy arrays.
+PINNED_RESULT_MIN = int(os.environ.get("NMQ_PINNED_RESULT_MIN", 1 << 20))  # bytes
+
+
+def result_array(shape, dtype):
+    nbytes = int(np.prod(shape)) * np.dtype(dtype).itemsize
+    if nbytes < PINNED_RESULT_MIN or not torch.cuda.is_available():
+        return np.empty(shape, dtype)
+    tdt = {np.dtype(np.float64): torch.float64, np.dtype(np.int64): torch.int64,
+           np.dtype(np.float32): torch.float32, np.dtype(np.int32): torch.int32}[np.dtype(dtype)]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()

@@ -755,7 +755,10 @@ class HostPool {
 
  private:
   HostPool() {
+    // 8 by default (measured on the 16-core B200 hosts: 8 > 6 > 12 > 16 for
+    // the C2 drop-in call — more threads contend with the driver's own)
     int n = (int)std::thread::hardware_concurrency();
+    n = n > 8 ? 8 : n;
     if (const char* v = getenv("NMQ_HOST_THREADS")) n = atoi(v);
     n = n < 1 ? 1 : (n > 32 ? 32 : n);
     for (int i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
@@ -835,6 +838,16 @@ struct BounceStage {
 BounceStage g_bounce[16];
 constexpr size_t kInRow = 8 + 4 + 4 + 12 + 12, kOutRow = 24 + 24 + 8, kDevOutRow = 12 + 12 + 4;
 
+bool is_pinned(const void* p) {
+  if (!p) return true;  // absent optional buffer
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int host_eval_bounce(const nm_material* m, int64_t n, const HostIo& io, int64_t chunk, void* stream) {
   BounceStage& B = g_bounce[m->device & 15];
   std::lock_guard<std::mutex> lock(B.mu);
@@ -876,11 +889,14 @@ int host_eval_bounce(const nm_material* m, int64_t n, const HostIo& io, int64_t 
     return q;
   };
   const int64_t nch = (n + ck - 1) / ck;
+  // page-locked result buffers take the DMA directly (no pinned slot, no host copy)
+  const bool direct_out = is_pinned(io.rgb) && is_pinned(io.albedo) && is_pinned(io.level);
   auto drain = [&](int64_t cj) -> int {  // results of chunk cj -> the caller's buffers
     const int s = (int)(cj % NMQ_HOST_SLOTS);
     const int64_t c0 = cj * ck, c = n - c0 < ck ? n - c0 : ck;
     cudaError_t err = cudaEventSynchronize(B.ev_out[s]);
     if (err != cudaSuccess) return cuda_fail(err, "nm_eval_host");
+    if (direct_out) return NM_OK;
     const Slot q = slot(s);
     std::vector<CopyJob> jobs{{(char*)io.rgb + 3 * c0 * ob, q.pin_out, (size_t)c * 3 * ob}};
     if (io.albedo) jobs.push_back({(char*)io.albedo + 3 * c0 * ob, q.pin_out + (size_t)ck * 3 * ob, (size_t)c * 3 * ob});
@@ -929,15 +945,17 @@ int host_eval_bounce(const nm_material* m, int64_t n, const HostIo& io, int64_t 
       out_src = q.dev_wide;
     }
     cudaEventRecord(B.ev_k[s], B.run);
-    // results -> pinned slot (DMA); same layout as the device slot: rgb | albedo | level
+    // results -> pinned slot (DMA; same layout as the device slot: rgb | albedo
+    // | level), or straight into page-locked result buffers
     cudaStreamWaitEvent(B.d2h, B.ev_k[s], 0);
-    cudaMemcpyAsync(q.pin_out, out_src, (size_t)c * 3 * ob, cudaMemcpyDeviceToHost, B.d2h);
+    char* o_rgb = direct_out ? (char*)io.rgb + 3 * c0 * ob : q.pin_out;
+    char* o_alb = direct_out ? (char*)io.albedo + 3 * c0 * ob : q.pin_out + (size_t)ck * 3 * ob;
+    char* o_lv = direct_out ? (char*)io.level + c0 * ob : q.pin_out + (size_t)ck * 6 * ob;
+    cudaMemcpyAsync(o_rgb, out_src, (size_t)c * 3 * ob, cudaMemcpyDeviceToHost, B.d2h);
     if (io.albedo)
-      cudaMemcpyAsync(q.pin_out + (size_t)ck * 3 * ob, out_src + (size_t)ck * 3 * ob, (size_t)c * 3 * ob,
-                      cudaMemcpyDeviceToHost, B.d2h);
+      cudaMemcpyAsync(o_alb, out_src + (size_t)ck * 3 * ob, (size_t)c * 3 * ob, cudaMemcpyDeviceToHost, B.d2h);
     if (io.level)
-      cudaMemcpyAsync(q.pin_out + (size_t)ck * 6 * ob, out_src + (size_t)ck * 6 * ob, (size_t)c * ob,
-                      cudaMemcpyDeviceToHost, B.d2h);
+      cudaMemcpyAsync(o_lv, out_src + (size_t)ck * 6 * ob, (size_t)c * ob, cudaMemcpyDeviceToHost, B.d2h);
     cudaEventRecord(B.ev_out[s], B.d2h);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "nm_eval_host");
     if (ci >= NMQ_HOST_SLOTS - 1) {

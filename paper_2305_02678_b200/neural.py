@@ -300,13 +300,13 @@ def _host_eval(mat, uv, level, wi, wo, u_rr, out, return_level):
     if out is None:
         # the reference's dtypes straight from the library (widened on the
         # device; pageable buffers through its pinned bounce pipeline)
-        f = np.empty((n, 3), np.float64)
-        alb = np.empty((n, 3), np.float64) if mat.cfg.albedo_head else None
-        lv = np.empty(n, np.int64) if return_level else None
+        f = _io.result_array((n, 3), np.float64)
+        alb = _io.result_array((n, 3), np.float64) if mat.cfg.albedo_head else None
+        lv = _io.result_array((n,), np.int64) if return_level else None
         _launch(lib.nm_eval_host_ref, h.ptr, n, h_uv.ctypes.data, h_lod.ctypes.data, lod_stride,
                 h_urr.ctypes.data, h_wi.ctypes.data, h_wo.ctypes.data, f.ctypes.data,
                 None if alb is None else alb.ctypes.data, None if lv is None else lv.ctypes.data,
-                0, _io.stream_ptr(h.device))
+                _io.REF_CHUNK, _io.stream_ptr(h.device))
         return f, alb, lv
     alb = np.empty((n, 3), np.float32) if mat.cfg.albedo_head else None
     lv = np.empty(n, np.int32) if return_level else None

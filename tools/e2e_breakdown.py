@@ -41,3 +41,13 @@ d = torch.empty(allin.size, device=dev)
 print("pageable H2D %d MB                  %.2f ms" % (allin.nbytes >> 20, t(lambda: d.copy_(torch.from_numpy(allin)))))
 out = np.empty(n * 4, np.float32)
 print("pageable D2H %d MB                  %.2f ms" % (out.nbytes >> 20, t(lambda: torch.from_numpy(out).copy_(d[: n * 4]))))
+# fresh result arrays every call (what the drop-in returns) vs reused ones
+def fresh():
+    f = np.empty((n, 3)); l = np.empty(n, np.int64)
+    _lib.check(lib.nm_eval_host_ref(h.ptr, n, hq["uv"].ctypes.data, hq["lod"].ctypes.data, 1, hq["u_rr"].ctypes.data,
+                                    hq["wi"].ctypes.data, hq["wo"].ctypes.data, f.ctypes.data, None, l.ctypes.data, 0,
+                                    _io.stream_ptr(dev)))
+print("nm_eval_host_ref, fresh outputs      %.2f ms" % t(fresh))
+def touch():
+    f = np.empty((n, 3)); l = np.empty(n, np.int64); f.fill(0); l.fill(0)
+print("np.empty + fill (first touch)        %.2f ms" % t(touch))
