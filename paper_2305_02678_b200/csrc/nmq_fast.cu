@@ -90,11 +90,13 @@ using namespace dev;
 
 constexpr float kLk = 0.98019802570343017578f;  // fp32(99/101)
 
-// Exact-rounding queue of one launch: CTA b owns entries [b * cap, (b+1) * cap)
-// of `ent` (kQueueWords x 16 B each: {row, x16[0..2]}, {x16[3..5], z16[0]},
-// {z16[1..3], wi.x}, {wi.y, wi.z, wo.x, wo.y}, {wo.z, frames to resolve, 0, 0},
-// {fast rgb (spp-mean launches only), 0}) and writes how
-// many it used to cnt[b] when it exits.
+// Exact-rounding queue of one launch: CTA b owns the region
+// ent[kQueueWords * b * cap, kQueueWords * (b+1) * cap), laid out by word
+// (structure of arrays: word w of entry k at region[w * cap + k], so a
+// warp's appends and the resolve's loads are coalesced): {row, x16[0..2]},
+// {x16[3..5], z16[0]}, {z16[1..3], wi.x}, {wi.y, wi.z, wo.x, wo.y},
+// {wo.z, frames to resolve, 0, 0}, {fast rgb (spp-mean launches only), 0};
+// it writes how many entries it used to cnt[b] when it exits.
 constexpr int kQueueWords = 6;
 struct ResolveQ {
   uint4* ent;
@@ -474,7 +476,8 @@ __device__ __forceinline__ void load_row8(const MatParams& mp, uint32_t off, int
 
 template <int BW, int BNH, bool RED = false>
 __device__ __forceinline__ void resolve_entries(const MatParams& mp, const QueryArgs& a, const uint4* ent,
-                                                uint32_t n, uint32_t first, uint32_t step, uint32_t tid) {
+                                                uint32_t n, uint32_t first, uint32_t step, uint32_t tid,
+                                                uint32_t cap) {
   const int lane = tid & 31;
   const bool seg_out = a.out_idx != nullptr;
   for (uint32_t b0 = first; b0 < n; b0 += step) {  // warp-uniform trip count
@@ -483,8 +486,9 @@ __device__ __forceinline__ void resolve_entries(const MatParams& mp, const Query
     int32_t row = 0;
     bool mism = false;
     if (i < n) {
-      const uint4* e = ent + kQueueWords * (size_t)i;
-      const uint4 e0 = __ldg(e), e1 = __ldg(e + 1), e2 = __ldg(e + 2), e3 = __ldg(e + 3), e4 = __ldg(e + 4);
+      const uint4* e = ent + i;
+      const uint4 e0 = __ldg(e), e1 = __ldg(e + cap), e2 = __ldg(e + 2 * cap), e3 = __ldg(e + 3 * cap),
+                  e4 = __ldg(e + 4 * cap);
       row = (int32_t)e0.x;
       zh[0] = e1.w; zh[1] = e2.x; zh[2] = e2.y; zh[3] = e2.z;
       const V3 wi = v3(__uint_as_float(e2.w), __uint_as_float(e3.x), __uint_as_float(e3.y));
@@ -576,7 +580,7 @@ __device__ __forceinline__ void resolve_entries(const MatParams& mp, const Query
         y[o] = p + mp.ob[o];
       }
       if (RED && lane == src) {  // replace the fast value's share of its pixel's mean
-        const uint4 e5 = __ldg(ent + kQueueWords * (size_t)i + 5);
+        const uint4 e5 = __ldg(ent + 5 * (size_t)cap + i);
         const float inv = __int_as_float((127 - a.spp_log2) << 23);
         float* o = a.img + 3 * ((int64_t)row >> a.spp_log2);
         atomicAdd(o, (brdf_output(y[0]) - __uint_as_float(e5.x)) * inv);
@@ -598,7 +602,7 @@ resolve_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ Que
                const __grid_constant__ FastConsts fc) {
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the fast kernel's queue and outputs
   resolve_entries<BW, BNH>(mp, a, fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap, fc.q.cnt[blockIdx.x],
-                           blockIdx.y * kResolveThreads, kResolveThreads * gridDim.y, threadIdx.x);
+                           blockIdx.y * kResolveThreads, kResolveThreads * gridDim.y, threadIdx.x, fc.q.cap);
 }
 
 template <int MODE, int BW, int BNH, int SW, int SNH, int G, int NS, bool TS, bool SEG, bool DBG = false,
@@ -860,13 +864,14 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
               if (flag) {
                 const uint32_t slot = wbase + __popc(wmask & lanemask_lt());
                 if constexpr (RED) S.qslot = (int32_t)slot;
-                uint4* e = fc.q.ent + kQueueWords * ((size_t)blockIdx.x * fc.q.cap + slot);
+                const size_t cap = fc.q.cap;
+                uint4* e = fc.q.ent + kQueueWords * (size_t)blockIdx.x * cap + slot;
                 e[0] = make_uint4((uint32_t)(seg_base + q_in), x[0], x[1], x[2]);
-                e[1] = make_uint4(x[3], x[4], x[5], S.zp[0]);
-                e[2] = make_uint4(S.zp[1], S.zp[2], S.zp[3], __float_as_uint(S.wi.x));
-                e[3] = make_uint4(__float_as_uint(S.wi.y), __float_as_uint(S.wi.z), __float_as_uint(wo.x),
-                                  __float_as_uint(wo.y));
-                e[4] = make_uint4(__float_as_uint(wo.z), (near_f0 ? 1u : 0u) | (near_f1 ? 2u : 0u), 0u, 0u);
+                e[cap] = make_uint4(x[3], x[4], x[5], S.zp[0]);
+                e[2 * cap] = make_uint4(S.zp[1], S.zp[2], S.zp[3], __float_as_uint(S.wi.x));
+                e[3 * cap] = make_uint4(__float_as_uint(S.wi.y), __float_as_uint(S.wi.z), __float_as_uint(wo.x),
+                                        __float_as_uint(wo.y));
+                e[4 * cap] = make_uint4(__float_as_uint(wo.z), (near_f0 ? 1u : 0u) | (near_f1 ? 2u : 0u), 0u, 0u);
               }
             }
             mma_issue<BW, 2, false, LW>(g, S.d0, S.a0, mp.fast_l1_off, 0, S.bar, refill);
@@ -905,7 +910,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
             const V3 f = S.up ? v3(brdf_output(y[0]), brdf_output(y[1]), brdf_output(y[2])) : v3(0.f, 0.f, 0.f);
             spp_accumulate(a.img, q_in, f, valid, a.spp_log2);
             if (S.qslot >= 0)
-              fc.q.ent[kQueueWords * ((size_t)blockIdx.x * fc.q.cap + S.qslot) + 5] =
+              fc.q.ent[kQueueWords * (size_t)blockIdx.x * fc.q.cap + 5 * (size_t)fc.q.cap + S.qslot] =
                   make_uint4(__float_as_uint(f.x), __float_as_uint(f.y), __float_as_uint(f.z), 0u);
           } else if (valid) {
             const int64_t q = seg_out ? (int64_t)__ldg(a.out_idx + seg_base + q_in) : q_in;
@@ -984,7 +989,7 @@ fast_kernel(const __grid_constant__ MatParams mp, const __grid_constant__ QueryA
       // every queued row's output is stored (the barrier above): the CTA
       // resolves its own rows while other SMs are still on their tiles
       resolve_entries<BW, BNH, RED>(mp, a, fc.q.ent + kQueueWords * (size_t)blockIdx.x * fc.q.cap, q_cnt, 0,
-                                    G * 128, tid);
+                                    G * 128, tid, fc.q.cap);
     } else if (tid == 0) {
       fc.q.cnt[blockIdx.x] = q_cnt;
     }
