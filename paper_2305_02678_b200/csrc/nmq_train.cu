@@ -19,7 +19,10 @@
 //    (out x in+1) partials in float64 and adds them to the result with
 //    float64 atomics.
 #include <cstdint>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <mutex>
 #include "nmq_device.cuh"
 #include "tc.cuh"
 #include "nmq_internal.h"
@@ -576,6 +579,185 @@ __global__ void __launch_bounds__(128) mlp_dparam_tc_kernel(const __grid_constan
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tb) : "memory");
 }
 
+// The same reduction fed by 2-D TMA: each layer's g (fo x B, float64) and
+// input (fi x B, fp32) caches are tensor maps; one box load per operand
+// brings a 32-row tile ([fo][32] / [fi][32], zero-filled past B) into a
+// 3-stage SMEM ring; all threads split the tile into the tf32 hi / lo operand
+// layout of one of two buffers while the tensor core runs on the other.
+// ~One CTA per SM over all layers.
+constexpr int kTmS = 3, kTmKT = 32, kTmThreads = 256;
+constexpr size_t kTmRawG = (size_t)kMaxW * kTmKT * 8, kTmRawX = (size_t)kMaxW * kTmKT * 4;
+constexpr size_t kTmSplit = (size_t)2 * (kTcM + kTcNMax) * kTmKT * 4;
+constexpr size_t kTmSmem = kTmS * (kTmRawG + kTmRawX) + 2 * kTmSplit + 128;  // + alignment slack
+
+struct DparamMaps {
+  CUtensorMap g[kMaxLayers], x[kMaxLayers];
+};
+
+__global__ void __launch_bounds__(kTmThreads) mlp_dparam_tma_kernel(const __grid_constant__ DparamArgs args,
+                                                                    const __grid_constant__ DparamMaps maps,
+                                                                    int64_t B, int64_t rows_per_cta) {
+  extern __shared__ uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)sm_raw + 127) & ~(uintptr_t)127);  // TMA: 128-B aligned
+  __shared__ uint64_t full[kTmS], mma_done[2];
+  __shared__ uint32_t tbase_sh;
+  const int l = blockIdx.y;
+  const int fi = args.fi[l], fo = args.fo[l], in_act = args.in_act[l];
+  double* __restrict__ dp = args.dp[l];
+  const int np = ((fi + 1) + 15) / 16 * 16;
+  const int t = threadIdx.x, warp = t / 32;
+  uint8_t* raw = sm;
+  uint8_t* split = sm + kTmS * (kTmRawG + kTmRawX);
+  auto raw_g = [&](int st) { return reinterpret_cast<double*>(raw + st * (kTmRawG + kTmRawX)); };
+  auto raw_x = [&](int st) { return reinterpret_cast<float*>(raw + st * (kTmRawG + kTmRawX) + kTmRawG); };
+  auto off = [](int rows, int row, int k) { return (k >> 2) * (rows * 4) + row * 4 + (k & 3); };
+  for (int i = t; i < (int)(2 * kTmSplit / 4); i += kTmThreads) reinterpret_cast<float*>(split)[i] = 0.f;
+  if (t == 0) {
+    for (int i = 0; i < kTmS; ++i) tc::mbar_init(&full[i], 1);
+    tc::mbar_init(&mma_done[0], 1);
+    tc::mbar_init(&mma_done[1], 1);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(tc::smem_u32(&tbase_sh))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc::fence_mbar_init();
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tb = tbase_sh;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = r0 + rows_per_cta < B ? r0 + rows_per_cta : B;
+  const int ntile = r1 > r0 ? (int)((r1 - r0 + kTmKT - 1) / kTmKT) : 0;
+  const uint32_t box_bytes = (uint32_t)kTmKT * (8u * fo + 4u * fi);
+  auto issue = [&](int j) {  // thread 0
+    const int st = j % kTmS;
+    const int32_t t0 = (int32_t)(r0 + (int64_t)j * kTmKT);
+    tc::mbar_arrive_expect_tx(&full[st], box_bytes);
+    tc::tma_load_2d(tc::smem_u32(raw_g(st)), &maps.g[l], t0, 0, &full[st]);
+    if (fi > 0) tc::tma_load_2d(tc::smem_u32(raw_x(st)), &maps.x[l], t0, 0, &full[st]);
+  };
+  if (t == 0)
+    for (int j = 0; j < kTmS && j < ntile; ++j) issue(j);
+  const uint32_t id = (tc::idesc_tf32(kTcM, 16) & ~(0x3Fu << 17)) | ((uint32_t)(np >> 3) << 17);
+  for (int j = 0; j < ntile; ++j) {
+    const int st = j % kTmS, b = j & 1;
+    const int64_t t0 = r0 + (int64_t)j * kTmKT;
+    const int rows = (int)(r1 - t0 < kTmKT ? r1 - t0 : kTmKT);  // rows past r1 (but < B) are another CTA's
+    tc::mbar_wait(&full[st], (uint32_t)(j / kTmS) & 1u);
+    if (j >= 2) tc::mbar_wait(&mma_done[b], (uint32_t)((j - 2) / 2) & 1u);  // buffer b's MMAs are done
+    tc::tc_fence_after();
+    float* a_hi = reinterpret_cast<float*>(split + b * kTmSplit);
+    float* a_lo = a_hi + kTcM * kTmKT;
+    float* b_hi = a_lo + kTcM * kTmKT;
+    float* b_lo = b_hi + kTcNMax * kTmKT;
+    const double* rg = raw_g(st);
+    const float* rx = raw_x(st);
+    // one item = one row x 4 consecutive k (the box is dense: [row][32])
+    for (int i = t; i < fo * (kTmKT / 4); i += kTmThreads) {
+      const int m = i / (kTmKT / 4), k0 = 4 * (i % (kTmKT / 4));
+      const double2 v01 = *reinterpret_cast<const double2*>(rg + m * kTmKT + k0);
+      const double2 v23 = *reinterpret_cast<const double2*>(rg + m * kTmKT + k0 + 2);
+      const double v[4] = {k0 < rows ? v01.x : 0.0, k0 + 1 < rows ? v01.y : 0.0, k0 + 2 < rows ? v23.x : 0.0,
+                           k0 + 3 < rows ? v23.y : 0.0};
+      float hi[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        hi[q] = __uint_as_float(__float_as_uint((float)v[q]) & 0xFFFFE000u);
+        lo[q] = (float)(v[q] - (double)hi[q]);
+      }
+      *reinterpret_cast<float4*>(a_hi + off(kTcM, m, k0)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(a_lo + off(kTcM, m, k0)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    for (int i = t; i < (fi + 1) * (kTmKT / 4); i += kTmThreads) {
+      const int n = i / (kTmKT / 4), k0 = 4 * (i % (kTmKT / 4));
+      float xv[4] = {1.f, 1.f, 1.f, 1.f};  // bias column: db = sum g
+      if (n < fi) {
+        const float4 r4 = *reinterpret_cast<const float4*>(rx + n * kTmKT + k0);
+        xv[0] = r4.x; xv[1] = r4.y; xv[2] = r4.z; xv[3] = r4.w;
+        if (in_act) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) xv[q] = xv[q] < 0.f ? xv[q] * kLeaky : xv[q];
+        }
+      }
+      float hi[4], lo[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) split_tf32(k0 + q < rows ? xv[q] : 0.f, hi[q], lo[q]);
+      *reinterpret_cast<float4*>(b_hi + off(kTcNMax, n, k0)) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      *reinterpret_cast<float4*>(b_lo + off(kTcNMax, n, k0)) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+    tc::fence_proxy_async_smem();  // the split tile -> the tensor core's async proxy
+    tc::tc_fence_before();
+    __syncthreads();               // raw stage st fully read; split buffer b complete
+    if (t == 0) {
+      tc::tc_fence_after();
+      const uint32_t lbo_a = kTcM * 16, lbo_b = kTcNMax * 16;
+#pragma unroll
+      for (int s2 = 0; s2 < kTmKT / 8; ++s2) {
+        const uint64_t ah = tc::smem_desc(tc::smem_u32(a_hi) + 2 * s2 * lbo_a, lbo_a, 128);
+        const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo) + 2 * s2 * lbo_a, lbo_a, 128);
+        const uint64_t bh = tc::smem_desc(tc::smem_u32(b_hi) + 2 * s2 * lbo_b, lbo_b, 128);
+        const uint64_t bl = tc::smem_desc(tc::smem_u32(b_lo) + 2 * s2 * lbo_b, lbo_b, 128);
+        tc::mma_ss_tf32(tb, ah, bh, id, (j > 0 || s2 > 0) ? 1u : 0u);
+        tc::mma_ss_tf32(tb, ah, bl, id, 1u);
+        tc::mma_ss_tf32(tb, al, bh, id, 1u);
+      }
+      tc::mma_commit(&mma_done[b]);
+      if (j + kTmS < ntile) issue(j + kTmS);  // refill the stage just consumed
+    }
+  }
+  if (ntile > 0) {
+    const int jl = ntile - 1;
+    tc::mbar_wait(&mma_done[jl & 1], (uint32_t)(jl / 2) & 1u);
+    tc::tc_fence_after();
+    if (warp < 4) {  // warps 0-3 own TMEM lanes 0-127 (D row = lane)
+      const uint32_t lane_addr = tb + ((uint32_t)(warp * 32) << 16);
+      for (int c0 = 0; c0 < np; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(lane_addr + (uint32_t)c0, r);
+        tc::tmem_ld_wait();
+        if (t < fo) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c0 + q <= fi) atomicAdd(dp + (int64_t)t * (fi + 1) + c0 + q, (double)__uint_as_float(r[q]));
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tb) : "memory");
+}
+
+PFN_cuTensorMapEncodeTiled encode_fn() {
+  static PFN_cuTensorMapEncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  });
+  return fn;
+}
+
+// [rows][B] row-major cache (row stride B elements) as a 2-D tensor map with
+// box [rows][kTmKT]
+bool encode_rows(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int esize, int64_t B, int rows) {
+  PFN_cuTensorMapEncodeTiled fn = encode_fn();
+  if (!fn || rows < 1 || rows > 256 || ((uintptr_t)base & 15u) || (B * esize) % 16) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)B, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)(B * esize)};
+  const cuuint32_t box[2] = {(cuuint32_t)kTmKT, (cuuint32_t)rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(map, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int max_width(const MlpView& v) {
   int w = 0;
   for (int l = 0; l < v.n_layers; ++l) {
@@ -698,6 +880,28 @@ cudaError_t launch_mlp_backward(const int32_t* fi, const int32_t* fo, const int3
 #ifndef NMQ_DPARAM_TC
 #define NMQ_DPARAM_TC 1  // dW / db on the tensor cores (3xTF32); 0: the float64 SIMT reduction
 #endif
+#ifndef NMQ_DPARAM_TMA
+#define NMQ_DPARAM_TMA 1
+#endif
+  if (NMQ_DPARAM_TC && NMQ_DPARAM_TMA && B < ((int64_t)1 << 31) &&
+      max_dynamic_smem((const void*)mlp_dparam_tma_kernel) >= (int)kTmSmem) {
+    static DparamMaps maps;  // host staging of the kernel parameter (copied at launch)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    bool ok = true;
+    for (int l = 0; l < n_layers && ok; ++l) {
+      ok = encode_rows(&maps.g[l], da.g[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 8, B, da.fo[l]) &&
+           encode_rows(&maps.x[l], da.in_src[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, da.fi[l]);
+    }
+    if (ok) {
+      int64_t rows = (B * n_layers + sm_count() - 1) / sm_count();  // ~one CTA per SM over all layers
+      rows = (rows + kTmKT - 1) / kTmKT * kTmKT;
+      const dim3 gt((unsigned)((B + rows - 1) / rows), (unsigned)n_layers);
+      mlp_dparam_tma_kernel<<<gt, kTmThreads, kTmSmem, s>>>(da, maps, B, rows);
+      ++g_launches;
+      return cudaGetLastError();
+    }
+  }
   if (NMQ_DPARAM_TC) {
     if (max_dynamic_smem((const void*)mlp_dparam_tc_kernel) < (int)kTcSmem) return cudaErrorNotSupported;
     const dim3 gtc((unsigned)((B + kTcRows - 1) / kTcRows), (unsigned)n_layers);

@@ -77,6 +77,16 @@ __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint3
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// 2-D tensor-map tile load (box at element coordinates {c0 inner, c1 outer});
+// out-of-range elements arrive as zeros and count toward the transaction
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const void* map, int32_t c0, int32_t c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 // per-thread 16-byte async gather global -> shared (LDGSTS)
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
