@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(128) mlp_dparam_tc_kernel(const __grid_constan
 // 3-stage SMEM ring; all threads split the tile into the tf32 hi / lo operand
 // layout of one of two buffers while the tensor core runs on the other.
 // ~One CTA per SM over all layers.
-constexpr int kTmS = 3, kTmKT = 32, kTmThreads = 256;
+constexpr int kTmS = 3, kTmKT = 32, kTmThreads = 256, kTmFlush = 8;  // flush D every 8 tiles = 256 rows
 constexpr size_t kTmRawG = (size_t)kMaxW * kTmKT * 8, kTmRawX = (size_t)kMaxW * kTmKT * 4;
 constexpr size_t kTmSplit = (size_t)2 * (kTcM + kTcNMax) * kTmKT * 4;
 constexpr size_t kTmSmem = kTmS * (kTmRawG + kTmRawX) + 2 * kTmSplit + 128;  // + alignment slack
@@ -641,6 +641,24 @@ __global__ void __launch_bounds__(kTmThreads) mlp_dparam_tma_kernel(const __grid
   if (t == 0)
     for (int j = 0; j < kTmS && j < ntile; ++j) issue(j);
   const uint32_t id = (tc::idesc_tf32(kTcM, 16) & ~(0x3Fu << 17)) | ((uint32_t)(np >> 3) << 17);
+  // D (fp32 in TMEM) is flushed into the float64 result every kTmFlush tiles,
+  // so fp32 accumulates over at most 256 rows whatever the batch
+  auto flush = [&]() {
+    if (warp < 4) {  // warps 0-3 own TMEM lanes 0-127 (D row = lane)
+      const uint32_t lane_addr = tb + ((uint32_t)(warp * 32) << 16);
+      for (int c0 = 0; c0 < np; c0 += 16) {
+        uint32_t r[16];
+        tc::tmem_ld16(lane_addr + (uint32_t)c0, r);
+        tc::tmem_ld_wait();
+        if (t < fo) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            if (c0 + q <= fi) atomicAdd(dp + (int64_t)t * (fi + 1) + c0 + q, (double)__uint_as_float(r[q]));
+        }
+      }
+    }
+  };
+  int acc_from = 0;  // first tile of the current fp32 accumulation
   for (int j = 0; j < ntile; ++j) {
     const int st = j % kTmS, b = j & 1;
     const int64_t t0 = r0 + (int64_t)j * kTmKT;
@@ -699,31 +717,27 @@ __global__ void __launch_bounds__(kTmThreads) mlp_dparam_tma_kernel(const __grid
         const uint64_t al = tc::smem_desc(tc::smem_u32(a_lo) + 2 * s2 * lbo_a, lbo_a, 128);
         const uint64_t bh = tc::smem_desc(tc::smem_u32(b_hi) + 2 * s2 * lbo_b, lbo_b, 128);
         const uint64_t bl = tc::smem_desc(tc::smem_u32(b_lo) + 2 * s2 * lbo_b, lbo_b, 128);
-        tc::mma_ss_tf32(tb, ah, bh, id, (j > 0 || s2 > 0) ? 1u : 0u);
+        tc::mma_ss_tf32(tb, ah, bh, id, (j > acc_from || s2 > 0) ? 1u : 0u);
         tc::mma_ss_tf32(tb, ah, bl, id, 1u);
         tc::mma_ss_tf32(tb, al, bh, id, 1u);
       }
       tc::mma_commit(&mma_done[b]);
       if (j + kTmS < ntile) issue(j + kTmS);  // refill the stage just consumed
     }
+    if ((j + 1) % kTmFlush == 0 && j + 1 < ntile) {
+      tc::mbar_wait(&mma_done[b], (uint32_t)(j / 2) & 1u);
+      tc::tc_fence_after();
+      flush();
+      tc::tc_fence_before();
+      __syncthreads();  // D read before the next tile's first MMA overwrites it
+      acc_from = j + 1;
+    }
   }
   if (ntile > 0) {
     const int jl = ntile - 1;
     tc::mbar_wait(&mma_done[jl & 1], (uint32_t)(jl / 2) & 1u);
     tc::tc_fence_after();
-    if (warp < 4) {  // warps 0-3 own TMEM lanes 0-127 (D row = lane)
-      const uint32_t lane_addr = tb + ((uint32_t)(warp * 32) << 16);
-      for (int c0 = 0; c0 < np; c0 += 16) {
-        uint32_t r[16];
-        tc::tmem_ld16(lane_addr + (uint32_t)c0, r);
-        tc::tmem_ld_wait();
-        if (t < fo) {
-#pragma unroll
-          for (int q = 0; q < 16; ++q)
-            if (c0 + q <= fi) atomicAdd(dp + (int64_t)t * (fi + 1) + c0 + q, (double)__uint_as_float(r[q]));
-        }
-      }
-    }
+    flush();
   }
   tc::tc_fence_before();
   __syncthreads();

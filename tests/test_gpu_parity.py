@@ -12,6 +12,7 @@ Tolerances (stated in DESIGN.md §5, from the north star / SURVEY §8c4):
 """
 
 import os
+import zlib
 
 import numpy as np
 import pytest
@@ -588,3 +589,27 @@ def test_eval_spp_mean_in_kernel(spp, kernel_path):
     with pytest.raises(ValueError):
         neural.eval_material_spp(mat, q["uv"][:100], q["lod"][:100], q["wi"][:100], q["wo"][:100],
                                  q["u_rr"][:100], 64)
+
+
+@pytest.mark.parametrize("B", [4096, 65536])
+def test_mlp_backward_tensor_core_path_vs_oracle(B):
+    """Batch sizes whose caches are 16-byte aligned take the TMA-fed
+    tensor-core dW/db (3xTF32, 2-D tensor maps; the golden batches above
+    are odd-sized and take the register-fed one): against the oracle's
+    numpy float64 reduction (pinned to the reference by
+    test_oracle_golden.py), within 1e-5 of each gradient's scale."""
+    from oracle import nm_oracle as O
+    g = load_golden("train")
+    for tag in ("brdf", "wide"):
+        net = _train_net(g, tag)
+        rng = np.random.default_rng(zlib.crc32(f"tc{tag}{B}".encode()))
+        x = rng.standard_normal((B, net.layers[0].w.shape[1])).astype(np.float32)
+        og = rng.standard_normal((B, net.layers[-1].w.shape[0])).astype(np.float32)
+        out, cache = net.forward_cached(x)
+        grads, _ = net.backward(cache, og)
+        onet = O.Net([(l.w, l.b, l.act) for l in net.layers])
+        ocache = O.forward_cached(onet, x)[1]
+        ograds, _ = O.backward(onet, ocache, og)
+        for (dw, db), (rw, rb) in zip(grads, ograds):
+            for a, w in ((dw, rw), (db, rb)):
+                assert np.abs(a - w).max() <= 1e-5 * np.abs(w).max(), (tag, B, np.abs(a - w).max() / np.abs(w).max())
