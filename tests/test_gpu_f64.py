@@ -103,3 +103,66 @@ def test_eval_material_float64_inputs_vs_reference_golden():
     u3 = np.random.default_rng(3).random((g["uv"].shape[0], 3))
     f3, _, _ = neural.query(mat, g["uv"], g["lod"], g["u_rr"], g["wi"], g["wo"], u3)
     check_rel(f3, g["f"], what="float64 query rgb")
+
+
+def test_decoder_inputs_one_frame_material():
+    """One learned frame: the decoder's direction inputs are [T.wi(3), T.wo(3)]
+    (x16 halves 0..5, the rest 0) — bit-exact against the oracle on float64
+    directions."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(87)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(n_frames=1), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 8, 8).levels)
+    n = 65536
+    z = rng.standard_normal((n, 8)).astype(np.float16).astype(np.float32)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    got = _decoder_inputs(mat, z, wi, wo)
+    ref = oracle_decoder_inputs(_oracle_from(mat), z, wi, wo)  # (n, 6)
+    assert np.array_equal(got[:, :6], ref) and not got[:, 6:].any()
+
+
+def test_float64_inputs_fp32_path_and_albedo():
+    """The reference's default fp16=False path and an albedo head on float64
+    inputs (nm_query_f64 on the precise material): levels bit-exact, colours
+    and albedo within the fp32 path's tolerance of the oracle."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(88)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(albedo_head=True), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 40, 24).levels)
+    n = 20000
+    uv = -1.0 + 3.0 * rng.random((n, 2))
+    lod = rng.random(n) * (mat.latent.n_levels - 1)
+    urr = rng.random(n)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    om = _oracle_from(mat)
+    for fp16 in (True, False):
+        f, alb, ch = neural.eval_material(mat, uv, lod, wi, wo, urr, fp16=fp16)
+        f_ref, alb_ref, ch_ref = O.eval_material(om, uv, lod, wi, wo, urr, fp16=fp16)
+        assert np.array_equal(ch, ch_ref)
+        tol = 1e-2 if fp16 else 1e-3
+        check_rel(f, f_ref, max_tol=tol, what=f"float64 inputs fp16={fp16} rgb")
+        check_rel(alb, alb_ref, max_tol=tol, what=f"float64 inputs fp16={fp16} albedo")
+
+
+def test_entry_points_without_float64_reject_inexact_input():
+    """spp and multi-material entry points have no float64 variant: they
+    raise instead of silently narrowing (the reference computes in float64)."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from paper_2305_02678_b200.latent import LatentPyramid
+    rng = np.random.default_rng(89)
+    mat = neural.NeuralMaterial.create(neural.NeuralMaterialConfig(), rng)
+    mat.latent = LatentPyramid(O.random_pyramid(rng, 16, 16).levels)
+    n = 256
+    uv = rng.random((n, 2))
+    lod = np.full(n, 1.0)
+    urr = rng.random(n)
+    wi, wo = O.draw_direction_pairs(rng, n)
+    with pytest.raises(ValueError):
+        neural.eval_material_spp(mat, uv, lod, wi, wo, urr, 16)
+    with pytest.raises(ValueError):
+        neural.eval_material_multi([mat, mat], np.zeros(n, np.int32), uv, lod, wi, wo, urr)
