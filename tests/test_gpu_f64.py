@@ -166,3 +166,22 @@ def test_entry_points_without_float64_reject_inexact_input():
         neural.eval_material_spp(mat, uv, lod, wi, wo, urr, 16)
     with pytest.raises(ValueError):
         neural.eval_material_multi([mat, mat], np.zeros(n, np.int32), uv, lod, wi, wo, urr)
+
+
+def test_full_query_float64_inputs_sampled_directions():
+    """The full query on float64 inputs: levels bit-exact, rgb strict, every
+    sampled direction within 1e-3 of the oracle's outside the lobe-pick band
+    (the reference samples from its float64 conditioning direction; the
+    sampler decoder sees it narrowed to fp32 as the reference's does)."""
+    from oracle import nm_oracle as O
+    from paper_2305_02678_b200 import neural
+    from test_gpu_parity import check_dirs
+    g = load_golden("f64_inputs")
+    mat = our_material(g)
+    om = _oracle_from(mat)
+    u3 = np.random.default_rng(5).random((g["uv"].shape[0], 3))
+    f, ws, pdf, ch = neural.query(mat, g["uv"], g["lod"], g["u_rr"], g["wi"], g["wo"], u3, return_level=True)
+    f_ref, ws_ref, pdf_ref, p_ref, ch_ref = O.full_query(om, g["uv"], g["lod"], g["u_rr"], g["wi"], g["wo"], u3)
+    assert np.array_equal(ch, ch_ref)
+    check_rel(f, f_ref, what="float64 full query rgb")
+    check_dirs(ws, ws_ref, u3, p_ref, g["wi"])
